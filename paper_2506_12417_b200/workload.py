@@ -1,0 +1,92 @@
+"""Synthetic routing workloads (router stand-in inputs for tests and the bench).
+
+The reference's router stand-in is ``skew_probabilities`` + per-source
+multinomial counts (moesim/workload.py:138-180).  That encodes top-k only as
+larger row sums (pkg/README.md:160-163).  The B200 block routes real tokens, so
+this module adds what SURVEY.md §8(d) specifies for measurement:
+
+* Zipf expert popularity p_i ∝ (i+1)^-s (hot experts are the low ids, so a
+  blocked placement piles them on GPU 0, mirroring PAPER.md:450-454);
+* top-k *without replacement* via Gumbel-top-k on log p (count matrices for
+  scheduler-only runs);
+* router-bias construction (bias_e = log p_e) so the real router kernel
+  produces Zipf-skewed routing from x ~ N(0,1), Wg ~ N(0, 1/d).
+
+All draws use ``numpy.random.Generator(PCG64(seed))``; generated inputs are
+serialised into fixtures where cross-version stability matters.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def skew_probabilities(alpha: float, skewed, num_experts: int) -> np.ndarray:
+    """Same contract as moesim/workload.py:138-164 (hot-set mass alpha)."""
+    if not 0.0 <= alpha <= 1.0:
+        raise ValueError(f"alpha must be in [0, 1], got {alpha}")
+    skewed = [int(e) for e in skewed]
+    if len(set(skewed)) != len(skewed):
+        raise ValueError("skewed expert indices must be distinct")
+    if any(not 0 <= e < num_experts for e in skewed):
+        raise ValueError("skewed expert index out of range")
+    if not skewed and alpha > 0:
+        raise ValueError("skewed experts required when alpha > 0")
+    probs = np.empty(num_experts, dtype=np.float64)
+    if alpha == 0.0 or len(skewed) == num_experts:
+        probs.fill(1.0 / num_experts)
+        return probs
+    probs.fill((1.0 - alpha) / (num_experts - len(skewed)))
+    probs[skewed] = alpha / len(skewed)
+    return probs
+
+
+def zipf_probabilities(num_experts: int, s: float) -> np.ndarray:
+    """p_i ∝ (i+1)^-s; s = 0 is uniform."""
+    if num_experts < 1:
+        raise ValueError("num_experts must be >= 1")
+    if s < 0:
+        raise ValueError("zipf exponent must be >= 0")
+    w = np.arange(1, num_experts + 1, dtype=np.float64) ** (-float(s))
+    return w / w.sum()
+
+
+def gumbel_topk_assignments(probs, num_tokens: int, k: int, rng: np.random.Generator) -> np.ndarray:
+    """[T, k] expert ids, top-k without replacement by Gumbel-top-k on log p."""
+    probs = np.asarray(probs, dtype=np.float64)
+    E = probs.size
+    if not 1 <= k <= E:
+        raise ValueError("k must be in [1, E]")
+    logp = np.log(np.maximum(probs, 1e-300))
+    out = np.empty((num_tokens, k), dtype=np.int32)
+    chunk = 4096
+    for s in range(0, num_tokens, chunk):
+        n = min(chunk, num_tokens - s)
+        keys = logp[None, :] + rng.gumbel(size=(n, E))
+        part = np.argpartition(-keys, k - 1, axis=1)[:, :k]
+        out[s : s + n] = part
+    return out
+
+
+def zipf_routing_matrix(num_gpus: int, tokens_per_gpu: int, num_experts: int, k: int, s: float,
+                        seed: int, permute_experts: bool = False) -> np.ndarray:
+    """m_all[G, E]: per-source-GPU histogram of Zipf top-k-without-replacement
+    routing.  ``permute_experts`` applies a seeded random
+    id permutation so the hot experts are spread over homes."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    p = zipf_probabilities(num_experts, s)
+    if permute_experts:
+        p = p[rng.permutation(num_experts)]
+    m = np.zeros((num_gpus, num_experts), dtype=np.int64)
+    for g in range(num_gpus):
+        a = gumbel_topk_assignments(p, tokens_per_gpu, k, rng)
+        m[g] = np.bincount(a.reshape(-1), minlength=num_experts)
+    return m
+
+
+def router_bias(num_experts: int, s: float, seed: int | None = None) -> np.ndarray:
+    """bias_e = log p_e (Zipf), optionally id-permuted with ``seed``."""
+    p = zipf_probabilities(num_experts, s)
+    if seed is not None:
+        p = p[np.random.Generator(np.random.PCG64(seed)).permutation(num_experts)]
+    return np.log(p).astype(np.float32)
