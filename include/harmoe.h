@@ -1,0 +1,155 @@
+/*
+ * harmoe.h - C ABI of the B200-native HarMoEny expert-parallel MoE block.
+ *
+ * libharmoe.so (paper_2506_12417_b200/libharmoe.so) exports exactly these
+ * entry points.  Plain pointers and sizes only: every pointer argument is a
+ * device pointer unless stated otherwise; `stream` is a cudaStream_t passed as
+ * void*.  Every call is stream-ordered, never allocates, never synchronises the
+ * host, and returns HM_OK (0) or an error code; hm_last_error() gives the
+ * message.  There is no CPU fallback.
+ *
+ * Each entry point replaces one phase of the reference's MoE-layer path
+ * (reference = /root/reference, moesim + PAPER.md Alg. 1):
+ *
+ *   hm_router_topk      Alg.1 step 1 "router"; the reference
+ *                       stand-in is workload.sample_routing (workload.py:167-180)
+ *   hm_hist_scan        per-GPU token->expert histogram = RoutingMatrix row
+ *                       (core.py:89-96) = metadata m_expert
+ *   hm_schedule /       initial_assign + rebalance (policies.py:109-171) as
+ *   hm_rebalance        dispatched by engine.build_schedule (engine.py:287-299)
+ *   hm_dispatch_layout  byte flows of the scatter (engine._exchange_byte_vectors,
+ *                       engine.py:278-284) + per-GPU execution order of
+ *                       plan_gpu_execution (engine.py:233-234)
+ *   hm_permute          Alg.1 step 4 scatter
+ *   hm_grouped_gemm     Alg.1 step 5 expert compute (cost
+ *                       model engine.py:128-132)
+ *   hm_fetch_expert     async expert fetch (engine.py:253-265)
+ *   hm_combine          Alg.1 step 6 gather + reconstruct
+ */
+#ifndef HARMOE_H_
+#define HARMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HM_API __attribute__((visibility("default")))
+#else
+#define HM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define HM_OK 0
+#define HM_EINVAL 1  /* invalid argument (the Python layer raises ValueError) */
+#define HM_ECUDA 2   /* CUDA runtime / driver error */
+#define HM_ENCCL 3   /* reserved: collective error (collectives run in torch.distributed) */
+#define HM_ENOSPC 4  /* a buffer capacity is too small */
+
+/* grouped-GEMM epilogues */
+#define HM_EPI_STORE 0  /* out = bf16(acc) */
+#define HM_EPI_RELU 1   /* out = bf16(relu(acc)) (Switch FFN1) */
+#define HM_EPI_SWIGLU 2 /* out = bf16(silu(gate) * up), W13 block-interleaved by 128 rows */
+
+/* dispatch layouts */
+#define HM_LAYOUT_LOCAL 0 /* all G ranks on this device: buffer [dest][expert][source][rank] */
+#define HM_LAYOUT_EP 1    /* this process is rank `me`: send buffer [dest][expert][rank], */
+                          /* receive buffer [source][expert][rank] (NCCL all_to_all chunks) */
+
+HM_API int hm_version(void);
+HM_API const char* hm_last_error(void);
+HM_API int hm_num_sms(void);
+HM_API int hm_gemm_tile_m(void); /* rows per GEMM tile (128) */
+
+/*
+ * Router (K1) + histogram/rank pass (K2), fused: one CTA per 128-token tile.
+ *   x        [n_ranks*tokens_per_rank, d] bf16      token activations
+ *   wg       [E_pad, d] bf16                         gate weights (nn.Linear layout),
+ *                                                    E_pad = E rounded up to 16 (rows >= E are ignored)
+ *   bias     [E] fp32 or NULL                        additive logit bias
+ *   topk_idx [T, k] int32, topk_w [T, k] fp32       top-k over fp32 logits, lowest index wins ties;
+ *                                                    weights = softmax probs (renormalised over k if set)
+ *   tile_hist[n_ranks*tiles_per_rank, E] int32       per-tile expert histogram
+ *   lrank    [T, k] int32                            rank of each assignment among same-expert
+ *                                                    assignments of its tile, (token, slot) order
+ * tiles_per_rank = ceil(tokens_per_rank / 128).  Requires d % 64 == 0, 1 <= k <= 16, k <= E <= 256.
+ */
+HM_API int hm_router_topk(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d,
+                   int E, int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist,
+                   int32_t* lrank, void* stream);
+
+/* Per-rank histogram m_expert[n_ranks, E] and per-tile exclusive offsets tile_off (same shape as
+ * tile_hist).  Row r of `hist` is RoutingMatrix.counts[r] (core.py:93-95). */
+HM_API int hm_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_rank, int E, int32_t* hist,
+                 int32_t* tile_off, void* stream);
+
+/*
+ * Scheduler (K3): S[g,e,home[e]] = m_all[g,e] (policies.py:109-117), then, when `rebalance`,
+ * HarMoEny's greedy token rebalancing (policies.py:120-141, Alg. 2) with threshold q, bit-exact
+ * against the reference (lowest-index ties).  Replicated on every rank; no communication.
+ *   m_all [G,E] int32, home [E] int32 -> S [G,E,G] int32, iters [1] int32, loads [G] int32 (or NULL).
+ * q < 1 -> HM_EINVAL ("token threshold q must be >= 1").  Requires G <= 32.
+ */
+HM_API int hm_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int q, int rebalance, int32_t* S,
+                int32_t* iters, int32_t* loads, void* stream);
+
+/*
+ * In-place rebalance of an arbitrary schedule S [G,E,G] int32 (policies.py:144-171, the
+ * drop-in for moesim.rebalance / rebalance_with_stats).  Same tie and stop rules as hm_schedule.
+ */
+HM_API int hm_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* loads, void* stream);
+
+/*
+ * Token placement for dispatch and the grouped GEMM's work list.
+ *   slot_base [G,E,G] int32: buffer row of the first token of bucket (g,e,d)
+ *   segs [cap,4] int32 {row_start, nrows, wslot, expert} in plan order, n_seg [1], mtile_prefix [cap+1]
+ *   fetch [E] int32: experts this rank must fetch (non-resident with work), plan order; n_fetch [1]
+ * LOCAL: segments are (dest, expert) over the whole [G] buffer, wslot = expert.
+ * EP:    segments are (expert, source) of rank `me`'s receive buffer; wslot = index of the expert
+ *        among me's home experts (ascending id), fetched experts get slots n_home + fetch ordinal.
+ * cap >= G*E.
+ */
+HM_API int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
+                       int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
+                       void* stream);
+
+/*
+ * Scatter (K4): copy token rows to their scheduled buffer rows (one read of x, k 128-bit-vector
+ * writes).  Token t's source rank is src_rank_base + t / tokens_per_rank; its r-th assignment to
+ * expert e goes to the first dest d with cumsum_d S[src,e,d] > r (split-bucket contract).
+ *   out [rows, d] bf16, pos [T, k] int32 (row index of each assignment in `out`).
+ */
+HM_API int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+               const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base,
+               int G, int E, int k, int d, void* out, int32_t* pos, void* stream);
+
+/*
+ * Grouped expert GEMM (K5), tcgen05/TMEM/TMA: for every segment, out[rows] = epi(A[rows] W[wslot]^T).
+ *   A [a_rows, K] bf16; W [w_rows, K] bf16 with w_rows = slots*N; out [a_rows, N] (or N/2 for SWIGLU).
+ *   slot_ready [slots] int32 or NULL: tiles of slot s >= ready_from_slot wait for slot_ready[s] >= epoch.
+ * Requires N % 256 == 0, K % 64 == 0.
+ */
+HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
+                    const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out,
+                    const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream);
+
+/*
+ * Async expert fetch (K6): copy `bytes` from src (peer HBM through UVA/NVLink, or pinned host
+ * memory) into dst on `stream` (the dedicated fetch stream), then publish *ready_flag = epoch.
+ */
+HM_API int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_flag, int epoch, void* stream);
+
+/*
+ * Combine (K7): y[t] = sum_j w[t,j] * Y[pos[t,j]] in fp32, slots in order j = 0..k-1, bf16 out.
+ */
+HM_API int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HARMOE_H_ */

@@ -1,0 +1,190 @@
+"""The HarMoEny MoE block on B200: Alg. 1 as a chain of
+hand-written sm_100a kernels behind the C ABI.
+
+    forward(x):                                   kernels (csrc/)
+      1 router: logits, top-k, weights            hm_router_topk      (K1, tcgen05)
+        per-tile histogram + (token,slot) ranks   (fused K2)
+      2 metadata exchange m_all                   hm_hist_scan + all_gather (EP)
+      3 schedule S = rebalance(initial_assign)    hm_schedule         (K3, bit-exact)
+      4 scatter tokens                            hm_dispatch_layout + hm_permute (K4) + all_to_all (EP)
+      5 experts (+ async fetch)                   hm_grouped_gemm x2  (K5, tcgen05) + hm_fetch_expert (K6)
+      6 gather + reconstruct                      all_to_all (EP) + hm_combine (K7)
+
+Two placements of the G ranks:
+
+* LOCAL ("logical ranks"): one process owns the whole batch and simulates G
+  GPUs on one device (BASELINE config 1 "simulated 4 GPUs").  The schedule is
+  the real HarMoEny schedule of the G token shards; buffer rows are laid out
+  [dest][expert][source], every expert's weights are local, no collectives.
+* EP (expert parallel): one process per GPU, G = world size; see ep.py.
+
+The paper's integration API (MoEConfig + replace_moe_layer)
+is kept: ``MoEConfig(rank, world_size, scheduling_policy, expert_cache_size,
+eq_tokens, d_model, num_experts, ...)``; eq_tokens is the threshold q
+(SPEC.md:529).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+from .policies import PlacementKind, SchedulingPolicy, blocked_placement, round_robin_placement
+
+
+@dataclass
+class MoEConfig:
+    rank: int = 0
+    world_size: int = 1
+    scheduling_policy: str = "harmony"  # "harmony"/"rebalance" or "round_robin" (no rebalancing)
+    expert_cache_size: int = 0  # fetch slots per GPU (0 = one per fetched expert)
+    eq_tokens: int = 32  # token threshold q (Eq. 4)
+    d_model: int = 2048
+    num_experts: int = 128
+    d_ff: int = 768
+    top_k: int = 8
+    activation: str = "swiglu"  # "swiglu" (Qwen/Mixtral) or "relu" (Switch)
+    renormalize: bool | None = None  # default: True for k > 1, False for top-1
+    placement: str = "round_robin"
+    logical_ranks: int = 1  # LOCAL mode: number of simulated GPUs (world_size must be 1)
+    fetch_source: str = "peer"  # EP mode: "peer" (NVLink) or "host" (pinned host memory)
+
+    def __post_init__(self):
+        if self.eq_tokens < 1:
+            raise ValueError("token_threshold_q must be >= 1")
+        if self.activation not in ("swiglu", "relu"):
+            raise ValueError("activation must be 'swiglu' or 'relu'")
+        if self.renormalize is None:
+            self.renormalize = self.top_k > 1
+        if self.world_size > 1 and self.logical_ranks not in (1, self.world_size):
+            raise ValueError("logical ranks are a single-process mode (world_size == 1)")
+
+    @property
+    def rebalance(self) -> bool:
+        return str(self.scheduling_policy).lower() in ("harmony", "harmoeny", "rebalance", SchedulingPolicy.REBALANCE)
+
+    @property
+    def num_ranks(self) -> int:
+        return self.world_size if self.world_size > 1 else self.logical_ranks
+
+
+def pack_w13(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """[E,f,d] gate + [E,f,d] up -> [E*2f, d], block-interleaved by 128 rows (the
+    SwiGLU epilogue of hm_grouped_gemm reads gate rows [0,128) and up rows
+    [128,256) of each 256-row block)."""
+    E, f, d = w_gate.shape
+    if f % 128 != 0:
+        raise ValueError("SwiGLU path needs d_ff % 128 == 0")
+    g = w_gate.reshape(E, f // 128, 128, d)
+    u = w_up.reshape(E, f // 128, 128, d)
+    return torch.stack([g, u], dim=2).reshape(E * 2 * f, d).contiguous()
+
+
+def placement_home(cfg: MoEConfig):
+    G = cfg.num_ranks
+    kind = PlacementKind(cfg.placement)
+    p = blocked_placement(cfg.num_experts, G) if kind is PlacementKind.BLOCKED else round_robin_placement(
+        cfg.num_experts, G)
+    return np.asarray(p.home, dtype=np.int32)
+
+
+@dataclass
+class BlockStats:
+    """Device tensors describing the last forward (read them after a sync)."""
+
+    m_all: torch.Tensor | None = None
+    schedule: torch.Tensor | None = None
+    iters: torch.Tensor | None = None
+    loads: torch.Tensor | None = None
+    extras: dict = field(default_factory=dict)
+
+    def load_imbalance(self) -> float:
+        loads = self.loads.double()
+        return float(loads.max() / loads.mean()) if float(loads.mean()) > 0 else 1.0
+
+
+class HarMoEnyBlock:
+    """One MoE layer: router + experts, weights resident in HBM (bf16).
+
+    LOCAL mode only here (world_size == 1); multi-process expert parallelism
+    lives in :class:`paper_2506_12417_b200.ep.EPHarMoEnyBlock`.
+    """
+
+    def __init__(self, cfg: MoEConfig, wg: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor,
+                 w3: torch.Tensor | None = None, bias: torch.Tensor | None = None, device=None):
+        if cfg.world_size != 1:
+            raise ValueError("HarMoEnyBlock is the single-process block; use ep.EPHarMoEnyBlock for world_size > 1")
+        device = torch.device(device if device is not None else "cuda")
+        if device.type != "cuda":
+            raise ValueError("HarMoEnyBlock runs on CUDA only (no CPU fallback)")
+        self.cfg = cfg
+        E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
+        bf = torch.bfloat16
+        wgp = torch.zeros((ops.e_pad(E), d), dtype=bf, device=device)
+        wgp[:E] = wg.to(device=device, dtype=bf)
+        self.wg = wgp
+        self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
+        if cfg.activation == "swiglu":
+            if w3 is None:
+                raise ValueError("SwiGLU experts need w3 (up projection)")
+            self.w_in = pack_w13(w1.to(device=device, dtype=bf), w3.to(device=device, dtype=bf))
+            self.n_in = 2 * f
+            self.epi_in = ops.HM_EPI_SWIGLU
+        else:
+            self.w_in = w1.to(device=device, dtype=bf).reshape(E * f, d).contiguous()
+            self.n_in = f
+            self.epi_in = ops.HM_EPI_RELU
+        self.w_out = w2.to(device=device, dtype=bf).reshape(E * d, f).contiguous()
+        self.home_np = placement_home(cfg)
+        self.home = torch.from_numpy(self.home_np).to(device)
+        self.device = device
+        self.stats = BlockStats()
+
+    @classmethod
+    def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s: float | None = None, std: float = 0.02):
+        """Random-init weights of the named architecture (no checkpoints offline):
+        experts ~ N(0, std), Wg ~ N(0, 1/d), optional Zipf router bias log p."""
+        from .workload import router_bias
+
+        g = torch.Generator(device=device).manual_seed(seed)
+        E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
+        kw = dict(device=device, dtype=torch.float32, generator=g)
+        wg = (torch.randn((E, d), **kw) * (1.0 / d) ** 0.5).to(torch.bfloat16)
+        w1 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16)
+        w2 = (torch.randn((E, d, f), **kw) * std).to(torch.bfloat16)
+        w3 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16) if cfg.activation == "swiglu" else None
+        bias = None if zipf_s is None else torch.from_numpy(router_bias(E, zipf_s)).to(device)
+        return cls(cfg, wg, w1, w2, w3, bias, device=device)
+
+    # ------------------------------------------------------------------------------------
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        cfg = self.cfg
+        if x.dim() != 2 or x.shape[1] != cfg.d_model:
+            raise ValueError(f"x must be [T, {cfg.d_model}]")
+        if x.dtype != torch.bfloat16:
+            raise ValueError("x must be bf16")
+        G = cfg.num_ranks
+        T = x.shape[0]
+        if T % G != 0:
+            raise ValueError("token count must divide evenly over the logical ranks")
+        Tg = T // G
+        k = cfg.top_k
+        tiles_per_rank = (Tg + ops.TILE_M - 1) // ops.TILE_M
+        x = x.contiguous()
+        idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, G, Tg, k, cfg.renormalize, stream=stream)
+        m_all, tile_off = ops.hist_scan(tile_hist, G, tiles_per_rank, stream=stream)
+        S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=stream)
+        lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_LOCAL, stream=stream)
+        xs, pos = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, G, Tg, 0, T * k, stream=stream)
+        h = ops.grouped_gemm(xs, self.w_in, self.n_in, lay, self.epi_in, stream=stream)
+        ys = ops.grouped_gemm(h, self.w_out, cfg.d_model, lay, ops.HM_EPI_STORE, stream=stream)
+        y = ops.combine(ys, pos, w, stream=stream)
+        self.stats = BlockStats(m_all=m_all, schedule=S, iters=iters, loads=loads,
+                                extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay, lrank=lrank,
+                                            tile_off=tile_off))
+        return y
+
+    __call__ = forward

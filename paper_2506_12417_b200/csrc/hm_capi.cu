@@ -1,0 +1,171 @@
+// C ABI of libharmoe.so (declared in include/harmoe.h) + host utilities:
+// error state, SM count, TMA descriptor encoding and the K6 fetch primitive.
+#include <cudaTypedefs.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "hm_common.cuh"
+#include "hm_internal.h"
+
+namespace hm {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return HM_OK;
+}
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+static std::once_flag g_driver_once;
+
+static void load_driver_entry_points() {
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fn);
+}
+
+int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                      uint32_t box_cols) {
+  std::call_once(g_driver_once, load_driver_entry_points);
+  if (g_encode == nullptr) return set_error(HM_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return set_error(HM_EINVAL, "TMA base must be 16-byte aligned");
+  if ((cols * 2) % 16 != 0) return set_error(HM_EINVAL, "TMA row pitch must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(HM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return HM_OK;
+}
+
+int launch_hist_scan(const int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
+int launch_schedule(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, cudaStream_t);
+int launch_rebalance(int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
+int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
+                  int32_t*, int32_t*, cudaStream_t);
+int launch_permute(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int,
+                   int, int, int, int, int, int, void*, int32_t*, cudaStream_t);
+int launch_combine(const void*, const int32_t*, const float*, int, int, int, void*, cudaStream_t);
+
+__global__ void publish_flag_kernel(int32_t* flag, int epoch) {
+  __threadfence_system();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+
+}  // namespace hm
+
+using namespace hm;
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int hm_version(void) { return 1; }
+
+const char* hm_last_error(void) { return hm::g_err; }
+
+int hm_num_sms(void) { return num_sms(); }
+
+int hm_gemm_tile_m(void) { return 128; }
+
+int hm_router_topk(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
+                   int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,
+                   void* stream) {
+  return launch_router(x, wg, bias, n_ranks, tokens_per_rank, d, E, k, renormalize, topk_idx, topk_w, tile_hist,
+                       lrank, as_stream(stream));
+}
+
+int hm_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_rank, int E, int32_t* hist, int32_t* tile_off,
+                 void* stream) {
+  return launch_hist_scan(tile_hist, n_ranks, tiles_per_rank, E, hist, tile_off, as_stream(stream));
+}
+
+int hm_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int q, int rebalance, int32_t* S,
+                int32_t* iters, int32_t* loads, void* stream) {
+  return launch_schedule(m_all, home, G, E, q, rebalance, S, iters, loads, as_stream(stream));
+}
+
+int hm_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* loads, void* stream) {
+  return launch_rebalance(S, G, E, q, iters, loads, as_stream(stream));
+}
+
+int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
+                       int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
+                       void* stream) {
+  return launch_layout(S, home, G, E, mode, me, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch,
+                       as_stream(stream));
+}
+
+int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+               const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base, int G,
+               int E, int k, int d, void* out, int32_t* pos, void* stream) {
+  return launch_permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks, tokens_per_rank, src_rank_base, G, E, k,
+                        d, out, pos, as_stream(stream));
+}
+
+int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
+                    const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out,
+                    const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream) {
+  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, slot_ready,
+                             ready_from_slot, epoch, as_stream(stream));
+}
+
+int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_flag, int epoch, void* stream) {
+  std::call_once(g_driver_once, load_driver_entry_points);
+  cudaStream_t s = as_stream(stream);
+  if (bytes > 0) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
+    if (e != cudaSuccess) return set_error(HM_ECUDA, "fetch_expert memcpy: %s", cudaGetErrorString(e));
+  }
+  if (ready_flag == nullptr) return HM_OK;
+  if (g_write32 != nullptr) {
+    const CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(ready_flag),
+                                 (cuuint32_t)epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) return set_error(HM_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    return HM_OK;
+  }
+  publish_flag_kernel<<<1, 1, 0, s>>>(ready_flag, epoch);
+  return check_launch("fetch_expert flag");
+}
+
+int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y, void* stream) {
+  return launch_combine(Y, pos, topk_w, T, k, d, y, as_stream(stream));
+}
+
+}  // extern "C"

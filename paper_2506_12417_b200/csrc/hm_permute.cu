@@ -1,0 +1,154 @@
+// K4 (scatter/permute) and K7 (combine) - HBM-bound row movers.
+//
+// permute_kernel: Alg.1 step 4.  One warp per token: the
+// token row is read ONCE into registers with 128-bit loads and written to each
+// of its k scheduled rows with 128-bit stores.  The destination of the r-th
+// assignment of (source g, expert e) is the first d with cumsum_d S[g,e,d] > r
+// (split-bucket contract; the reference leaves token
+// identity out).  r = tile_off + lrank comes from the router's
+// deterministic rank pass, so the scatter is bit-reproducible.
+//
+// combine_kernel: Alg.1 step 6 + reconstruct.
+// y[t] = sum_j w[t,j] * Y[pos[t,j]], fp32 multiply and add with explicit
+// round-to-nearest (no FMA contraction) in slot order j = 0..k-1, bf16 output;
+// the CPU oracle performs the identical float32 operation sequence.
+#include "hm_common.cuh"
+#include "hm_internal.h"
+
+namespace hm {
+
+constexpr int kPermWarps = 8;
+
+template <int VEC>
+__global__ void __launch_bounds__(kPermWarps * 32)
+    permute_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ topk_idx,
+                   const int32_t* __restrict__ lrank, const int32_t* __restrict__ tile_off,
+                   const int32_t* __restrict__ S, const int32_t* __restrict__ slot_base, int64_t T,
+                   int tokens_per_rank, int tiles_per_rank, int src_rank_base, int G, int E, int k, int n16,
+                   uint4* __restrict__ out, int32_t* __restrict__ pos) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int lr = (int)(t / tokens_per_rank);
+  const int tin = (int)(t - (int64_t)lr * tokens_per_rank);
+  const int g = src_rank_base + lr;
+  const int tile = lr * tiles_per_rank + tin / 128;
+
+  uint4 v[VEC];
+  const uint4* src = x + t * n16;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = i * 32 + lane;
+    if (c < n16) v[i] = ld_global_nc_v4(src + c);
+  }
+  for (int j = 0; j < k; ++j) {
+    const int e = __ldg(topk_idx + t * k + j);
+    const int r = __ldg(tile_off + (int64_t)tile * E + e) + __ldg(lrank + t * k + j);
+    const int32_t* srow = S + ((int64_t)g * E + e) * G;
+    int c = 0, d = 0;
+    for (; d < G - 1; ++d) {
+      const int s = __ldg(srow + d);
+      if (c + s > r) break;
+      c += s;
+    }
+    const int64_t p = (int64_t)__ldg(slot_base + ((int64_t)g * E + e) * G + d) + (r - c);
+    if (lane == 0) pos[t * k + j] = (int32_t)p;
+    uint4* dst = out + p * n16;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int cc = i * 32 + lane;
+      if (cc < n16) dst[cc] = v[i];
+    }
+  }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kPermWarps * 32)
+    combine_kernel(const uint4* __restrict__ Y, const int32_t* __restrict__ pos, const float* __restrict__ w,
+                   int64_t T, int k, int n16, uint4* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
+  if (t >= T) return;
+  float acc[VEC][8];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
+  for (int j = 0; j < k; ++j) {
+    const int64_t p = __ldg(pos + t * k + j);
+    const float wj = __ldg(w + t * k + j);
+    const uint4* row = Y + p * n16;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int c = i * 32 + lane;
+      if (c < n16) {
+        const uint4 u = ld_global_nc_v4(row + c);
+        const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          acc[i][2 * h] = __fadd_rn(acc[i][2 * h], __fmul_rn(wj, bf16lo(uu[h])));
+          acc[i][2 * h + 1] = __fadd_rn(acc[i][2 * h + 1], __fmul_rn(wj, bf16hi(uu[h])));
+        }
+      }
+    }
+  }
+  uint4* dst = y + t * n16;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = i * 32 + lane;
+    if (c < n16)
+      dst[c] = make_uint4(pack_bf16x2(acc[i][0], acc[i][1]), pack_bf16x2(acc[i][2], acc[i][3]),
+                          pack_bf16x2(acc[i][4], acc[i][5]), pack_bf16x2(acc[i][6], acc[i][7]));
+  }
+}
+
+int launch_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+                   const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base,
+                   int G, int E, int k, int d, void* out, int32_t* pos, cudaStream_t stream) {
+  if (d <= 0 || d % 8 != 0 || d > 8192) return set_error(HM_EINVAL, "permute: need d %% 8 == 0 and d <= 8192");
+  if (n_ranks < 1 || tokens_per_rank < 0 || G < 1 || E < 1 || k < 1)
+    return set_error(HM_EINVAL, "permute: bad sizes");
+  const int64_t T = (int64_t)n_ranks * tokens_per_rank;
+  if (T == 0) return HM_OK;
+  const int n16 = d / 8;
+  const int vec = (n16 + 31) / 32;
+  const int tiles_per_rank = (tokens_per_rank + 127) / 128;
+  const unsigned grid = (unsigned)((T + kPermWarps - 1) / kPermWarps);
+  auto* xs = reinterpret_cast<const uint4*>(x);
+  auto* o = reinterpret_cast<uint4*>(out);
+#define HM_PERM(V)                                                                                              \
+  permute_kernel<V><<<grid, kPermWarps * 32, 0, stream>>>(xs, topk_idx, lrank, tile_off, S, slot_base, T,       \
+                                                          tokens_per_rank, tiles_per_rank, src_rank_base, G, E, \
+                                                          k, n16, o, pos)
+  if (vec <= 1) HM_PERM(1);
+  else if (vec <= 2) HM_PERM(2);
+  else if (vec <= 4) HM_PERM(4);
+  else if (vec <= 8) HM_PERM(8);
+  else if (vec <= 16) HM_PERM(16);
+  else HM_PERM(32);
+#undef HM_PERM
+  return check_launch("permute");
+}
+
+int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y,
+                   cudaStream_t stream) {
+  if (d <= 0 || d % 8 != 0 || d > 8192) return set_error(HM_EINVAL, "combine: need d %% 8 == 0 and d <= 8192");
+  if (T < 0 || k < 1) return set_error(HM_EINVAL, "combine: bad sizes");
+  if (T == 0) return HM_OK;
+  const int n16 = d / 8;
+  const int vec = (n16 + 31) / 32;
+  const unsigned grid = (unsigned)((T + kPermWarps - 1) / kPermWarps);
+  auto* Ys = reinterpret_cast<const uint4*>(Y);
+  auto* o = reinterpret_cast<uint4*>(y);
+#define HM_COMB(V) combine_kernel<V><<<grid, kPermWarps * 32, 0, stream>>>(Ys, pos, topk_w, T, k, n16, o)
+  if (vec <= 1) HM_COMB(1);
+  else if (vec <= 2) HM_COMB(2);
+  else if (vec <= 4) HM_COMB(4);
+  else if (vec <= 8) HM_COMB(8);
+  else if (vec <= 16) HM_COMB(16);
+  else HM_COMB(32);
+#undef HM_COMB
+  return check_launch("combine");
+}
+
+}  // namespace hm

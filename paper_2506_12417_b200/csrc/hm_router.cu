@@ -1,0 +1,297 @@
+// K1 + K2: router (gate GEMM + softmax + top-k) fused with the per-tile expert
+// histogram and the deterministic (token, slot)-order rank pass.
+//
+// Replaces Alg.1 step 1 whose reference stand-in is
+// workload.sample_routing (workload.py:167-180), and builds the per-GPU
+// token->expert histogram that becomes RoutingMatrix.counts[g] (core.py:89-96),
+// i.e. the 4 KB metadata exchanged in step 2.
+//
+// One CTA per 128-token tile.  Logits [128, E_pad] accumulate in TMEM via
+// tcgen05.mma (A = x tile via TMA, B = Wg via TMA); the 4 epilogue warps own one
+// token row each (TMEM lane == row) and run softmax + top-k in registers.
+// Top-k is taken over the fp32 logits, ties to the lowest expert id; weights are
+// the softmax probabilities of the winners (optionally renormalised over k).
+// The rank pass uses __match_any_sync over 32-assignment chunks in (token, slot)
+// order so lrank is deterministic (no atomics), which is what makes the
+// dispatch bit-reproducible.
+#include "hm_common.cuh"
+#include "hm_internal.h"
+
+namespace hm {
+
+namespace {
+constexpr int kRBM = 128;
+constexpr int kRBK = 64;
+constexpr int kRStages = 4;
+constexpr uint32_t kRA = kRBM * kRBK * 2;       // 16 KB
+constexpr uint32_t kRBmax = 256 * kRBK * 2;     // 32 KB (E_pad <= 256)
+constexpr int kRThreads = 192;
+constexpr int kRKmax = 16;
+constexpr size_t kRSmem =
+    1024 + kRStages * (kRA + kRBmax) + 256 + 2 * kRBM * kRKmax * sizeof(int) + 4 * 256 * sizeof(int);
+}  // namespace
+
+template <int KMAX>
+__global__ void __launch_bounds__(kRThreads, 1)
+    router_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                  const float* __restrict__ bias, int tokens_per_rank, int tiles_per_rank, int d, int E, int E_pad,
+                  int k, int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                  int32_t* __restrict__ tile_hist, int32_t* __restrict__ lrank) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kRStages * kRA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_b + kRStages * kRBmax);
+  uint64_t* empty = full + kRStages;
+  uint64_t* tfull = empty + kRStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  int* s_idx = reinterpret_cast<int*>(smem_b + kRStages * kRBmax + 256);
+  int* s_rank = s_idx + kRBM * kRKmax;
+  int* s_cnt = s_rank + kRBM * kRKmax;  // [4][E_pad]
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int tile = blockIdx.x;
+  const int rank = tile / tiles_per_rank;
+  const int mt = tile - rank * tiles_per_rank;
+  const int row0 = rank * tokens_per_rank + mt * kRBM;
+  const int rows = min(kRBM, tokens_per_rank - mt * kRBM);
+  const int KB = d / kRBK;
+  const uint32_t b_bytes = (uint32_t)E_pad * kRBK * 2;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kRStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmap_x);
+    tma_prefetch_desc(&tmap_w);
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_x = l2_policy_evict_first();
+      const uint64_t pol_w = l2_policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], kRA + b_bytes);
+        tma_load_2d(smem_a + stage * kRA, &tmap_x, &full[stage], kb * kRBK, row0, pol_x);
+        tma_load_2d(smem_b + stage * kRBmax, &tmap_w, &full[stage], kb * kRBK, 0, pol_w);
+        if (++stage == kRStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(kRBM, (uint32_t)E_pad);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint64_t a0 = make_sdesc_sw128(smem_u32(smem_a + stage * kRA));
+        const uint64_t b0 = make_sdesc_sw128(smem_u32(smem_b + stage * kRBmax));
+#pragma unroll
+        for (int kk = 0; kk < kRBK / 16; ++kk)
+          umma_bf16(tmem_base, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+        umma_commit(&empty[stage]);
+        if (++stage == kRStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      umma_commit(&tfull[0]);
+    }
+  } else {
+    // ===== epilogue: softmax + top-k + histogram/rank =====
+    const int etid = threadIdx.x - 64;  // 0..127
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const bool valid = r < rows;
+    const int64_t t = (int64_t)row0 + r;
+    for (int i = etid; i < 4 * E_pad; i += 128) s_cnt[i] = 0;
+
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+    const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
+
+    float tv[KMAX];
+    int ti[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      tv[j] = -INFINITY;
+      ti[j] = 0x7fffffff;
+    }
+    const int nchunk = (E + 31) / 32;
+    for (int c = 0; c < nchunk; ++c) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(taddr + c * 32, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int e = c * 32 + jj;
+        if (e < E) {
+          float v = __uint_as_float(a[jj]);
+          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
+          float cv = v;
+          int ci = e;
+          bool ins = false;
+#pragma unroll
+          for (int j = 0; j < KMAX; ++j) {
+            if (j < k && (ins || cv > tv[j])) {
+              const float tf = tv[j];
+              const int tix = ti[j];
+              tv[j] = cv;
+              ti[j] = ci;
+              cv = tf;
+              ci = tix;
+              ins = true;
+            }
+          }
+        }
+      }
+    }
+    const float mx = tv[0];
+    float sum = 0.0f;
+    for (int c = 0; c < nchunk; ++c) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(taddr + c * 32, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int e = c * 32 + jj;
+        if (e < E) {
+          float v = __uint_as_float(a[jj]);
+          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
+          sum = __fadd_rn(sum, expf(__fsub_rn(v, mx)));
+        }
+      }
+    }
+    float p[KMAX];
+    float psum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      if (j < k) {
+        p[j] = __fdiv_rn(expf(__fsub_rn(tv[j], mx)), sum);
+        psum = __fadd_rn(psum, p[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      if (j < k) {
+        const float w = renorm ? __fdiv_rn(p[j], psum) : p[j];
+        if (valid) {
+          topk_idx[t * k + j] = ti[j];
+          topk_w[t * k + j] = w;
+        }
+        s_idx[r * k + j] = valid ? ti[j] : -1;
+      }
+    }
+    named_bar_sync(1, 128);
+
+    // rank pass: warp q walks its 32 rows' assignments in (token, slot) order
+    const int base_a = q * 32 * k;
+    for (int c = 0; c < k; ++c) {
+      const int a = base_a + c * 32 + lane;
+      const int e = s_idx[a];
+      const uint32_t mask = __match_any_sync(0xffffffffu, e);
+      const int cnt0 = (e >= 0) ? s_cnt[q * E_pad + e] : 0;
+      __syncwarp();
+      const int leader = 31 - __clz(mask);
+      if (e >= 0 && lane == leader) s_cnt[q * E_pad + e] = cnt0 + __popc(mask);
+      s_rank[a] = cnt0 + __popc(mask & lanemask_lt());
+      __syncwarp();
+    }
+    named_bar_sync(1, 128);
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        if (j < k) {
+          const int e = ti[j];
+          int off = 0;
+          for (int qq = 0; qq < q; ++qq) off += s_cnt[qq * E_pad + e];
+          lrank[t * k + j] = s_rank[r * k + j] + off;
+        }
+      }
+    }
+    for (int e = etid; e < E; e += 128)
+      tile_hist[(int64_t)tile * E + e] =
+          s_cnt[e] + s_cnt[E_pad + e] + s_cnt[2 * E_pad + e] + s_cnt[3 * E_pad + e];
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem_base);
+  }
+}
+
+// Reduce per-tile histograms to per-rank m_expert rows and exclusive per-tile offsets.
+__global__ void hist_scan_kernel(const int32_t* __restrict__ tile_hist, int tiles_per_rank, int E,
+                                 int32_t* __restrict__ hist, int32_t* __restrict__ tile_off) {
+  const int rank = blockIdx.x;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = 0;
+    for (int m = 0; m < tiles_per_rank; ++m) {
+      const int64_t i = ((int64_t)rank * tiles_per_rank + m) * E + e;
+      const int v = tile_hist[i];
+      tile_off[i] = run;
+      run += v;
+    }
+    hist[(int64_t)rank * E + e] = run;
+  }
+}
+
+int launch_router(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
+                  int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,
+                  cudaStream_t stream) {
+  if (n_ranks < 1 || tokens_per_rank < 0 || d <= 0 || d % 64 != 0)
+    return set_error(HM_EINVAL, "router: need n_ranks >= 1 and d %% 64 == 0");
+  if (E < 1 || E > 256 || k < 1 || k > kRKmax || k > E)
+    return set_error(HM_EINVAL, "router: need 1 <= k <= min(E, 16) and E <= 256");
+  if (tokens_per_rank == 0) return HM_OK;
+  const int E_pad = (E + 15) / 16 * 16;
+  const int tiles_per_rank = (tokens_per_rank + kRBM - 1) / kRBM;
+  const int64_t T = (int64_t)n_ranks * tokens_per_rank;
+  CUtensorMap tx, tw;
+  int rc = make_tmap_2d_bf16(&tx, x, (uint64_t)T, (uint64_t)d, kRBM, kRBK);
+  if (rc) return rc;
+  rc = make_tmap_2d_bf16(&tw, wg, (uint64_t)E_pad, (uint64_t)d, (uint32_t)E_pad, kRBK);
+  if (rc) return rc;
+  const int grid = n_ranks * tiles_per_rank;
+#define HM_LAUNCH_ROUTER(KM)                                                                                 \
+  do {                                                                                                       \
+    cudaFuncSetAttribute(router_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRSmem);       \
+    router_kernel<KM><<<grid, kRThreads, kRSmem, stream>>>(tx, tw, bias, tokens_per_rank, tiles_per_rank, d, \
+                                                           E, E_pad, k, renormalize, topk_idx, topk_w,       \
+                                                           tile_hist, lrank);                                \
+  } while (0)
+  if (k == 1) HM_LAUNCH_ROUTER(1);
+  else if (k == 2) HM_LAUNCH_ROUTER(2);
+  else if (k <= 4) HM_LAUNCH_ROUTER(4);
+  else if (k <= 8) HM_LAUNCH_ROUTER(8);
+  else HM_LAUNCH_ROUTER(16);
+#undef HM_LAUNCH_ROUTER
+  return check_launch("router_topk");
+}
+
+int launch_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_rank, int E, int32_t* hist,
+                     int32_t* tile_off, cudaStream_t stream) {
+  if (n_ranks < 1 || tiles_per_rank < 0 || E < 1) return set_error(HM_EINVAL, "hist_scan: bad sizes");
+  hist_scan_kernel<<<n_ranks, 256, 0, stream>>>(tile_hist, tiles_per_rank, E, hist, tile_off);
+  return check_launch("hist_scan");
+}
+
+}  // namespace hm

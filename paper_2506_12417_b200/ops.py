@@ -1,0 +1,175 @@
+"""Torch-tensor wrappers over the C ABI (device memory + streams are torch's;
+the compute is libharmoe.so).  Every function is stream-ordered on the current
+torch CUDA stream unless ``stream`` is given, allocates only its outputs, and
+never synchronises the host.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import HM_EPI_RELU, HM_EPI_STORE, HM_EPI_SWIGLU, HM_LAYOUT_EP, HM_LAYOUT_LOCAL  # noqa: F401
+
+TILE_M = 128
+
+
+def _require_cuda(*tensors):
+    for t in tensors:
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError("harmoe ops need CUDA tensors (no CPU fallback)")
+        if not t.is_contiguous():
+            raise ValueError("harmoe ops need contiguous tensors")
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def e_pad(E: int) -> int:
+    return (E + 15) // 16 * 16
+
+
+def router_topk(x, wg, bias, n_ranks: int, tokens_per_rank: int, k: int, renormalize: bool, stream=None):
+    """K1+K2.  x [n_ranks*T_g, d] bf16, wg [E_pad, d] bf16 (rows >= E are zero padding), bias [E] fp32|None.
+    Returns topk_idx [T,k] i32, topk_w [T,k] f32, tile_hist [tiles, E] i32, lrank [T,k] i32."""
+    _require_cuda(x, wg, bias)
+    if x.dtype != torch.bfloat16 or wg.dtype != torch.bfloat16:
+        raise ValueError("router expects bf16 x and wg")
+    T, d = x.shape
+    if T != n_ranks * tokens_per_rank:
+        raise ValueError("x rows must equal n_ranks * tokens_per_rank")
+    E = bias.numel() if bias is not None else wg.shape[0]
+    if wg.shape[0] != e_pad(E) or wg.shape[1] != d:
+        raise ValueError(f"wg must be [E_pad={e_pad(E)}, d]")
+    tiles = n_ranks * ((tokens_per_rank + TILE_M - 1) // TILE_M)
+    dev = x.device
+    idx = torch.empty((T, k), dtype=torch.int32, device=dev)
+    w = torch.empty((T, k), dtype=torch.float32, device=dev)
+    tile_hist = torch.empty((tiles, E), dtype=torch.int32, device=dev)
+    lrank = torch.empty((T, k), dtype=torch.int32, device=dev)
+    _lib.call("hm_router_topk", _ptr(x), _ptr(wg), _ptr(bias), n_ranks, tokens_per_rank, d, E, k,
+              int(bool(renormalize)), _ptr(idx), _ptr(w), _ptr(tile_hist), _ptr(lrank), _stream(stream))
+    return idx, w, tile_hist, lrank
+
+
+def hist_scan(tile_hist, n_ranks: int, tiles_per_rank: int, stream=None):
+    """Per-rank histogram m_expert [n_ranks, E] + per-tile exclusive offsets."""
+    _require_cuda(tile_hist)
+    E = tile_hist.shape[1]
+    hist = torch.empty((n_ranks, E), dtype=torch.int32, device=tile_hist.device)
+    tile_off = torch.empty_like(tile_hist)
+    _lib.call("hm_hist_scan", _ptr(tile_hist), n_ranks, tiles_per_rank, E, _ptr(hist), _ptr(tile_off),
+              _stream(stream))
+    return hist, tile_off
+
+
+def schedule(m_all, home, q: int, rebalance: bool = True, stream=None):
+    """K3: S [G,E,G] i32, iters [1] i32, loads [G] i32 — all on device."""
+    _require_cuda(m_all, home)
+    if m_all.dtype != torch.int32 or home.dtype != torch.int32:
+        raise ValueError("schedule expects int32 m_all and home")
+    G, E = m_all.shape
+    dev = m_all.device
+    S = torch.empty((G, E, G), dtype=torch.int32, device=dev)
+    iters = torch.empty(1, dtype=torch.int32, device=dev)
+    loads = torch.empty(G, dtype=torch.int32, device=dev)
+    _lib.call("hm_schedule", _ptr(m_all), _ptr(home), G, E, int(q), int(bool(rebalance)), _ptr(S), _ptr(iters),
+              _ptr(loads), _stream(stream))
+    return S, iters, loads
+
+
+def rebalance_(S, q: int, stream=None):
+    """In-place rebalance of S [G,E,G] i32; returns (iters, loads) device tensors."""
+    _require_cuda(S)
+    if S.dtype != torch.int32:
+        raise ValueError("rebalance expects int32 S")
+    G, E, _ = S.shape
+    iters = torch.empty(1, dtype=torch.int32, device=S.device)
+    loads = torch.empty(G, dtype=torch.int32, device=S.device)
+    _lib.call("hm_rebalance", _ptr(S), G, E, int(q), _ptr(iters), _ptr(loads), _stream(stream))
+    return iters, loads
+
+
+class Layout:
+    """Device-side result of hm_dispatch_layout."""
+
+    __slots__ = ("slot_base", "segs", "n_seg", "mtile_prefix", "fetch", "n_fetch")
+
+    def __init__(self, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch):
+        self.slot_base, self.segs, self.n_seg = slot_base, segs, n_seg
+        self.mtile_prefix, self.fetch, self.n_fetch = mtile_prefix, fetch, n_fetch
+
+
+def dispatch_layout(S, home, mode: int, me: int = 0, stream=None) -> Layout:
+    _require_cuda(S, home)
+    G, E, _ = S.shape
+    dev = S.device
+    cap = G * E
+    slot_base = torch.zeros((G, E, G), dtype=torch.int32, device=dev)
+    segs = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+    n_seg = torch.empty(1, dtype=torch.int32, device=dev)
+    mprefix = torch.empty(cap + 1, dtype=torch.int32, device=dev)
+    fetch = torch.empty(E, dtype=torch.int32, device=dev)
+    n_fetch = torch.empty(1, dtype=torch.int32, device=dev)
+    _lib.call("hm_dispatch_layout", _ptr(S), _ptr(home), G, E, int(mode), int(me), _ptr(slot_base), _ptr(segs),
+              _ptr(n_seg), _ptr(mprefix), _ptr(fetch), _ptr(n_fetch), _stream(stream))
+    return Layout(slot_base, segs, n_seg, mprefix, fetch, n_fetch)
+
+
+def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per_rank: int, src_rank_base: int,
+            out_rows: int, out=None, stream=None):
+    """K4.  Returns (out [out_rows, d] bf16, pos [T,k] i32)."""
+    _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base)
+    T, d = x.shape
+    k = topk_idx.shape[1]
+    G, E, _ = S.shape
+    if out is None:
+        out = torch.empty((max(out_rows, 1), d), dtype=x.dtype, device=x.device)
+    pos = torch.empty((T, k), dtype=torch.int32, device=x.device)
+    _lib.call("hm_permute", _ptr(x), _ptr(topk_idx), _ptr(lrank), _ptr(tile_off), _ptr(S), _ptr(slot_base),
+              n_ranks, tokens_per_rank, src_rank_base, G, E, k, d, _ptr(out), _ptr(pos), _stream(stream))
+    return out, pos
+
+
+def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, slot_ready=None, ready_from_slot: int = 0,
+                 epoch: int = 0, stream=None):
+    """K5.  A [rows, K] bf16, W [slots*N, K] bf16 -> out [rows, N or N/2] bf16."""
+    if isinstance(layout_or_segs, Layout):
+        segs, n_seg, mprefix = layout_or_segs.segs, layout_or_segs.n_seg, layout_or_segs.mtile_prefix
+    else:
+        segs, n_seg, mprefix = layout_or_segs
+    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready)
+    rows, K = A.shape
+    ncols = N // 2 if epilogue == HM_EPI_SWIGLU else N
+    if out is None:
+        out = torch.empty((rows, ncols), dtype=torch.bfloat16, device=A.device)
+    _lib.call("hm_grouped_gemm", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(segs), _ptr(n_seg), _ptr(mprefix),
+              int(epilogue), _ptr(out), _ptr(slot_ready), int(ready_from_slot), int(epoch), _stream(stream))
+    return out
+
+
+def fetch_expert(dst, src, ready_flag=None, epoch: int = 0, stream=None):
+    """K6 primitive: async copy src -> dst (peer HBM / pinned host) + flag publish."""
+    if dst.numel() * dst.element_size() != src.numel() * src.element_size():
+        raise ValueError("fetch_expert: size mismatch")
+    _lib.call("hm_fetch_expert", _ptr(dst), _ptr(src), dst.numel() * dst.element_size(),
+              None if ready_flag is None else ready_flag.data_ptr(), int(epoch), _stream(stream))
+
+
+def combine(Y, pos, topk_w, out=None, stream=None):
+    """K7.  y [T, d] bf16 = sum_j w[t,j] * Y[pos[t,j]]."""
+    _require_cuda(Y, pos, topk_w)
+    T, k = pos.shape
+    d = Y.shape[1]
+    if out is None:
+        out = torch.empty((T, d), dtype=torch.bfloat16, device=Y.device)
+    _lib.call("hm_combine", _ptr(Y), _ptr(pos), _ptr(topk_w), T, k, d, _ptr(out), _stream(stream))
+    return out

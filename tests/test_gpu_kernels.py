@@ -1,0 +1,316 @@
+"""GPU parity of each hot-path kernel against the CPU oracle (through the C ABI).
+
+Bars: routing indices, histograms, ranks and schedules are
+bit-exact; expert outputs within |y - y_ref| <= 1e-2 + 2e-2*|y_ref| elementwise
+and relative Frobenius error <= 5e-3.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import iter_packed  # noqa: E402
+from oracle import moe_oracle as orc  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL, FROB = 1e-2, 2e-2, 5e-3
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda")
+
+
+def bits(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def assert_close(y, y_ref, what=""):
+    y = np.asarray(y, np.float64)
+    y_ref = np.asarray(y_ref, np.float64)
+    err = np.abs(y - y_ref)
+    bad = err > ATOL + RTOL * np.abs(y_ref)
+    assert not bad.any(), f"{what}: {bad.sum()} elements out of tolerance, max err {err.max()}"
+    frob = np.linalg.norm(y - y_ref) / max(np.linalg.norm(y_ref), 1e-30)
+    assert frob <= FROB, f"{what}: relative Frobenius error {frob}"
+
+
+# ------------------------------------------------------------------------------------------
+# K3 scheduler
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("pack", ["fig4", "acceptance_c2", "baseline_shapes"])
+def test_schedule_kernel_bit_exact(golden, pack):
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    n = 0
+    for inst in iter_packed(golden(pack)):
+        m = torch.from_numpy(inst["m"].astype(np.int32)).to(dev)
+        home = torch.from_numpy(inst["home"].astype(np.int32)).to(dev)
+        S, iters, loads = ops.schedule(m, home, inst["q"], rebalance=True)
+        S = S.cpu().numpy()
+        assert np.array_equal(S, inst["S"]), f"{pack} instance {inst['i']}"
+        assert int(iters.item()) == inst["iters"], f"{pack} instance {inst['i']}"
+        assert np.array_equal(loads.cpu().numpy(), inst["S"].sum(axis=(0, 1)))
+        n += 1
+        if pack == "acceptance_c2" and n >= 600:
+            break
+
+
+def test_rebalance_dropin_api(golden):
+    """The moesim-signature wrappers (policies.rebalance_with_stats) reproduce the reference."""
+    _cuda()
+    from paper_2506_12417_b200 import Placement, RoutingMatrix, initial_assign, rebalance, rebalance_with_stats
+
+    for inst in list(iter_packed(golden("acceptance_c2")))[:60]:
+        G = inst["m"].shape[0]
+        s0 = initial_assign(RoutingMatrix(inst["m"]), Placement(home=tuple(int(h) for h in inst["home"]), num_gpus=G))
+        before = s0.counts.copy()
+        s1, it = rebalance_with_stats(s0, inst["q"])
+        assert np.array_equal(s1.counts, inst["S"]) and it == inst["iters"]
+        assert np.array_equal(s0.counts, before)  # input not mutated (test_policies.py:120-124)
+        assert rebalance(s1, inst["q"]) == s1  # fixpoint
+    with pytest.raises(ValueError):
+        rebalance(s0, 0)
+
+
+# ------------------------------------------------------------------------------------------
+# K1 + K2 router
+# ------------------------------------------------------------------------------------------
+def _router_inputs(T, d, E, integer, seed, dev):
+    rng = np.random.default_rng(seed)
+    if integer:
+        # small integers: every fp32 partial sum is exact -> logits exact in any order,
+        # and ties are frequent (exercises the lowest-index rule)
+        x = rng.integers(-2, 3, size=(T, d)).astype(np.float32)
+        wg = rng.integers(-1, 2, size=(E, d)).astype(np.float32)
+    else:
+        x = rng.standard_normal((T, d)).astype(np.float32)
+        wg = (rng.standard_normal((E, d)) / np.sqrt(d)).astype(np.float32)
+    xb = orc.f32_to_bf16(x)
+    wb = orc.f32_to_bf16(wg)
+    x_t = torch.from_numpy(xb.view(np.int16)).view(torch.bfloat16).to(dev)
+    from paper_2506_12417_b200.ops import e_pad
+
+    wpad = np.zeros((e_pad(E), d), np.uint16)
+    wpad[:E] = wb
+    w_t = torch.from_numpy(wpad.view(np.int16)).view(torch.bfloat16).to(dev)
+    return xb, wb, x_t, w_t
+
+
+def _cpu_ranks(idx, n_ranks, Tg):
+    """Reference lrank/tile_hist from the GPU's own indices: rank within (tile, expert) in (t, j) order."""
+    T, k = idx.shape
+    tiles_per_rank = (Tg + 127) // 128
+    lrank = np.zeros_like(idx)
+    counts = {}
+    for t in range(T):
+        r = t // Tg
+        tile = r * tiles_per_rank + (t % Tg) // 128
+        for j in range(k):
+            key = (tile, int(idx[t, j]))
+            lrank[t, j] = counts.get(key, 0)
+            counts[key] = lrank[t, j] + 1
+    return lrank, counts
+
+
+@pytest.mark.parametrize("E,k,d,n_ranks,Tg,bias", [
+    (128, 8, 256, 1, 512, False),
+    (128, 1, 768, 4, 256, True),
+    (8, 2, 512, 2, 200, False),   # E_pad = 16, ragged last tile
+    (60, 4, 128, 3, 130, True),   # E not a multiple of 16
+])
+@pytest.mark.parametrize("integer", [True, False])
+def test_router_topk_hist(E, k, d, n_ranks, Tg, bias, integer):
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    T = n_ranks * Tg
+    xb, wb, x_t, w_t = _router_inputs(T, d, E, integer, seed=E * 31 + k, dev=dev)
+    b = None
+    b_t = None
+    if bias:
+        b = np.log(np.arange(1, E + 1, dtype=np.float64) ** -1.0 / np.sum(np.arange(1, E + 1) ** -1.0)).astype(
+            np.float32)
+        if integer:
+            b = np.round(b).astype(np.float32)
+        b_t = torch.from_numpy(b).to(dev)
+    renorm = k > 1
+    idx, w, tile_hist, lrank = ops.router_topk(x_t, w_t, b_t, n_ranks, Tg, k, renorm)
+    torch.cuda.synchronize()
+    idx = idx.cpu().numpy()
+    logits, idx_ref, w_ref = orc.router(xb, wb, b, k, renorm)
+    if integer:
+        assert np.array_equal(idx, idx_ref)
+    else:
+        margin = orc.topk_margin(logits, k)
+        ok = margin > 1e-4 * np.maximum(1.0, np.abs(logits).max(axis=1))
+        assert ok.mean() > 0.95
+        # exact set and order wherever the top-k is not a near tie
+        assert np.array_equal(idx[ok], idx_ref[ok])
+    np.testing.assert_allclose(w.cpu().numpy()[np.all(idx == idx_ref, axis=1)],
+                               w_ref[np.all(idx == idx_ref, axis=1)], rtol=2e-5, atol=1e-6)
+    # histogram + ranks are exact functions of the GPU's own indices
+    lr_ref, counts = _cpu_ranks(idx, n_ranks, Tg)
+    assert np.array_equal(lrank.cpu().numpy(), lr_ref)
+    th = tile_hist.cpu().numpy()
+    th_ref = np.zeros_like(th)
+    for (tile, e), c in counts.items():
+        th_ref[tile, e] = c
+    assert np.array_equal(th, th_ref)
+    tiles_per_rank = (Tg + 127) // 128
+    hist, tile_off = ops.hist_scan(tile_hist, n_ranks, tiles_per_rank)
+    for r in range(n_ranks):
+        assert np.array_equal(hist[r].cpu().numpy(), orc.histogram(idx[r * Tg:(r + 1) * Tg], E))
+
+
+# ------------------------------------------------------------------------------------------
+# K5 grouped GEMM
+# ------------------------------------------------------------------------------------------
+def _segs_from_counts(counts, wslots, device):
+    segs, starts, mt = [], 0, [0]
+    for n, s in zip(counts, wslots):
+        if n == 0:
+            continue
+        segs.append([starts, n, s, s])
+        starts += n
+        mt.append(mt[-1] + (n + 127) // 128)
+    segs_t = torch.tensor(segs if segs else [[0, 0, 0, 0]], dtype=torch.int32, device=device)
+    return (segs_t, torch.tensor([len(segs)], dtype=torch.int32, device=device),
+            torch.tensor(mt, dtype=torch.int32, device=device)), starts
+
+
+@pytest.mark.parametrize("epi", ["store", "relu", "swiglu"])
+@pytest.mark.parametrize("N,K", [(256, 64), (512, 768), (1536, 2048)])
+def test_grouped_gemm(epi, N, K):
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    g = torch.Generator(device=dev).manual_seed(N + K)
+    E = 5
+    counts = [1, 0, 300, 129, 64, 17][:E]
+    wslots = [3, 1, 0, 4, 2][:E]
+    lay, rows = _segs_from_counts(counts, wslots, dev)
+    A = torch.randn((rows, K), device=dev, generator=g).to(torch.bfloat16)
+    W = (torch.randn((E * N, K), device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    code = dict(store=ops.HM_EPI_STORE, relu=ops.HM_EPI_RELU, swiglu=ops.HM_EPI_SWIGLU)[epi]
+    out = ops.grouped_gemm(A, W, N, lay, code)
+    torch.cuda.synchronize()
+    ref = []
+    r0 = 0
+    for n, s in zip(counts, wslots):
+        if n == 0:
+            continue
+        acc = A[r0:r0 + n].float() @ W[s * N:(s + 1) * N].float().T
+        if epi == "relu":
+            acc = torch.relu(acc)
+        elif epi == "swiglu":
+            a = acc.view(n, N // 256, 2, 128)
+            gate, up = a[:, :, 0, :], a[:, :, 1, :]
+            acc = (torch.nn.functional.silu(gate) * up).reshape(n, N // 2)
+        ref.append(acc)
+        r0 += n
+    ref = torch.cat(ref).to(torch.bfloat16).float().cpu().numpy()
+    assert_close(out.float().cpu().numpy(), ref, f"gemm {epi} N={N} K={K}")
+
+
+# ------------------------------------------------------------------------------------------
+# full block (LOCAL layout) vs the oracle
+# ------------------------------------------------------------------------------------------
+def _block(cfg, seed, dev, zipf_s=1.0):
+    from paper_2506_12417_b200.block import HarMoEnyBlock
+
+    return HarMoEnyBlock.random(cfg, seed=seed, device=dev, zipf_s=zipf_s, std=0.05)
+
+
+@pytest.mark.parametrize("arch", ["qwen_small", "switch_small", "mixtral_small"])
+@pytest.mark.parametrize("G", [1, 4])
+def test_block_matches_oracle(arch, G):
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    shapes = dict(
+        qwen_small=dict(d_model=256, num_experts=32, d_ff=256, top_k=8, activation="swiglu"),
+        switch_small=dict(d_model=256, num_experts=16, d_ff=512, top_k=1, activation="relu"),
+        mixtral_small=dict(d_model=512, num_experts=8, d_ff=768, top_k=2, activation="swiglu"),
+    )[arch]
+    cfg = MoEConfig(logical_ranks=G, eq_tokens=4, placement="blocked", **shapes)
+    blk = _block(cfg, seed=G, dev=dev)
+    T = 512
+    x = torch.randn((T, cfg.d_model), device=dev, generator=torch.Generator(device=dev).manual_seed(7)).to(
+        torch.bfloat16)
+    y = blk(x)
+    torch.cuda.synchronize()
+    # oracle on identical bf16 inputs
+    E, f, d = cfg.num_experts, cfg.d_ff, cfg.d_model
+    wg = bits(blk.wg[:E])
+    if cfg.activation == "swiglu":
+        w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, d)
+        w1 = w13[:, :, 0].reshape(E, f, d)
+        w3 = w13[:, :, 1].reshape(E, f, d)
+    else:
+        w1 = bits(blk.w_in).reshape(E, f, d)
+        w3 = None
+    w2 = bits(blk.w_out).reshape(E, d, f)
+    bias = None if blk.bias is None else blk.bias.cpu().numpy()
+    y_ref, idx_ref, w_ref, logits = orc.moe_block(bits(x), wg, bias, w1, w2, cfg.top_k, cfg.activation,
+                                                  cfg.renormalize, w3)
+    idx = blk.stats.extras["topk_idx"].cpu().numpy()
+    agree = np.all(idx == idx_ref, axis=1)
+    assert agree.mean() > 0.97
+    assert_close(orc.bf16_to_f32(bits(y))[agree], orc.bf16_to_f32(y_ref)[agree], f"block {arch} G={G}")
+    # schedule of the block == oracle schedule on the GPU's histogram
+    m_all = blk.stats.m_all.cpu().numpy()
+    S_ref, it_ref = orc.schedule(m_all, blk.home_np, cfg.eq_tokens, True)
+    assert np.array_equal(blk.stats.schedule.cpu().numpy(), S_ref)
+    assert int(blk.stats.iters.item()) == it_ref
+    for g in range(G):
+        assert np.array_equal(m_all[g], orc.histogram(idx[g * (T // G):(g + 1) * (T // G)], E))
+
+
+def test_block_output_independent_of_schedule():
+    """Rebalancing moves work between (logical) GPUs but never changes the math:
+    the block output is bit-identical with rebalancing on and off."""
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    shapes = dict(d_model=256, num_experts=32, d_ff=256, top_k=4, activation="swiglu")
+    x = torch.randn((1024, 256), device=dev, generator=torch.Generator(device=dev).manual_seed(3)).to(torch.bfloat16)
+    ys = []
+    for policy in ("harmony", "round_robin"):
+        cfg = MoEConfig(logical_ranks=4, eq_tokens=1, placement="blocked", scheduling_policy=policy, **shapes)
+        blk = _block(cfg, seed=11, dev=dev, zipf_s=1.5)
+        ys.append(bits(blk(x)))
+        if policy == "harmony":
+            assert blk.stats.load_imbalance() <= 1.1
+            assert int(blk.stats.iters.item()) > 0
+    assert np.array_equal(ys[0], ys[1])
+
+
+def test_dispatch_positions_follow_contract():
+    """pos[t,j] lands in the scheduled destination's region (split-bucket contract)."""
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    cfg = MoEConfig(logical_ranks=4, eq_tokens=1, placement="blocked", d_model=128, num_experts=16, d_ff=256,
+                    top_k=2, activation="swiglu")
+    blk = _block(cfg, seed=5, dev=dev, zipf_s=1.2)
+    T = 1024
+    x = torch.randn((T, 128), device=dev).to(torch.bfloat16)
+    blk(x)
+    torch.cuda.synchronize()
+    st = blk.stats
+    S = st.schedule.cpu().numpy().astype(np.int64)
+    idx = st.extras["topk_idx"].cpu().numpy()
+    pos = st.extras["pos"].cpu().numpy()
+    loads = S.sum(axis=(0, 1))
+    base = np.concatenate([[0], np.cumsum(loads)])
+    assert sorted(pos.reshape(-1).tolist()) == list(range(T * cfg.top_k))  # a permutation
+    Tg = T // 4
+    for g in range(4):
+        dest, rank = orc.dispatch_ranks(idx[g * Tg:(g + 1) * Tg], S, g)
+        p = pos[g * Tg:(g + 1) * Tg].reshape(-1)
+        assert np.all(p >= base[dest]) and np.all(p < base[dest + 1])
