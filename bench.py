@@ -1,0 +1,411 @@
+"""Benchmark of the HarMoEny MoE block on B200 (BASELINE.json metric: MoE-block
+tokens/sec under skew; max/mean GPU load; % roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload qwen128]
+
+A step = one forward of one MoE block over one batch of synthetic Zipf-skewed
+tokens (router -> schedule -> scatter -> grouped-GEMM experts -> combine).
+N=1 runs BASELINE configs[1] (Qwen 128-expert layer, d 2048, expert d_ff 768,
+top-8, 16,384 tokens) on one GPU.  N>1 (torchrun, one rank per GPU, NCCL)
+shards the same 16,384-token batch over the ranks (strong scaling) with
+expert parallelism (ep.py).  Random-init weights and x ~ N(0,1); router bias
+log p_zipf(s) makes routing Zipf-skewed.
+
+``--impl reference`` times the reference's CPU path (the oracle port in
+oracle/: C scheduler + numpy numeric restatement; the reference itself is a
+Python count-only simulator that cannot run the numeric block) on the host
+cores, on a bounded token sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOADS = {
+    # name: (d_model, d_ff, E, top_k, activation, T_total)
+    "qwen128": (2048, 768, 128, 8, "swiglu", 16384),
+    "switch128": (768, 3072, 128, 1, "relu", 4096),
+    "mixtral8": (4096, 14336, 8, 2, "swiglu", 16384),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="qwen128", choices=sorted(WORKLOADS))
+    ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--q", type=int, default=32)
+    ap.add_argument("--placement", default="round_robin")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int, enabled: bool = True):
+        self.index, self.enabled, self.proc, self.lines = index, enabled, None, []
+
+    def __enter__(self):
+        if self.enabled:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except OSError:
+                self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU side: the oracle port (reference arm + cpu_baseline)
+# ------------------------------------------------------------------------------------------
+class CpuOracleBlock:
+    """The reference's path on the host: oracle C scheduler + numpy restatement of the
+    numeric block (router, per-expert FFN, combine), weights pre-converted to fp32."""
+
+    def __init__(self, wl, seed=0, zipf_s=1.0, q=32):
+        from oracle import moe_oracle as orc
+        from paper_2506_12417_b200.workload import router_bias
+
+        self.orc = orc
+        d, f, E, k, act, T = wl
+        self.d, self.f, self.E, self.k, self.act, self.q = d, f, E, k, act, q
+        rng = np.random.default_rng(seed)
+        # weights only set the amount of work here (timing), so they are drawn directly in fp32
+        r32 = lambda *shape, s=1.0: rng.standard_normal(shape, dtype=np.float32) * np.float32(s)  # noqa
+        self.wg = r32(E, d, s=(1.0 / d) ** 0.5)
+        self.w1 = r32(E, f, d, s=0.02)
+        self.w3 = r32(E, f, d, s=0.02) if act == "swiglu" else None
+        self.w2 = r32(E, d, f, s=0.02)
+        self.bias = router_bias(E, zipf_s)
+        self.home = orc.round_robin_home(E, 1)
+
+    def step(self, x):
+        orc = self.orc
+        logits = x @ self.wg.T + self.bias[None, :]
+        idx = orc.topk_lowest_index(logits, self.k)
+        mx = logits.max(axis=1, keepdims=True)
+        ex = np.exp(logits - mx)
+        p = ex / ex.sum(axis=1, keepdims=True)
+        w = np.take_along_axis(p, idx, axis=1)
+        if self.k > 1:
+            w = w / w.sum(axis=1, keepdims=True)
+        hist = np.bincount(idx.reshape(-1), minlength=self.E)[None, :]
+        orc.schedule(hist, self.home, self.q, True)
+        y = np.zeros_like(x)
+        for e in np.nonzero(hist[0])[0]:
+            t, j = np.nonzero(idx == e)
+            a = x[t] @ self.w1[e].T
+            if self.act == "swiglu":
+                h = a / (1.0 + np.exp(-a)) * (x[t] @ self.w3[e].T)
+            else:
+                h = np.maximum(a, 0)
+            y[t] += w[t, j][:, None] * (orc.round_bf16(h) @ self.w2[e].T)
+        return y
+
+
+def cpu_measure(wl, sample_tokens, seconds=None, steps=None, warmup=1, zipf_s=1.0, q=32):
+    blk = CpuOracleBlock(wl, zipf_s=zipf_s, q=q)
+    rng = np.random.default_rng(1)
+    x = blk.orc.round_bf16(rng.standard_normal((sample_tokens, wl[0])).astype(np.float32))
+    for _ in range(warmup):
+        blk.step(x)
+    times = []
+    t_end = time.perf_counter() + (seconds or 0)
+    while True:
+        t0 = time.perf_counter()
+        blk.step(x)
+        times.append(time.perf_counter() - t0)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and time.perf_counter() >= t_end:
+            break
+    return times
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    wl = WORKLOADS[args.workload]
+    if rank != 0:
+        return
+    sample = 256
+    times = cpu_measure(wl, sample, steps=args.steps, warmup=args.warmup, zipf_s=args.zipf, q=args.q)
+    per_step = float(np.mean(times))
+    value = sample / per_step
+    cores = cpu_cores()
+    line = {
+        "impl": "reference", "metric": "moe_block_tokens_per_sec", "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16-in/fp32",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload} MoE layer, Zipf s={args.zipf}, CPU oracle port on {sample} tokens/step",
+                   "d_model": wl[0], "d_ff": wl[1], "experts": wl[2], "top_k": wl[3], "tokens": wl[5]},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} tokens of the {args.workload} batch per step (numpy/OpenBLAS "
+                                   f"restatement + C scheduler oracle)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+# GPU side
+# ------------------------------------------------------------------------------------------
+def algorithmic_work(wl, tokens):
+    """FLOPs and HBM bytes of the expert GEMMs for `tokens` input tokens."""
+    d, f, E, k, act, _ = wl
+    n_in = 2 * f if act == "swiglu" else f
+    a = tokens * k
+    f1 = 2.0 * a * d * n_in
+    f2 = 2.0 * a * f * d
+    w_bytes = E * (n_in * d + d * f) * 2
+    act_bytes = a * d * 2 * 2 + a * f * 2 * 2  # A read + Y write (gemm2) ; H write + read
+    return f1, f2, w_bytes, act_bytes
+
+
+def load_ratio_logical(block_cls, cfg_kw, x, G, q, placement, zipf_s, seed, dev):
+    """max/mean load of HarMoEny's schedule when the same batch is split over G ranks."""
+    from paper_2506_12417_b200.block import MoEConfig
+
+    cfg = MoEConfig(logical_ranks=G, eq_tokens=q, placement=placement, **cfg_kw)
+    out = {}
+    for pol in ("harmony", "round_robin"):
+        cfg.scheduling_policy = pol
+        blk = block_cls.random(cfg, seed=seed, device=dev, zipf_s=zipf_s)
+        blk(x)
+        out[pol] = blk.stats.load_imbalance()
+    return out
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
+
+    wl = WORKLOADS[args.workload]
+    d, f, E, k, act, T_total = wl
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    cfg_kw = dict(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act)
+    if world > 1:
+        from paper_2506_12417_b200.ep import EPHarMoEnyBlock
+
+        cfg = MoEConfig(rank=rank, world_size=world, eq_tokens=args.q, placement=args.placement, **cfg_kw)
+        blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
+    else:
+        cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, **cfg_kw)
+        blk = HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
+    T_local = T_total // world
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn((T_local, d), device=dev, generator=g).to(torch.bfloat16)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        blk(x)
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: inputs resident in HBM, L2 flushed between steps ----
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    all_marks = []
+    sampler = ClockSampler(local_rank, enabled=not args.no_clocks)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        time.sleep(0.25 if not args.no_clocks else 0)
+        for i in range(args.steps):
+            flush.fill_(i)
+            marks = []
+            starts[i].record(stream)
+            blk(x, marks=marks)
+            ends[i].record(stream)
+            all_marks.append(marks)
+        torch.cuda.synchronize()
+        barrier()
+    step_ms = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)])
+    stage_ms = {}
+    for marks in all_marks:
+        for (n0, e0), (n1, e1) in zip(marks[:-1], marks[1:]):
+            stage_ms.setdefault(n1, []).append(e0.elapsed_time(e1))
+    stage_us = {n: float(np.mean(v)) * 1e3 for n, v in stage_ms.items()}
+    t_step = float(step_ms.sum())  # ms for K steps on this rank
+    if world > 1:
+        t = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(t.item())
+    ms_per_step = t_step / args.steps
+    value = T_total * args.steps / (t_step / 1e3)
+
+    # ---- end to end through the public API with host buffers ----
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty((T_local, d), dtype=torch.bfloat16, pin_memory=True)
+    for _ in range(3):
+        blk.forward_host(x_host, y_host)
+    torch.cuda.synchronize()
+    e_steps = max(3, min(args.steps, 30))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(e_steps):
+        blk.forward_host(x_host, y_host)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e_value = T_total * e_steps / (e_ms / 1e3)
+    nbytes = T_local * d * 2
+
+    if rank != 0:
+        return
+    hbm, tc, tc_sus, peak_kind = peaks()
+    f1, f2, w_bytes, act_bytes = algorithmic_work(wl, T_total // world)
+    g1_us = stage_us.get("gemm1", float("nan"))
+    achieved = f1 / (g1_us * 1e-6) / 1e12
+    traffic = None
+    prof = os.path.join(REPO, "profiles", f"ncu_{args.workload}_gemm1.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    # block roofline: expert GEMMs only (the dominant term), tokens / max(F/P_tc, B/P_hbm)
+    t_roof = max((f1 + f2) / (tc * 1e12), (w_bytes + act_bytes) / (hbm * 1e9))
+    roof_tokens = (T_total // world) / t_roof * world
+    loads = {}
+    if world == 1 and args.gpus == 1:
+        loads = load_ratio_logical(HarMoEnyBlock, cfg_kw, x, 8, args.q, "blocked", args.zipf, 0, dev)
+    cpu = None
+    if not args.no_cpu_baseline:
+        sample = 256
+        times = cpu_measure(wl, sample, seconds=args.cpu_seconds, zipf_s=args.zipf, q=args.q)
+        cpu = {"value": sample / float(np.mean(times)), "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+               "sample": f"{sample}-token slices of the {args.workload} batch, {len(times)} reps "
+                         f"(~{args.cpu_seconds:.0f}s; numpy/OpenBLAS restatement + C scheduler oracle)"}
+    line = {
+        "metric": "moe_block_tokens_per_sec", "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {
+            "workload": f"{args.workload} MoE layer (BASELINE configs[1]), {T_total} tokens, Zipf s={args.zipf} router "
+                        f"bias, random-init weights",
+            "d_model": d, "d_ff": f, "experts": E, "top_k": k, "activation": act, "tokens": T_total,
+            "q": args.q, "placement": args.placement, "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+            "l2": "flushed between timed steps (256 MB write)",
+            "stages_us": stage_us,
+            "block_roofline_tokens_per_sec": roof_tokens,
+            "block_roofline_frac": value / roof_tokens,
+            "peak_kind": peak_kind, "bf16_tflops_sustained": tc_sus,
+            "load_max_over_mean_G8_logical": loads or None,
+        },
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
+                     "frac": achieved / tc, "traffic": traffic,
+                     "kernel": "grouped_gemm_kernel<SwiGLU> (expert FFN1)",
+                     "work_per_launch": f"{f1 / 1e9:.1f} GFLOP = 2 * {T_total // world * k} rows * {d} * {2 * f if act == 'swiglu' else f}"},
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+        "gpu_launches": HarMoEnyBlock.KERNELS_PER_FORWARD * args.steps,
+        "clocks": sampler.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if world > 1 and rank != 0:
+            return
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -160,7 +160,9 @@ class HarMoEnyBlock:
         return cls(cfg, wg, w1, w2, w3, bias, device=device)
 
     # ------------------------------------------------------------------------------------
-    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, stream=None, marks: list | None = None) -> torch.Tensor:
+        """y = MoE(x) for x [T, d] bf16 on this device.  ``marks``, if given, receives
+        (stage, cuda.Event) pairs recorded after each stage (bench instrumentation)."""
         cfg = self.cfg
         if x.dim() != 2 or x.shape[1] != cfg.d_model:
             raise ValueError(f"x must be [T, {cfg.d_model}]")
@@ -174,17 +176,47 @@ class HarMoEnyBlock:
         k = cfg.top_k
         tiles_per_rank = (Tg + ops.TILE_M - 1) // ops.TILE_M
         x = x.contiguous()
-        idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, G, Tg, k, cfg.renormalize, stream=stream)
-        m_all, tile_off = ops.hist_scan(tile_hist, G, tiles_per_rank, stream=stream)
-        S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=stream)
-        lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_LOCAL, stream=stream)
-        xs, pos = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, G, Tg, 0, T * k, stream=stream)
-        h = ops.grouped_gemm(xs, self.w_in, self.n_in, lay, self.epi_in, stream=stream)
-        ys = ops.grouped_gemm(h, self.w_out, cfg.d_model, lay, ops.HM_EPI_STORE, stream=stream)
-        y = ops.combine(ys, pos, w, stream=stream)
+        s = stream if stream is not None else torch.cuda.current_stream()
+
+        def mark(name):
+            if marks is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                marks.append((name, ev))
+
+        mark("start")
+        idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, G, Tg, k, cfg.renormalize,
+                                                   E=cfg.num_experts, stream=s)
+        mark("router")
+        m_all, tile_off = ops.hist_scan(tile_hist, G, tiles_per_rank, stream=s)
+        S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=s)
+        lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_LOCAL, stream=s)
+        mark("schedule")
+        xs, pos = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, G, Tg, 0, T * k, stream=s)
+        mark("permute")
+        h = ops.grouped_gemm(xs, self.w_in, self.n_in, lay, self.epi_in, stream=s)
+        mark("gemm1")
+        ys = ops.grouped_gemm(h, self.w_out, cfg.d_model, lay, ops.HM_EPI_STORE, stream=s)
+        mark("gemm2")
+        y = ops.combine(ys, pos, w, stream=s)
+        mark("combine")
         self.stats = BlockStats(m_all=m_all, schedule=S, iters=iters, loads=loads,
                                 extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay, lrank=lrank,
                                             tile_off=tile_off))
         return y
+
+    KERNELS_PER_FORWARD = 8  # router, hist_scan, schedule, layout, permute, gemm1, gemm2, combine
+
+    def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Public end-to-end call with host buffers: H2D of x (pinned -> HBM), the block,
+        D2H of y into pinned host memory.  Stream-ordered; sync before reading y_host."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            x = x_host.to(self.device, non_blocking=True)
+            y = self.forward(x, stream=s)
+            if y_host is None:
+                y_host = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+            y_host.copy_(y, non_blocking=True)
+        return y_host
 
     __call__ = forward

@@ -37,7 +37,8 @@ def e_pad(E: int) -> int:
     return (E + 15) // 16 * 16
 
 
-def router_topk(x, wg, bias, n_ranks: int, tokens_per_rank: int, k: int, renormalize: bool, stream=None):
+def router_topk(x, wg, bias, n_ranks: int, tokens_per_rank: int, k: int, renormalize: bool, E: int | None = None,
+                stream=None):
     """K1+K2.  x [n_ranks*T_g, d] bf16, wg [E_pad, d] bf16 (rows >= E are zero padding), bias [E] fp32|None.
     Returns topk_idx [T,k] i32, topk_w [T,k] f32, tile_hist [tiles, E] i32, lrank [T,k] i32."""
     _require_cuda(x, wg, bias)
@@ -46,7 +47,10 @@ def router_topk(x, wg, bias, n_ranks: int, tokens_per_rank: int, k: int, renorma
     T, d = x.shape
     if T != n_ranks * tokens_per_rank:
         raise ValueError("x rows must equal n_ranks * tokens_per_rank")
-    E = bias.numel() if bias is not None else wg.shape[0]
+    if E is None:
+        E = bias.numel() if bias is not None else wg.shape[0]
+    if bias is not None and bias.numel() != E:
+        raise ValueError("bias must have E entries")
     if wg.shape[0] != e_pad(E) or wg.shape[1] != d:
         raise ValueError(f"wg must be [E_pad={e_pad(E)}, d]")
     tiles = n_ranks * ((tokens_per_rank + TILE_M - 1) // TILE_M)

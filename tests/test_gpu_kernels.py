@@ -139,7 +139,7 @@ def test_router_topk_hist(E, k, d, n_ranks, Tg, bias, integer):
             b = np.round(b).astype(np.float32)
         b_t = torch.from_numpy(b).to(dev)
     renorm = k > 1
-    idx, w, tile_hist, lrank = ops.router_topk(x_t, w_t, b_t, n_ranks, Tg, k, renorm)
+    idx, w, tile_hist, lrank = ops.router_topk(x_t, w_t, b_t, n_ranks, Tg, k, renorm, E=E)
     torch.cuda.synchronize()
     idx = idx.cpu().numpy()
     logits, idx_ref, w_ref = orc.router(xb, wb, b, k, renorm)
@@ -295,11 +295,11 @@ def test_dispatch_positions_follow_contract():
     from paper_2506_12417_b200.block import MoEConfig
 
     dev = _cuda()
-    cfg = MoEConfig(logical_ranks=4, eq_tokens=1, placement="blocked", d_model=128, num_experts=16, d_ff=256,
+    cfg = MoEConfig(logical_ranks=4, eq_tokens=1, placement="blocked", d_model=256, num_experts=16, d_ff=256,
                     top_k=2, activation="swiglu")
     blk = _block(cfg, seed=5, dev=dev, zipf_s=1.2)
     T = 1024
-    x = torch.randn((T, 128), device=dev).to(torch.bfloat16)
+    x = torch.randn((T, 256), device=dev).to(torch.bfloat16)
     blk(x)
     torch.cuda.synchronize()
     st = blk.stats
