@@ -120,20 +120,23 @@ HM_API int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int 
  * Scatter (K4): copy token rows to their scheduled buffer rows (one read of x, k 128-bit-vector
  * writes).  Token t's source rank is src_rank_base + t / tokens_per_rank; its r-th assignment to
  * expert e goes to the first dest d with cumsum_d S[src,e,d] > r (split-bucket contract).
- *   out [rows, d] bf16, pos [T, k] int32 (row index of each assignment in `out`).
+ *   out [rows, d] bf16, pos [T, k] int32 (row index of each assignment in `out`),
+ *   inv [rows] int32 or NULL: inverse map, inv[pos[t,j]] = t*k + j (lets the FFN2 epilogue write
+ *   its rows token-major so the combine streams contiguous memory).
  */
 HM_API int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
                const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base,
-               int G, int E, int k, int d, void* out, int32_t* pos, void* stream);
+               int G, int E, int k, int d, void* out, int32_t* pos, int32_t* inv, void* stream);
 
 /*
  * Grouped expert GEMM (K5), tcgen05/TMEM/TMA: for every segment, out[rows] = epi(A[rows] W[wslot]^T).
  *   A [a_rows, K] bf16; W [w_rows, K] bf16 with w_rows = slots*N; out [a_rows, N] (or N/2 for SWIGLU).
+ *   row_map [a_rows] int32 or NULL: output row of A-row r is row_map[r] (scatter epilogue).
  *   slot_ready [slots] int32 or NULL: tiles of slot s >= ready_from_slot wait for slot_ready[s] >= epoch.
  * Requires N % 256 == 0, K % 64 == 0.
  */
 HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
-                    const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out,
+                    const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out, const int32_t* row_map,
                     const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream);
 
 /*
@@ -144,6 +147,8 @@ HM_API int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* re
 
 /*
  * Combine (K7): y[t] = sum_j w[t,j] * Y[pos[t,j]] in fp32, slots in order j = 0..k-1, bf16 out.
+ * pos == NULL means Y is token-major [T*k, d] (row t*k + j), the layout the FFN2 epilogue writes
+ * through row_map.
  */
 HM_API int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y,
                void* stream);

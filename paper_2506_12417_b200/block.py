@@ -192,13 +192,16 @@ class HarMoEnyBlock:
         S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=s)
         lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_LOCAL, stream=s)
         mark("schedule")
-        xs, pos = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, G, Tg, 0, T * k, stream=s)
+        xs, pos, inv = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, G, Tg, 0, T * k, with_inverse=True,
+                                   stream=s)
         mark("permute")
         h = ops.grouped_gemm(xs, self.w_in, self.n_in, lay, self.epi_in, stream=s)
         mark("gemm1")
-        ys = ops.grouped_gemm(h, self.w_out, cfg.d_model, lay, ops.HM_EPI_STORE, stream=s)
+        # FFN2 scatters its rows token-major (row_map = inverse permutation) so the
+        # combine reads each token's k expert outputs as one contiguous block
+        ys = ops.grouped_gemm(h, self.w_out, cfg.d_model, lay, ops.HM_EPI_STORE, row_map=inv, stream=s)
         mark("gemm2")
-        y = ops.combine(ys, pos, w, stream=s)
+        y = ops.combine(ys, None, w, stream=s)
         mark("combine")
         self.stats = BlockStats(m_all=m_all, schedule=S, iters=iters, loads=loads,
                                 extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay, lrank=lrank,

@@ -80,7 +80,7 @@ int launch_rebalance(int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
 int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
                   int32_t*, int32_t*, cudaStream_t);
 int launch_permute(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int,
-                   int, int, int, int, int, int, void*, int32_t*, cudaStream_t);
+                   int, int, int, int, int, int, void*, int32_t*, int32_t*, cudaStream_t);
 int launch_combine(const void*, const int32_t*, const float*, int, int, int, void*, cudaStream_t);
 
 __global__ void publish_flag_kernel(int32_t* flag, int epoch) {
@@ -134,16 +134,16 @@ int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int E, int 
 
 int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
                const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base, int G,
-               int E, int k, int d, void* out, int32_t* pos, void* stream) {
+               int E, int k, int d, void* out, int32_t* pos, int32_t* inv, void* stream) {
   return launch_permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks, tokens_per_rank, src_rank_base, G, E, k,
-                        d, out, pos, as_stream(stream));
+                        d, out, pos, inv, as_stream(stream));
 }
 
 int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
                     const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out,
-                    const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream) {
-  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, slot_ready,
-                             ready_from_slot, epoch, as_stream(stream));
+                    const int32_t* row_map, const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream) {
+  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, row_map,
+                             slot_ready, ready_from_slot, epoch, as_stream(stream));
 }
 
 int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_flag, int epoch, void* stream) {

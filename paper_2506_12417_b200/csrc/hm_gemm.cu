@@ -13,14 +13,19 @@
 //   residents first, then fetched experts) so async weight fetches (K6) get the
 //   longest possible compute shadow.
 //
-// Warp roles (192 threads): warp0 = TMA producer, warp1 = MMA issuer (one
-// elected thread) + TMEM owner, warps2-5 = epilogue (TMEM -> regs -> global).
-// 4-stage smem ring (48 KB/stage), 2 TMEM accumulators of 256 fp32 columns so
-// the epilogue of tile i overlaps the MMAs of tile i+1.
+// Warp roles (320 threads): warp0 = TMA producer, warp1 = MMA issuer (one
+// elected thread) + TMEM owner, warps2-9 = epilogue.  4-stage smem ring
+// (48 KB/stage); 2 TMEM accumulators of 256 fp32 columns so the epilogue of
+// tile i overlaps the MMAs of tile i+1.
 //
-// Epilogues: kEpiStore (bf16 out), kEpiRelu (Switch FFN1), kEpiSwiGLU (W13 is
-// block-interleaved: within each 256-row block, rows [0,128) are gate rows and
-// [128,256) the matching up rows -> 128 bf16 outputs per tile).
+// Epilogue: epilogue warp w owns TMEM lane quarter w%4 (32 rows) and one half
+// of the tile's columns.  Each thread converts its row (TMEM -> regs -> bf16)
+// into a padded per-warp smem staging tile, then the warp writes whole 128-byte
+// row segments (4 rows per instruction), optionally scattered through row_map
+// (the FFN2 output goes token-major so the combine streams contiguously).
+//   kEpiStore (bf16 out), kEpiRelu (Switch FFN1), kEpiSwiGLU (W13 is block-
+//   interleaved: within each 256-row block, rows [0,128) are gate rows and
+//   [128,256) the matching up rows -> 128 bf16 outputs per tile).
 #include "hm_common.cuh"
 #include "hm_internal.h"
 
@@ -33,31 +38,73 @@ constexpr int kStages = 4;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr uint32_t kBBytes = kBN * kBK * 2;  // 32 KB
 constexpr uint32_t kTmemCols = 512;
-constexpr int kGemmThreads = 192;
-constexpr size_t kGemmSmem = 1024 + kStages * (kABytes + kBBytes) + 256;
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 64 + kEpiWarps * 32;
+constexpr int kMaxSmemSegs = 512;                 // segment table staged in smem (10 KB) when it fits
+constexpr int kStgCols = 32;                      // bf16 output columns per staging pass
+constexpr int kStgPitch = kStgCols * 2 + 16;      // 80 B: conflict-free 16-byte row writes
+constexpr int kStgBytes = 32 * kStgPitch;         // per epilogue warp
+constexpr size_t kGemmSmem =
+    1024 + kStages * (kABytes + kBBytes) + 256 + kMaxSmemSegs * 20 + 16 + kEpiWarps * kStgBytes;
 
-__device__ __forceinline__ void decode_tile(int t, int NB, const int4* __restrict__ segs,
-                                            const int* __restrict__ mprefix, int n_seg, int4& seg, int& m, int& nb) {
-  // largest s with mprefix[s] * NB <= t
-  int lo = 0, hi = n_seg - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (mprefix[mid] * NB <= t) lo = mid;
-    else hi = mid - 1;
+// Persistent tile walk.  Tile t (increasing per CTA) -> segment via a monotone
+// cursor (amortised O(1), no dependent global-memory search per tile).
+struct TileCursor {
+  const int4* segs;
+  const int* mp;
+  int NB;
+  int s = 0;
+  __device__ __forceinline__ void seek(int t, int4& seg, int& m, int& nb) {
+    while (mp[s + 1] * NB <= t) ++s;
+    seg = segs[s];
+    const int ms = mp[s + 1] - mp[s];
+    const int local = t - mp[s] * NB;
+    nb = local / ms;
+    m = local - nb * ms;
   }
-  seg = segs[lo];
-  const int ms = mprefix[lo + 1] - mprefix[lo];
-  const int local = t - mprefix[lo] * NB;
-  nb = local / ms;
-  m = local - nb * ms;
+};
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// Convert 32 fp32 accumulator columns of this thread's row to bf16 and store them
+// (64 B) into the warp's staging row.
+template <int kEpi>
+__device__ __forceinline__ void stage_row(uint32_t srow, const uint32_t (&a)[32], const uint32_t (&u)[32]) {
+#pragma unroll
+  for (int v = 0; v < 4; ++v) {
+    uint32_t pk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = v * 8 + j * 2;
+      float x0 = __uint_as_float(a[c]), x1 = __uint_as_float(a[c + 1]);
+      if constexpr (kEpi == kEpiRelu) {
+        x0 = fmaxf(x0, 0.0f);
+        x1 = fmaxf(x1, 0.0f);
+      } else if constexpr (kEpi == kEpiSwiGLU) {
+        const float u0 = __uint_as_float(u[c]), u1 = __uint_as_float(u[c + 1]);
+        x0 = x0 / (1.0f + __expf(-x0)) * u0;
+        x1 = x1 / (1.0f + __expf(-x1)) * u1;
+      }
+      pk[j] = pack_bf16x2(x0, x1);
+    }
+    st_shared_v4(srow + v * 16, pk[0], pk[1], pk[2], pk[3]);
+  }
 }
 
 template <int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                        const int4* __restrict__ segs, const int* __restrict__ mprefix,
+                        const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
                         const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K, int ldo,
-                        const int* __restrict__ slot_ready, int ready_from_slot, int epoch) {
+                        const int* __restrict__ row_map, const int* __restrict__ slot_ready, int ready_from_slot,
+                        int epoch) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -67,9 +114,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int4* s_segs = reinterpret_cast<int4*>(smem_b + kStages * kBBytes + 256);
+  int* s_mp = reinterpret_cast<int*>(s_segs + kMaxSmemSegs);
+  uint8_t* s_stage = reinterpret_cast<uint8_t*>(s_mp + kMaxSmemSegs + 4);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const int n_seg = *n_seg_ptr;
+  const bool seg_in_smem = n_seg <= kMaxSmemSegs;
+  if (seg_in_smem) {
+    for (int i = threadIdx.x; i < n_seg; i += blockDim.x) s_segs[i] = segs_g[i];
+    for (int i = threadIdx.x; i <= n_seg; i += blockDim.x) s_mp[i] = mprefix_g[i];
+  }
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -78,7 +134,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], kEpiWarps);
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmap_a);
@@ -90,9 +146,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int n_seg = *n_seg_ptr;
   const int NB = N / kBN;
-  const int total = n_seg > 0 ? mprefix[n_seg] * NB : 0;
+  const int4* segs = seg_in_smem ? s_segs : segs_g;
+  const int* mp = seg_in_smem ? s_mp : mprefix_g;
+  const int total = n_seg > 0 ? mp[n_seg] * NB : 0;
   const int KB = K / kBK;
 
   if (warp == 0) {
@@ -100,12 +157,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ===== TMA producer =====
       const uint64_t pol_a = l2_policy_evict_normal();
       const uint64_t pol_b = l2_policy_evict_last();
+      TileCursor cur{segs, mp, NB};
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         int4 seg;
         int m, nb;
-        decode_tile(t, NB, segs, mprefix, n_seg, seg, m, nb);
+        cur.seek(t, seg, m, nb);
         const int row0 = seg.x + m * kBM;
         const int brow = seg.z * N + nb * kBN;
         if (slot_ready != nullptr && seg.z >= ready_from_slot) {
@@ -157,67 +215,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ===== epilogue: warps 2..5, TMEM lane quarter = warp % 4 =====
-    const int q = warp & 3;
-    const int r_in_tile = q * 32 + lane;
+    // ===== epilogue: warps 2..9 =====
+    const int ew = warp - 2;             // 0..7
+    const int q = warp & 3;              // TMEM lane quarter (hardware: warp id % 4)
+    const int half = ew >> 2;            // which half of the tile's output columns
+    constexpr int kOutCols = (kEpi == kEpiSwiGLU) ? kBN / 2 : kBN;  // bf16 outputs per tile row
+    constexpr int kHalfCols = kOutCols / 2;
+    const uint32_t stg = smem_u32(s_stage + ew * kStgBytes);
+    const uint32_t my_srow = stg + lane * kStgPitch;
+    TileCursor cur{segs, mp, NB};
     int i = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
       int4 seg;
       int m, nb;
-      decode_tile(t, NB, segs, mprefix, n_seg, seg, m, nb);
+      cur.seek(t, seg, m, nb);
       const int rows = min(kBM, seg.y - m * kBM);
+      const int r_in_tile = q * 32 + lane;
       const bool valid = r_in_tile < rows;
-      const int64_t row = (int64_t)seg.x + m * kBM + r_in_tile;
+      int64_t row = (int64_t)seg.x + m * kBM + r_in_tile;
+      if (row_map != nullptr && valid) row = __ldg(row_map + row);
+      const int64_t obase = row * ldo + (int64_t)nb * kOutCols + half * kHalfCols;  // element offset
+      const int nvalid = max(0, min(32, rows - q * 32));                            // valid rows of this warp
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16);
-      if constexpr (kEpi == kEpiSwiGLU) {
-        __nv_bfloat16* orow = out + row * ldo + nb * (kBN / 2);
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t g[32], u[32];
-          tmem_ld_32x32b_x32(taddr + c * 32, g);
-          tmem_ld_32x32b_x32(taddr + 128 + c * 32, u);
-          tmem_ld_wait();
-          uint32_t pk[16];
+      for (int c0 = 0; c0 < kHalfCols; c0 += kStgCols) {
+        uint32_t a[32], u[32];
+        const int col = half * kHalfCols + c0;  // output column within the tile
+        tmem_ld_32x32b_x32(taddr + col, a);
+        if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + 128 + col, u);
+        tmem_ld_wait();
+        stage_row<kEpi>(my_srow, a, u);
+        __syncwarp();
+        // warp writes its 32 staged rows: 4 lanes x 16 B per row -> 8 rows per instruction
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float g0 = __uint_as_float(g[2 * j]), g1 = __uint_as_float(g[2 * j + 1]);
-            float u0 = __uint_as_float(u[2 * j]), u1 = __uint_as_float(u[2 * j + 1]);
-            float h0 = g0 / (1.0f + __expf(-g0)) * u0;
-            float h1 = g1 / (1.0f + __expf(-g1)) * u1;
-            pk[j] = pack_bf16x2(h0, h1);
-          }
-          if (valid) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              st_global_v4(orow + c * 32 + v * 8, pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2);
+          const int piece = lane & 3;
+          const int64_t ob = __shfl_sync(0xffffffffu, obase, rr);
+          if (rr < nvalid) {
+            const uint4 v = ld_shared_v4(stg + rr * kStgPitch + piece * 16);
+            st_global_v4(out + ob + c0 + piece * 8, v.x, v.y, v.z, v.w);
           }
         }
-      } else {
-        __nv_bfloat16* orow = out + row * ldo + nb * kBN;
-#pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
-          uint32_t a[32];
-          tmem_ld_32x32b_x32(taddr + c * 32, a);
-          tmem_ld_wait();
-          uint32_t pk[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float x0 = __uint_as_float(a[2 * j]), x1 = __uint_as_float(a[2 * j + 1]);
-            if constexpr (kEpi == kEpiRelu) {
-              x0 = fmaxf(x0, 0.0f);
-              x1 = fmaxf(x1, 0.0f);
-            }
-            pk[j] = pack_bf16x2(x0, x1);
-          }
-          if (valid) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              st_global_v4(orow + c * 32 + v * 8, pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
-          }
-        }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -235,8 +278,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                         const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
-                        void* out, const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream) {
-  if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0) return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
+                        void* out, const int32_t* row_map, const int32_t* slot_ready, int ready_from_slot, int epoch,
+                        cudaStream_t stream) {
+  if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
+    return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
   if (a_rows <= 0) return HM_OK;
   CUtensorMap ta, tb;
@@ -248,25 +293,19 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
   const int grid = num_sms();
   const int4* s4 = reinterpret_cast<const int4*>(segs);
   auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+#define HM_GEMM(EPI)                                                                                         \
+  do {                                                                                                       \
+    cudaFuncSetAttribute(grouped_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem); \
+    grouped_gemm_kernel<EPI><<<grid, kGemmThreads, kGemmSmem, stream>>>(                                    \
+        ta, tb, s4, mtile_prefix, n_seg, o, N, K, ldo, row_map, slot_ready, ready_from_slot, epoch);         \
+  } while (0)
   switch (epilogue) {
-    case kEpiStore:
-      cudaFuncSetAttribute(grouped_gemm_kernel<kEpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      grouped_gemm_kernel<kEpiStore><<<grid, kGemmThreads, kGemmSmem, stream>>>(
-          ta, tb, s4, mtile_prefix, n_seg, o, N, K, ldo, slot_ready, ready_from_slot, epoch);
-      break;
-    case kEpiRelu:
-      cudaFuncSetAttribute(grouped_gemm_kernel<kEpiRelu>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      grouped_gemm_kernel<kEpiRelu><<<grid, kGemmThreads, kGemmSmem, stream>>>(
-          ta, tb, s4, mtile_prefix, n_seg, o, N, K, ldo, slot_ready, ready_from_slot, epoch);
-      break;
-    case kEpiSwiGLU:
-      cudaFuncSetAttribute(grouped_gemm_kernel<kEpiSwiGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-      grouped_gemm_kernel<kEpiSwiGLU><<<grid, kGemmThreads, kGemmSmem, stream>>>(
-          ta, tb, s4, mtile_prefix, n_seg, o, N, K, ldo, slot_ready, ready_from_slot, epoch);
-      break;
-    default:
-      return set_error(HM_EINVAL, "grouped_gemm: unknown epilogue");
+    case kEpiStore: HM_GEMM(kEpiStore); break;
+    case kEpiRelu: HM_GEMM(kEpiRelu); break;
+    case kEpiSwiGLU: HM_GEMM(kEpiSwiGLU); break;
+    default: return set_error(HM_EINVAL, "grouped_gemm: unknown epilogue");
   }
+#undef HM_GEMM
   return check_launch("grouped_gemm");
 }
 

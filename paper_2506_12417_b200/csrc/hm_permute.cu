@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kPermWarps * 32)
                    const int32_t* __restrict__ lrank, const int32_t* __restrict__ tile_off,
                    const int32_t* __restrict__ S, const int32_t* __restrict__ slot_base, int64_t T,
                    int tokens_per_rank, int tiles_per_rank, int src_rank_base, int G, int E, int k, int n16,
-                   uint4* __restrict__ out, int32_t* __restrict__ pos) {
+                   uint4* __restrict__ out, int32_t* __restrict__ pos, int32_t* __restrict__ inv) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
   if (t >= T) return;
@@ -52,7 +52,10 @@ __global__ void __launch_bounds__(kPermWarps * 32)
       c += s;
     }
     const int64_t p = (int64_t)__ldg(slot_base + ((int64_t)g * E + e) * G + d) + (r - c);
-    if (lane == 0) pos[t * k + j] = (int32_t)p;
+    if (lane == 0) {
+      pos[t * k + j] = (int32_t)p;
+      if (inv != nullptr) inv[p] = (int32_t)(t * k + j);
+    }
     uint4* dst = out + p * n16;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
@@ -62,6 +65,8 @@ __global__ void __launch_bounds__(kPermWarps * 32)
   }
 }
 
+// Gather combine: rows addressed through pos (EP path: rows come back through the
+// all_to_all in the send layout).
 template <int VEC>
 __global__ void __launch_bounds__(kPermWarps * 32)
     combine_kernel(const uint4* __restrict__ Y, const int32_t* __restrict__ pos, const float* __restrict__ w,
@@ -102,9 +107,49 @@ __global__ void __launch_bounds__(kPermWarps * 32)
   }
 }
 
+// Dense combine: Y is token-major [T*k, d] (the FFN2 epilogue scattered its rows there),
+// so token t's k rows are one contiguous k*d*2-byte block.  One warp per token; for every
+// 16-byte column chunk the k row loads are issued back to back (KT unrolled).
+template <int KT>
+__global__ void __launch_bounds__(kPermWarps * 32)
+    combine_dense_kernel(const uint4* __restrict__ Y, const float* __restrict__ w, int64_t T, int k, int n16,
+                         uint4* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int kk = KT > 0 ? KT : k;
+  float wj[KT > 0 ? KT : 16];
+#pragma unroll
+  for (int j = 0; j < (KT > 0 ? KT : 16); ++j) wj[j] = (j < kk) ? __ldg(w + t * kk + j) : 0.0f;
+  const uint4* base = Y + t * kk * n16;
+  uint4* dst = y + t * n16;
+  for (int c = lane; c < n16; c += 32) {
+    uint4 u[KT > 0 ? KT : 16];
+#pragma unroll
+    for (int j = 0; j < (KT > 0 ? KT : 16); ++j)
+      if (j < kk) u[j] = ld_global_nc_v4(base + (int64_t)j * n16 + c);
+    float acc[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) acc[h] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < (KT > 0 ? KT : 16); ++j) {
+      if (j < kk) {
+        const uint32_t uu[4] = {u[j].x, u[j].y, u[j].z, u[j].w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          acc[2 * h] = __fadd_rn(acc[2 * h], __fmul_rn(wj[j], bf16lo(uu[h])));
+          acc[2 * h + 1] = __fadd_rn(acc[2 * h + 1], __fmul_rn(wj[j], bf16hi(uu[h])));
+        }
+      }
+    }
+    dst[c] = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                        pack_bf16x2(acc[6], acc[7]));
+  }
+}
+
 int launch_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
                    const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base,
-                   int G, int E, int k, int d, void* out, int32_t* pos, cudaStream_t stream) {
+                   int G, int E, int k, int d, void* out, int32_t* pos, int32_t* inv, cudaStream_t stream) {
   if (d <= 0 || d % 8 != 0 || d > 8192) return set_error(HM_EINVAL, "permute: need d %% 8 == 0 and d <= 8192");
   if (n_ranks < 1 || tokens_per_rank < 0 || G < 1 || E < 1 || k < 1)
     return set_error(HM_EINVAL, "permute: bad sizes");
@@ -119,7 +164,7 @@ int launch_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank,
 #define HM_PERM(V)                                                                                              \
   permute_kernel<V><<<grid, kPermWarps * 32, 0, stream>>>(xs, topk_idx, lrank, tile_off, S, slot_base, T,       \
                                                           tokens_per_rank, tiles_per_rank, src_rank_base, G, E, \
-                                                          k, n16, o, pos)
+                                                          k, n16, o, pos, inv)
   if (vec <= 1) HM_PERM(1);
   else if (vec <= 2) HM_PERM(2);
   else if (vec <= 4) HM_PERM(4);
@@ -140,6 +185,17 @@ int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T
   const unsigned grid = (unsigned)((T + kPermWarps - 1) / kPermWarps);
   auto* Ys = reinterpret_cast<const uint4*>(Y);
   auto* o = reinterpret_cast<uint4*>(y);
+  if (pos == nullptr) {
+    if (k > 16) return set_error(HM_EINVAL, "combine: dense layout needs k <= 16");
+#define HM_DENSE(KT) combine_dense_kernel<KT><<<grid, kPermWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, o)
+    if (k == 1) HM_DENSE(1);
+    else if (k == 2) HM_DENSE(2);
+    else if (k == 4) HM_DENSE(4);
+    else if (k == 8) HM_DENSE(8);
+    else HM_DENSE(0);
+#undef HM_DENSE
+    return check_launch("combine_dense");
+  }
 #define HM_COMB(V) combine_kernel<V><<<grid, kPermWarps * 32, 0, stream>>>(Ys, pos, topk_w, T, k, n16, o)
   if (vec <= 1) HM_COMB(1);
   else if (vec <= 2) HM_COMB(2);

@@ -129,8 +129,8 @@ def dispatch_layout(S, home, mode: int, me: int = 0, stream=None) -> Layout:
 
 
 def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per_rank: int, src_rank_base: int,
-            out_rows: int, out=None, stream=None):
-    """K4.  Returns (out [out_rows, d] bf16, pos [T,k] i32)."""
+            out_rows: int, out=None, with_inverse: bool = False, stream=None):
+    """K4.  Returns (out [out_rows, d] bf16, pos [T,k] i32, inv [out_rows] i32 | None)."""
     _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base)
     T, d = x.shape
     k = topk_idx.shape[1]
@@ -138,25 +138,28 @@ def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per
     if out is None:
         out = torch.empty((max(out_rows, 1), d), dtype=x.dtype, device=x.device)
     pos = torch.empty((T, k), dtype=torch.int32, device=x.device)
+    inv = torch.empty(max(out_rows, 1), dtype=torch.int32, device=x.device) if with_inverse else None
     _lib.call("hm_permute", _ptr(x), _ptr(topk_idx), _ptr(lrank), _ptr(tile_off), _ptr(S), _ptr(slot_base),
-              n_ranks, tokens_per_rank, src_rank_base, G, E, k, d, _ptr(out), _ptr(pos), _stream(stream))
-    return out, pos
+              n_ranks, tokens_per_rank, src_rank_base, G, E, k, d, _ptr(out), _ptr(pos), _ptr(inv), _stream(stream))
+    return out, pos, inv
 
 
-def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, slot_ready=None, ready_from_slot: int = 0,
-                 epoch: int = 0, stream=None):
-    """K5.  A [rows, K] bf16, W [slots*N, K] bf16 -> out [rows, N or N/2] bf16."""
+def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=None, slot_ready=None,
+                 ready_from_slot: int = 0, epoch: int = 0, stream=None):
+    """K5.  A [rows, K] bf16, W [slots*N, K] bf16 -> out [rows, N or N/2] bf16
+    (row r written to row_map[r] when a row map is given)."""
     if isinstance(layout_or_segs, Layout):
         segs, n_seg, mprefix = layout_or_segs.segs, layout_or_segs.n_seg, layout_or_segs.mtile_prefix
     else:
         segs, n_seg, mprefix = layout_or_segs
-    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready)
+    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready, row_map)
     rows, K = A.shape
     ncols = N // 2 if epilogue == HM_EPI_SWIGLU else N
     if out is None:
         out = torch.empty((rows, ncols), dtype=torch.bfloat16, device=A.device)
     _lib.call("hm_grouped_gemm", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(segs), _ptr(n_seg), _ptr(mprefix),
-              int(epilogue), _ptr(out), _ptr(slot_ready), int(ready_from_slot), int(epoch), _stream(stream))
+              int(epilogue), _ptr(out), _ptr(row_map), _ptr(slot_ready), int(ready_from_slot), int(epoch),
+              _stream(stream))
     return out
 
 
@@ -169,9 +172,9 @@ def fetch_expert(dst, src, ready_flag=None, epoch: int = 0, stream=None):
 
 
 def combine(Y, pos, topk_w, out=None, stream=None):
-    """K7.  y [T, d] bf16 = sum_j w[t,j] * Y[pos[t,j]]."""
+    """K7.  y [T, d] bf16 = sum_j w[t,j] * Y[pos[t,j]]; pos=None: Y is token-major [T*k, d]."""
     _require_cuda(Y, pos, topk_w)
-    T, k = pos.shape
+    T, k = topk_w.shape
     d = Y.shape[1]
     if out is None:
         out = torch.empty((T, d), dtype=torch.bfloat16, device=Y.device)

@@ -198,7 +198,11 @@ def test_grouped_gemm(epi, N, K):
     W = (torch.randn((E * N, K), device=dev, generator=g) * 0.05).to(torch.bfloat16)
     code = dict(store=ops.HM_EPI_STORE, relu=ops.HM_EPI_RELU, swiglu=ops.HM_EPI_SWIGLU)[epi]
     out = ops.grouped_gemm(A, W, N, lay, code)
+    # scatter epilogue: row r lands at row_map[r]
+    perm = torch.randperm(rows, device=dev, generator=g).to(torch.int32)
+    out_s = ops.grouped_gemm(A, W, N, lay, code, row_map=perm)
     torch.cuda.synchronize()
+    assert torch.equal(out_s[perm.long()], out)
     ref = []
     r0 = 0
     for n, s in zip(counts, wslots):
