@@ -146,6 +146,15 @@ HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t
 HM_API int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_flag, int epoch, void* stream);
 
 /*
+ * Peer-HBM access for K6 over NVLink/NVSwitch: export a device allocation as a 64-byte CUDA IPC
+ * handle (host buffer), open a peer's handle in this process, close it.  The expert-parallel
+ * layer exchanges handles once at setup so every rank can fetch any home expert directly.
+ */
+HM_API int hm_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 B, host */);
+HM_API int hm_ipc_open(const void* handle /* 64 B, host */, void** dev_ptr_out);
+HM_API int hm_ipc_close(void* dev_ptr);
+
+/*
  * Combine (K7): y[t] = sum_j w[t,j] * Y[pos[t,j]] in fp32, slots in order j = 0..k-1, bf16 out.
  * pos == NULL means Y is token-major [T*k, d] (row t*k + j), the layout the FFN2 epilogue writes
  * through row_map.

@@ -146,6 +146,87 @@ def plan_order(work, resident) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------------------------
+# buffer layouts of the scatter (restatement of the contract the device layout kernel follows)
+# --------------------------------------------------------------------------------------------
+def _excl_cumsum(a, axis):
+    c = np.cumsum(a, axis=axis)
+    return c - a
+
+
+def local_positions(idx_all, S, tokens_per_rank: int):
+    """LOCAL layout (all G ranks on one device): buffer [dest][expert][source][rank].
+    Returns pos[T, k] (buffer row of every assignment) and segments in plan order."""
+    S = np.asarray(S, dtype=np.int64)
+    G, E, _ = S.shape
+    n = S.sum(axis=0).T  # [d, e]
+    base = np.concatenate([[0], np.cumsum(n.sum(axis=1))[:-1]])  # [d]
+    off = _excl_cumsum(n, axis=1)  # [d, e]
+    src_pre = _excl_cumsum(S, axis=0)  # [g, e, d]: sum_{g'<g} S[g', e, d]
+    cum_d = _excl_cumsum(S, axis=2)  # [g, e, d]: sum_{d'<d} S[g, e, d']
+    T, k = idx_all.shape
+    pos = np.empty((T, k), np.int64)
+    for g in range(G):
+        sl = slice(g * tokens_per_rank, (g + 1) * tokens_per_rank)
+        e = idx_all[sl].astype(np.int64)
+        dest, rank = dispatch_ranks(idx_all[sl], S, g)
+        dest = dest.reshape(e.shape).astype(np.int64)
+        rank = rank.reshape(e.shape).astype(np.int64)
+        pos[sl] = base[dest] + off[dest, e] + src_pre[g, e, dest] + rank - cum_d[g, e, dest]
+    return pos
+
+
+def local_segments(S, home):
+    S = np.asarray(S, dtype=np.int64)
+    G, E, _ = S.shape
+    n = S.sum(axis=0).T
+    base = np.concatenate([[0], np.cumsum(n.sum(axis=1))[:-1]])
+    off = _excl_cumsum(n, axis=1)
+    segs = []
+    for d in range(G):
+        for e in plan_order(n[d], (np.asarray(home) == d).astype(np.int32)):
+            segs.append((int(base[d] + off[d, e]), int(n[d, e]), int(e), int(e)))
+    return segs
+
+
+def ep_send_positions(idx_local, S, me: int):
+    """EP send buffer of rank `me`: [dest][expert][rank] (NCCL all_to_all chunks)."""
+    S = np.asarray(S, dtype=np.int64)
+    flows_me = S[me].sum(axis=0)  # [d]
+    send_off = np.concatenate([[0], np.cumsum(flows_me)[:-1]])
+    pre_e = _excl_cumsum(S[me], axis=0)  # [e, d]
+    cum_d = _excl_cumsum(S[me], axis=1)  # [e, d]
+    e = idx_local.astype(np.int64)
+    dest, rank = dispatch_ranks(idx_local, S, me)
+    dest = dest.reshape(e.shape).astype(np.int64)
+    rank = rank.reshape(e.shape).astype(np.int64)
+    return send_off[dest] + pre_e[e, dest] + rank - cum_d[e, dest]
+
+
+def ep_recv_segments(S, home, me: int):
+    """EP receive buffer of rank `me`: chunks per source g, experts ascending inside a chunk.
+    Segments (row_start, nrows, wslot, expert) in plan order of experts, then source."""
+    S = np.asarray(S, dtype=np.int64)
+    G, E, _ = S.shape
+    home = np.asarray(home)
+    flows_to_me = S[:, :, me].sum(axis=1)
+    chunk_off = np.concatenate([[0], np.cumsum(flows_to_me)[:-1]])
+    pre = _excl_cumsum(S[:, :, me], axis=1)  # [g, e]
+    n_e = S[:, :, me].sum(axis=0)
+    resident = (home == me).astype(np.int32)
+    order = plan_order(n_e, resident)
+    n_home = int(resident.sum())
+    hslot = np.cumsum(resident) - resident
+    n_res_work = int(sum(1 for e in order if resident[e]))
+    segs = []
+    for o, e in enumerate(order):
+        wslot = int(hslot[e]) if resident[e] else n_home + (o - n_res_work)
+        for g in range(G):
+            if S[g, e, me] > 0:
+                segs.append((int(chunk_off[g] + pre[g, e]), int(S[g, e, me]), wslot, int(e)))
+    return segs
+
+
+# --------------------------------------------------------------------------------------------
 # bf16 helpers (numpy has no bf16): values carried as uint16 bit patterns
 # --------------------------------------------------------------------------------------------
 def bf16_to_f32(bits) -> np.ndarray:

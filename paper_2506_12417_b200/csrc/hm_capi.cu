@@ -164,6 +164,28 @@ int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_fla
   return check_launch("fetch_expert flag");
 }
 
+int hm_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  memcpy(handle_out, &h, sizeof(h));
+  return HM_OK;
+}
+
+int hm_ipc_open(const void* handle, void** dev_ptr_out) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  return HM_OK;
+}
+
+int hm_ipc_close(void* dev_ptr) {
+  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return HM_OK;
+}
+
 int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y, void* stream) {
   return launch_combine(Y, pos, topk_w, T, k, d, y, as_stream(stream));
 }

@@ -1,0 +1,271 @@
+"""Expert-parallel HarMoEny block: one process per GPU, G = world size.
+
+Alg. 1 across ranks, every step a kernel or a collective:
+
+  1 router + histogram          hm_router_topk / hm_hist_scan on the local tokens
+  2 metadata exchange           all_gather of hist[E] int32 -> m_all[G,E] (4 KB at G=8)
+  3 schedule                    hm_schedule, replicated bit-identically on every rank
+  4 scatter                     hm_permute into a dest-major send buffer + all_to_all_single
+  5 experts + async fetch       hm_grouped_gemm x2 over the receive buffer's (expert, source)
+                                segments in plan order; experts this rank does not host are
+                                fetched (hm_fetch_expert) from the home GPU's HBM over NVLink
+                                (CUDA IPC) or from pinned host memory, on a dedicated stream,
+                                one transfer channel in plan order (engine.py:253-265); the
+                                GEMM's producer waits on a per-slot ready flag
+  6 gather                      all_to_all_single back + hm_combine
+
+The split sizes of the all_to_all are host arguments in NCCL, so S is copied to
+the host once per layer (32 KB at G=8, E=128).  Host-side plumbing lives in
+plain functions (``ep_counts``, ``exchange_*``) that are exercised with the
+gloo backend on CPU by tests/test_ep_gloo.py.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib, ops
+from .block import BlockStats, MoEConfig, pack_w13, placement_home
+
+
+# ------------------------------------------------------------------------------------------
+# host-side plumbing (device agnostic; gloo-testable)
+# ------------------------------------------------------------------------------------------
+def ep_counts(S: np.ndarray, me: int):
+    """Rows this rank sends to / receives from every rank: the flows matrix of
+    engine._exchange_byte_vectors (engine.py:278-284), flows[g_from, g_to] = sum_e S."""
+    flows = np.asarray(S, dtype=np.int64).sum(axis=1)
+    return flows[me, :].tolist(), flows[:, me].tolist()
+
+
+def exchange_metadata(hist_local: torch.Tensor, group=None) -> torch.Tensor:
+    """Step 2: all_gather of the local histogram [1, E] -> m_all [G, E]."""
+    G = dist.get_world_size(group)
+    out = torch.empty((G, hist_local.shape[-1]), dtype=hist_local.dtype, device=hist_local.device)
+    dist.all_gather_into_tensor(out, hist_local.reshape(1, -1).contiguous(), group=group)
+    return out
+
+
+def exchange_tokens(send_buf: torch.Tensor, send_counts, recv_counts, group=None, out=None) -> torch.Tensor:
+    """Step 4 scatter: all_to_all_single with per-destination row counts."""
+    rows = int(sum(recv_counts))
+    if out is None:
+        out = torch.empty((max(rows, 1), send_buf.shape[1]), dtype=send_buf.dtype, device=send_buf.device)
+    dist.all_to_all_single(out[:rows], send_buf[: int(sum(send_counts))], output_split_sizes=list(recv_counts),
+                           input_split_sizes=list(send_counts), group=group)
+    return out
+
+
+def return_tokens(y_recv: torch.Tensor, send_counts, recv_counts, group=None, out=None) -> torch.Tensor:
+    """Step 6 gather: the mirror all_to_all (engine.py:368-371) - every row goes home."""
+    return exchange_tokens(y_recv, recv_counts, send_counts, group=group, out=out)
+
+
+# ------------------------------------------------------------------------------------------
+# the block
+# ------------------------------------------------------------------------------------------
+class EPHarMoEnyBlock:
+    """One MoE layer sharded by expert over the ranks of `group` (NCCL)."""
+
+    KERNELS_PER_FORWARD = 8
+
+    def __init__(self, cfg: MoEConfig, wg, w1, w2, w3=None, bias=None, device=None, group=None):
+        if not dist.is_initialized():
+            raise RuntimeError("EPHarMoEnyBlock needs torch.distributed (one process per GPU)")
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.me = dist.get_rank(group)
+        if cfg.world_size != self.G or cfg.rank != self.me:
+            raise ValueError("MoEConfig rank/world_size must match the process group")
+        self.cfg = cfg
+        device = torch.device(device if device is not None else "cuda")
+        self.device = device
+        E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
+        bf = torch.bfloat16
+        wgp = torch.zeros((ops.e_pad(E), d), dtype=bf, device=device)
+        wgp[:E] = wg.to(device=device, dtype=bf)
+        self.wg = wgp
+        self.bias = None if bias is None else bias.to(device=device, dtype=torch.float32).contiguous()
+        self.home_np = placement_home(cfg)
+        self.home = torch.from_numpy(self.home_np).to(device)
+        self.home_experts = [e for e in range(E) if self.home_np[e] == self.me]
+        self.n_home = len(self.home_experts)
+        self.n_cache = cfg.expert_cache_size if cfg.expert_cache_size > 0 else E - self.n_home
+        if cfg.activation == "swiglu":
+            if w3 is None:
+                raise ValueError("SwiGLU experts need w3")
+            w_in_all = pack_w13(w1.to(device=device, dtype=bf), w3.to(device=device, dtype=bf)).view(E, 2 * f, d)
+            self.n_in, self.epi_in = 2 * f, ops.HM_EPI_SWIGLU
+        else:
+            w_in_all = w1.to(device=device, dtype=bf).reshape(E, f, d)
+            self.n_in, self.epi_in = f, ops.HM_EPI_RELU
+        w_out_all = w2.to(device=device, dtype=bf).reshape(E, d, f)
+        slots = self.n_home + self.n_cache
+        self.w_in = torch.empty((slots, self.n_in, d), dtype=bf, device=device)
+        self.w_out = torch.empty((slots, d, f), dtype=bf, device=device)
+        if self.n_home:
+            idx = torch.tensor(self.home_experts, device=device)
+            self.w_in[: self.n_home] = w_in_all[idx]
+            self.w_out[: self.n_home] = w_out_all[idx]
+        # fetch sources
+        self.fetch_source = cfg.fetch_source
+        self._hslot = {}
+        for g in range(self.G):
+            for i, e in enumerate([e for e in range(E) if self.home_np[e] == g]):
+                self._hslot[e] = i
+        if self.fetch_source == "host":
+            self.w_in_host = w_in_all.cpu().pin_memory()
+            self.w_out_host = w_out_all.cpu().pin_memory()
+        elif self.fetch_source == "peer":
+            self._open_peers()
+        else:
+            raise ValueError("fetch_source must be 'peer' or 'host'")
+        del w_in_all, w_out_all
+        self.ready_in = torch.zeros(slots, dtype=torch.int32, device=device)
+        self.ready_out = torch.zeros(slots, dtype=torch.int32, device=device)
+        self.epoch = 0
+        self.fetch_stream = torch.cuda.Stream(device=device)
+        self._last_gemm = None
+        self.S_host = torch.empty((self.G, E, self.G), dtype=torch.int32, pin_memory=True)
+        self.fetch_host = torch.empty(E + 1, dtype=torch.int32, pin_memory=True)
+        self.stats = BlockStats()
+
+    @classmethod
+    def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s=None, std: float = 0.02, group=None):
+        """Identical random weights on every rank (same seed), Zipf router bias."""
+        from .workload import router_bias
+
+        g = torch.Generator(device=device).manual_seed(seed)
+        E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
+        kw = dict(device=device, dtype=torch.float32, generator=g)
+        wg = (torch.randn((E, d), **kw) * (1.0 / d) ** 0.5).to(torch.bfloat16)
+        w1 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16)
+        w2 = (torch.randn((E, d, f), **kw) * std).to(torch.bfloat16)
+        w3 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16) if cfg.activation == "swiglu" else None
+        bias = None if zipf_s is None else torch.from_numpy(router_bias(E, zipf_s)).to(device)
+        return cls(cfg, wg, w1, w2, w3, bias, device=device, group=group)
+
+    def _open_peers(self):
+        """Exchange CUDA IPC handles of every rank's home-expert weights (once)."""
+        L = _lib.load()
+        hs = []
+        for t in (self.w_in, self.w_out):
+            buf = ctypes.create_string_buffer(64)
+            _lib.check(L.hm_ipc_get_handle(t.data_ptr(), buf), "hm_ipc_get_handle")
+            hs.append(bytes(buf.raw))
+        allh = [None] * self.G
+        dist.all_gather_object(allh, hs, group=self.group)
+        self.peer_in, self.peer_out = [], []
+        for g in range(self.G):
+            if g == self.me:
+                self.peer_in.append(self.w_in.data_ptr())
+                self.peer_out.append(self.w_out.data_ptr())
+                continue
+            ptrs = []
+            for h in allh[g]:
+                p = ctypes.c_void_p()
+                _lib.check(L.hm_ipc_open(h, ctypes.byref(p)), "hm_ipc_open")
+                ptrs.append(p.value)
+            self.peer_in.append(ptrs[0])
+            self.peer_out.append(ptrs[1])
+
+    def _fetch(self, experts):
+        """K6: one transfer channel (the fetch stream), plan order, overwrite semantics:
+        fetched experts land in cache slots n_home + i and publish ready flags."""
+        if len(experts) > self.n_cache:
+            raise RuntimeError(f"{len(experts)} experts to fetch exceed the {self.n_cache} cache slots")
+        d, f = self.cfg.d_model, self.cfg.d_ff
+        s = self.fetch_stream
+        if self._last_gemm is not None:
+            s.wait_event(self._last_gemm)  # previous layer's GEMMs are done with the slots
+        in_bytes = self.n_in * d * 2
+        out_bytes = d * f * 2
+        L = _lib.load()
+        for i, e in enumerate(experts):
+            slot = self.n_home + i
+            h = int(self.home_np[e])
+            hs = self._hslot[e]
+            if self.fetch_source == "host":
+                src_in = self.w_in_host[e].data_ptr()
+                src_out = self.w_out_host[e].data_ptr()
+            else:
+                src_in = self.peer_in[h] + hs * in_bytes
+                src_out = self.peer_out[h] + hs * out_bytes
+            _lib.check(L.hm_fetch_expert(self.w_in[slot].data_ptr(), src_in, in_bytes,
+                                         self.ready_in[slot:].data_ptr(), self.epoch, s.cuda_stream),
+                       "hm_fetch_expert")
+            _lib.check(L.hm_fetch_expert(self.w_out[slot].data_ptr(), src_out, out_bytes,
+                                         self.ready_out[slot:].data_ptr(), self.epoch, s.cuda_stream),
+                       "hm_fetch_expert")
+
+    def forward(self, x: torch.Tensor, stream=None, marks=None) -> torch.Tensor:
+        cfg = self.cfg
+        if x.dim() != 2 or x.shape[1] != cfg.d_model or x.dtype != torch.bfloat16:
+            raise ValueError(f"x must be bf16 [T, {cfg.d_model}]")
+        s = stream if stream is not None else torch.cuda.current_stream()
+        Tg, k, E, G, me = x.shape[0], cfg.top_k, cfg.num_experts, self.G, self.me
+        tiles = (Tg + ops.TILE_M - 1) // ops.TILE_M
+        self.epoch += 1
+
+        def mark(name):
+            if marks is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                marks.append((name, ev))
+
+        with torch.cuda.stream(s):
+            mark("start")
+            x = x.contiguous()
+            idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, 1, Tg, k, cfg.renormalize, E=E,
+                                                       stream=s)
+            hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)
+            mark("router")
+            m_all = exchange_metadata(hist, self.group)
+            S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=s)
+            lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_EP, me, stream=s)
+            self.S_host.copy_(S, non_blocking=True)
+            self.fetch_host[:E].copy_(lay.fetch, non_blocking=True)
+            self.fetch_host[E:].copy_(lay.n_fetch, non_blocking=True)
+            s.synchronize()  # NCCL split sizes are host arguments
+            mark("schedule")
+            S_np = self.S_host.numpy()
+            n_fetch = int(self.fetch_host[E])
+            self._fetch(self.fetch_host[:n_fetch].tolist())
+            send_counts, recv_counts = ep_counts(S_np, me)
+            send, pos, _ = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, 1, Tg, me, Tg * k, stream=s)
+            mark("permute")
+            recv = exchange_tokens(send, send_counts, recv_counts, self.group)
+            mark("dispatch_a2a")
+            h = ops.grouped_gemm(recv, self.w_in.view(-1, cfg.d_model), self.n_in, lay, self.epi_in,
+                                 slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=self.epoch, stream=s)
+            mark("gemm1")
+            yr = ops.grouped_gemm(h, self.w_out.view(-1, cfg.d_ff), cfg.d_model, lay, ops.HM_EPI_STORE,
+                                  slot_ready=self.ready_out, ready_from_slot=self.n_home, epoch=self.epoch,
+                                  stream=s)
+            self._last_gemm = torch.cuda.Event()
+            self._last_gemm.record(s)
+            mark("gemm2")
+            ys = return_tokens(yr, send_counts, recv_counts, self.group)
+            mark("combine_a2a")
+            y = ops.combine(ys, pos, w, stream=s)
+            mark("combine")
+        self.stats = BlockStats(m_all=m_all, schedule=S, iters=iters, loads=loads,
+                                extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay, n_fetch=n_fetch,
+                                            send_counts=send_counts, recv_counts=recv_counts))
+        return y
+
+    __call__ = forward
+
+    def forward_host(self, x_host, y_host=None, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            x = x_host.to(self.device, non_blocking=True)
+            y = self.forward(x, stream=s)
+            if y_host is None:
+                y_host = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+            y_host.copy_(y, non_blocking=True)
+        return y_host

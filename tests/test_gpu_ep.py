@@ -1,0 +1,172 @@
+"""GPU tests of the layout kernel (both layouts), the async expert fetch (K6)
+and the expert-parallel block on a 1-rank NCCL group."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import moe_oracle as orc  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda")
+
+
+def _rand_S(G, E, T, k, s, seed, placement):
+    from paper_2506_12417_b200.workload import zipf_routing_matrix
+
+    m = zipf_routing_matrix(G, T // G, E, k, s, seed)
+    home = orc.blocked_home(E, G) if placement == "blocked" else orc.round_robin_home(E, G)
+    S, _ = orc.schedule(m, home, 1, True)
+    return m, home, S
+
+
+@pytest.mark.parametrize("G,E", [(1, 16), (4, 32), (8, 128), (3, 10)])
+def test_layout_local_matches_oracle(G, E):
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    m, home, S = _rand_S(G, E, 512 * G, 4 if E >= 4 else 1, 1.2, G * 7 + E, "blocked")
+    St = torch.from_numpy(S.astype(np.int32)).to(dev)
+    ht = torch.from_numpy(home.astype(np.int32)).to(dev)
+    lay = ops.dispatch_layout(St, ht, ops.HM_LAYOUT_LOCAL)
+    torch.cuda.synchronize()
+    n_seg = int(lay.n_seg.item())
+    segs = [tuple(r) for r in lay.segs[:n_seg].cpu().numpy().tolist()]
+    assert segs == orc.local_segments(S, home)
+    mp = lay.mtile_prefix[: n_seg + 1].cpu().numpy()
+    assert np.array_equal(mp, np.concatenate([[0], np.cumsum([(s[1] + 127) // 128 for s in segs])]))
+    assert int(lay.n_fetch.item()) == 0
+
+
+@pytest.mark.parametrize("G,E,me", [(2, 16, 0), (2, 16, 1), (8, 128, 3), (4, 10, 2)])
+def test_layout_ep_matches_oracle(G, E, me):
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    m, home, S = _rand_S(G, E, 256 * G, 2, 1.5, G + E + me, "blocked")
+    St = torch.from_numpy(S.astype(np.int32)).to(dev)
+    ht = torch.from_numpy(home.astype(np.int32)).to(dev)
+    lay = ops.dispatch_layout(St, ht, ops.HM_LAYOUT_EP, me)
+    torch.cuda.synchronize()
+    n_seg = int(lay.n_seg.item())
+    segs = [tuple(r) for r in lay.segs[:n_seg].cpu().numpy().tolist()]
+    assert segs == orc.ep_recv_segments(S, home, me)
+    n_fetch = int(lay.n_fetch.item())
+    fetched = lay.fetch[:n_fetch].cpu().numpy().tolist()
+    resident = (home == me).astype(np.int32)
+    order = orc.plan_order(S[:, :, me].sum(axis=0), resident)
+    assert fetched == [int(e) for e in order if not resident[e]]  # plan order, one channel
+
+
+def test_permute_positions_ep_match_oracle():
+    """EP send layout: positions of every assignment = oracle ep_send_positions."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    G, E, k, me, Tg, d = 4, 32, 4, 1, 384, 256
+    rng = np.random.default_rng(0)
+    idx = np.stack([rng.permutation(E)[:k] for _ in range(Tg)]).astype(np.int32)
+    m_me = np.bincount(idx.reshape(-1), minlength=E)
+    from paper_2506_12417_b200.workload import zipf_routing_matrix
+
+    m = zipf_routing_matrix(G, Tg, E, k, 1.0, 5)
+    m[me] = m_me
+    home = orc.blocked_home(E, G)
+    S, _ = orc.schedule(m, home, 1, True)
+    St = torch.from_numpy(S.astype(np.int32)).to(dev)
+    lay = ops.dispatch_layout(St, torch.from_numpy(home.astype(np.int32)).to(dev), ops.HM_LAYOUT_EP, me)
+    # lrank / tile_off exactly as the router would produce them
+    tiles = (Tg + 127) // 128
+    lrank = np.zeros_like(idx)
+    tile_hist = np.zeros((tiles, E), np.int32)
+    for t in range(Tg):
+        for j in range(k):
+            e = idx[t, j]
+            lrank[t, j] = tile_hist[t // 128, e]
+            tile_hist[t // 128, e] += 1
+    tile_off = (np.cumsum(tile_hist, axis=0) - tile_hist).astype(np.int32)
+    x = torch.randn((Tg, d), device=dev).to(torch.bfloat16)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    out, pos, _ = ops.permute(x, T(idx), T(lrank), T(tile_off), St, lay.slot_base, 1, Tg, me, Tg * k)
+    torch.cuda.synchronize()
+    assert np.array_equal(pos.cpu().numpy(), orc.ep_send_positions(idx, S, me))
+    p = pos.cpu().numpy()
+    for j in range(k):
+        assert torch.equal(out[torch.from_numpy(p[:, j]).long().to(dev)], x)
+
+
+def test_async_fetch_gates_gemm():
+    """K6: GEMM tiles of fetched slots wait for the slot's ready flag while the weights
+    stream in from pinned host memory on a side stream; results are exact."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    N, K, slots, n_home = 256, 512, 6, 2
+    W_host = (torch.randn((slots, N, K)) * 0.05).to(torch.bfloat16).pin_memory()
+    W = torch.zeros((slots * N, K), dtype=torch.bfloat16, device=dev)
+    W[: n_home * N] = W_host[:n_home].reshape(-1, K).to(dev)
+    counts = [300, 200, 129, 64, 17, 250]
+    segs, mt, r0 = [], [0], 0
+    for s, n in enumerate(counts):
+        segs.append([r0, n, s, s])
+        r0 += n
+        mt.append(mt[-1] + (n + 127) // 128)
+    lay = (torch.tensor(segs, dtype=torch.int32, device=dev), torch.tensor([len(segs)], dtype=torch.int32, device=dev),
+           torch.tensor(mt, dtype=torch.int32, device=dev))
+    A = torch.randn((r0, K), device=dev).to(torch.bfloat16)
+    ready = torch.zeros(slots, dtype=torch.int32, device=dev)
+    fetch_stream = torch.cuda.Stream()
+    for epoch in (1, 2):
+        W[n_home * N:].zero_()
+        torch.cuda.synchronize()
+        out = ops.grouped_gemm(A, W, N, lay, ops.HM_EPI_STORE, slot_ready=ready, ready_from_slot=n_home, epoch=epoch)
+        for s in range(n_home, slots):
+            ops.fetch_expert(W[s * N:(s + 1) * N], W_host[s], ready_flag=ready[s:], epoch=epoch, stream=fetch_stream)
+        torch.cuda.synchronize()
+        ref = []
+        for s, n in enumerate(counts):
+            ref.append(A[sum(counts[:s]):sum(counts[:s]) + n].float() @ W_host[s].to(dev).float().T)
+        ref = torch.cat(ref).to(torch.bfloat16)
+        assert torch.allclose(out.float(), ref.float(), atol=2e-2, rtol=2e-2)
+        assert int(ready.min().item()) >= 0 and int(ready[n_home:].min().item()) == epoch
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_ep_block_single_rank_matches_local_block():
+    """EP block on a 1-rank NCCL group (all_gather, all_to_all, EP layouts, pos-gather
+    combine) is bit-identical to the single-process block."""
+    import torch.distributed as dist
+
+    from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
+    from paper_2506_12417_b200.ep import EPHarMoEnyBlock
+
+    dev = _cuda()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        kw = dict(d_model=256, num_experts=32, d_ff=256, top_k=4, activation="swiglu", eq_tokens=4)
+        loc = HarMoEnyBlock.random(MoEConfig(**kw), seed=9, device=dev, zipf_s=1.0)
+        ep = EPHarMoEnyBlock.random(MoEConfig(rank=0, world_size=1, **kw), seed=9, device=dev, zipf_s=1.0)
+        x = torch.randn((640, 256), device=dev).to(torch.bfloat16)
+        y1 = loc(x)
+        y2 = ep(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y1, y2)
+        assert torch.equal(loc.stats.schedule, ep.stats.schedule)
+    finally:
+        dist.destroy_process_group()
