@@ -1,0 +1,149 @@
+"""Integration seams: the paper's model-level API and the reference simulator's
+scheduler seam.
+
+* ``replace_moe_layer(model, moe_parent_type, moe_type, path_to_experts,
+  path_to_router_linear_layer, config)`` - the listing of PAPER.md:231-258:
+  walks a PyTorch model, and every ``moe_type`` submodule found under a
+  ``moe_parent_type`` module is replaced by a :class:`HarMoEnyLayer` that runs
+  the B200 block with the original router and expert weights.
+* ``patch_moesim(moesim_module)`` - drops the GPU scheduler into the reference
+  simulator by rebinding ``moesim.engine.build_schedule`` and
+  ``moesim.engine.rebalance`` (the names engine.py:40-51 imports; patching
+  ``moesim.policies`` alone is not seen by the engine).
+
+Inference only, like HarMoEny (§3: expert-parallel MoE inference).
+"""
+
+from __future__ import annotations
+
+import torch
+from torch import nn
+
+from .block import HarMoEnyBlock, MoEConfig
+
+
+def _get_path(module: nn.Module, path: str):
+    obj = module
+    for part in path.split("."):
+        obj = obj[int(part)] if part.isdigit() else getattr(obj, part)
+    return obj
+
+
+_GATE_NAMES = ("gate_proj", "w1", "wi_0", "fc1", "wi")
+_UP_NAMES = ("up_proj", "w3", "wi_1")
+_DOWN_NAMES = ("down_proj", "w2", "wo", "fc2")
+
+
+def _linear_weight(expert: nn.Module, names) -> torch.Tensor | None:
+    for n in names:
+        if hasattr(expert, n):
+            lin = getattr(expert, n)
+            return lin.weight if isinstance(lin, nn.Module) else lin
+    return None
+
+
+def extract_expert_weights(experts, activation: str):
+    """Stack per-expert nn.Linear weights (nn.Linear layout [out, in]).
+    Accepts an nn.ModuleList of expert MLPs with HF names (gate_proj/up_proj/down_proj,
+    w1/w3/w2, wi/wo) or a module holding fused 3-D parameters ``gate_up_proj``
+    [E, d, 2f] / ``down_proj`` [E, f, d] (HF fused-expert layout)."""
+    if hasattr(experts, "gate_up_proj") and hasattr(experts, "down_proj") and not isinstance(experts, nn.ModuleList):
+        gu = experts.gate_up_proj.detach()  # [E, d, 2f]
+        f = gu.shape[-1] // 2
+        w1 = gu[..., :f].transpose(1, 2).contiguous()
+        w3 = gu[..., f:].transpose(1, 2).contiguous()
+        w2 = experts.down_proj.detach().transpose(1, 2).contiguous()  # [E, d, f]
+        return w1, w2, w3
+    w1 = torch.stack([_linear_weight(e, _GATE_NAMES).detach() for e in experts])
+    w2 = torch.stack([_linear_weight(e, _DOWN_NAMES).detach() for e in experts])
+    w3 = None
+    if activation == "swiglu":
+        w3 = torch.stack([_linear_weight(e, _UP_NAMES).detach() for e in experts])
+    return w1, w2, w3
+
+
+class HarMoEnyLayer(nn.Module):
+    """nn.Module wrapper: hidden [..., d] -> MoE(hidden) through the B200 block."""
+
+    def __init__(self, block, returns_router_logits: bool = False):
+        super().__init__()
+        self.block = block
+        self.returns_router_logits = returns_router_logits
+
+    @torch.no_grad()
+    def forward(self, hidden_states: torch.Tensor, *args, **kwargs):
+        shape = hidden_states.shape
+        x = hidden_states.reshape(-1, shape[-1]).to(torch.bfloat16).contiguous()
+        y = self.block(x).reshape(shape).to(hidden_states.dtype)
+        if self.returns_router_logits:
+            return y, None
+        return y
+
+
+def build_block(moe_module: nn.Module, path_to_experts: str, path_to_router_linear_layer: str, config: MoEConfig,
+                device=None):
+    experts = _get_path(moe_module, path_to_experts)
+    router = _get_path(moe_module, path_to_router_linear_layer)
+    wg = router.weight.detach() if isinstance(router, nn.Module) else router.detach()
+    w1, w2, w3 = extract_expert_weights(experts, config.activation)
+    if config.world_size > 1:
+        from .ep import EPHarMoEnyBlock
+
+        return EPHarMoEnyBlock(config, wg, w1, w2, w3, device=device)
+    return HarMoEnyBlock(config, wg, w1, w2, w3, device=device)
+
+
+def replace_moe_layer(model: nn.Module, moe_parent_type, moe_type, path_to_experts: str,
+                      path_to_router_linear_layer: str, config: MoEConfig, device=None,
+                      returns_router_logits: bool = False) -> int:
+    """PAPER.md:249-256.  Returns the number of layers replaced."""
+    replaced = 0
+    for parent in list(model.modules()):
+        if not isinstance(parent, moe_parent_type):
+            continue
+        for name, child in list(parent.named_children()):
+            if isinstance(child, moe_type):
+                blk = build_block(child, path_to_experts, path_to_router_linear_layer, config, device=device)
+                setattr(parent, name, HarMoEnyLayer(blk, returns_router_logits))
+                replaced += 1
+    return replaced
+
+
+def patch_moesim(moesim_module=None):
+    """Rebind the reference simulator's scheduler seam to the GPU kernels.
+
+    ``moesim.engine.simulate_layer`` calls ``build_schedule`` (engine.py:334),
+    which calls ``rebalance`` (engine.py:298); both names are module globals of
+    ``moesim.engine``.  Returns a callable that restores the originals."""
+    import numpy as np
+
+    if moesim_module is None:
+        import moesim as moesim_module  # noqa: F811
+    eng = moesim_module.engine
+    ref_core = moesim_module.core
+    from . import policies
+
+    orig = (eng.build_schedule, eng.rebalance)
+
+    def rebalance(s_initial, q):
+        s, _ = policies.rebalance_with_stats(s_initial, q)
+        return ref_core.ScheduleTensor(np.asarray(s.counts))
+
+    def build_schedule(m_all, placement, config, flags):
+        if config.policy is moesim_module.SchedulingPolicy.EVEN_SPLIT:
+            return orig[0](m_all, placement, config, flags)  # baseline policy: left to the reference
+        from . import ops
+        from .policies import _to_i32
+
+        do_rb = config.policy is moesim_module.SchedulingPolicy.REBALANCE and flags.rebalancing_enabled
+        S, _, _ = ops.schedule(_to_i32(m_all.counts, "build_schedule"),
+                               _to_i32(np.asarray(placement.home, np.int64), "home"),
+                               config.token_threshold_q, rebalance=do_rb)
+        return ref_core.ScheduleTensor(S.cpu().numpy().astype(np.int64))
+
+    eng.build_schedule, eng.rebalance = build_schedule, rebalance
+
+    def restore():
+        eng.build_schedule, eng.rebalance = orig
+
+    return restore

@@ -1,0 +1,130 @@
+"""Drop-in seams on the GPU:
+
+* patch_moesim(): the reference simulator (baseline/_ref, installed from
+  /root/reference/pkg) runs with its build_schedule/rebalance rebound to the
+  B200 scheduler kernel and produces identical layer results and run metrics;
+* replace_moe_layer(): a PyTorch MoE model (HF-style expert names) keeps its
+  outputs (vs the original fp32 torch forward) after its MoE modules are
+  swapped for HarMoEnyLayer.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+from torch import nn  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch.device("cuda")
+
+
+def _moesim():
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "moesim")):
+        pytest.skip("reference not installed in baseline/_ref")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import moesim
+
+    return moesim
+
+
+def test_patch_moesim_simulate_run_identical():
+    _cuda()
+    moesim = _moesim()
+    from paper_2506_12417_b200.integration import patch_moesim
+
+    model = moesim.model_preset("switch128")
+    cluster = moesim.ClusterSpec(num_gpus=8, expert_slots_per_gpu=16, link_bandwidth=2e11, link_latency=1e-6,
+                                 pcie_bandwidth=8e9, gpu_flops=1e12)
+    wl = moesim.WorkloadSpec(num_batches=2, tokens_per_gpu_per_batch=8192,
+                             skew=moesim.SkewSpec(alpha=0.9, skewed_experts=tuple(range(10))), seed=7)
+    trace = moesim.generate_trace(wl, model, cluster.num_gpus)
+    cfg = moesim.SchedulerConfig(token_threshold_q=64, policy=moesim.SchedulingPolicy.REBALANCE,
+                                 placement=moesim.PlacementKind.BLOCKED)
+    ref = moesim.simulate_run(trace, model, cluster, cfg, moesim.SimFlags())
+    restore = patch_moesim(moesim)
+    try:
+        got = moesim.simulate_run(trace, model, cluster, cfg, moesim.SimFlags())
+        for a, b in zip(ref.per_gpu_token_loads, got.per_gpu_token_loads):
+            assert np.array_equal(a, b)
+        assert ref.per_batch_latency == got.per_batch_latency
+        # Fig. 4 layer through the patched seam
+        m = moesim.RoutingMatrix([[1, 1, 3], [1, 1, 3], [0, 2, 3]])
+        s = moesim.engine.build_schedule(m, moesim.Placement(home=(0, 1, 2), num_gpus=3),
+                                         moesim.SchedulerConfig(token_threshold_q=1), moesim.SimFlags())
+        assert moesim.load_per_gpu(s).tolist() == [5, 5, 5]
+    finally:
+        restore()
+
+
+class _Expert(nn.Module):
+    def __init__(self, d, f):
+        super().__init__()
+        self.gate_proj = nn.Linear(d, f, bias=False)
+        self.up_proj = nn.Linear(d, f, bias=False)
+        self.down_proj = nn.Linear(f, d, bias=False)
+
+    def forward(self, x):
+        return self.down_proj(nn.functional.silu(self.gate_proj(x)) * self.up_proj(x))
+
+
+class _MoE(nn.Module):
+    def __init__(self, d, f, E, k):
+        super().__init__()
+        self.gate = nn.Linear(d, E, bias=False)
+        self.experts = nn.ModuleList([_Expert(d, f) for _ in range(E)])
+        self.k = k
+
+    def forward(self, x):
+        shape = x.shape
+        x = x.reshape(-1, shape[-1])
+        p = torch.softmax(self.gate(x).float(), dim=-1)
+        w, idx = torch.topk(p, self.k, dim=-1)
+        w = w / w.sum(-1, keepdim=True)
+        y = torch.zeros_like(x)
+        for e in range(len(self.experts)):
+            t, j = torch.nonzero(idx == e, as_tuple=True)
+            if t.numel():
+                y[t] += w[t, j, None] * self.experts[e](x[t])
+        return y.reshape(shape)
+
+
+class _Layer(nn.Module):
+    def __init__(self, d, f, E, k):
+        super().__init__()
+        self.mlp = _MoE(d, f, E, k)
+
+    def forward(self, x):
+        return x + self.mlp(x)
+
+
+def test_replace_moe_layer_matches_torch_reference():
+    dev = _cuda()
+    from paper_2506_12417_b200 import MoEConfig, replace_moe_layer
+
+    torch.manual_seed(0)
+    d, f, E, k = 256, 256, 16, 2
+    model = nn.Sequential(_Layer(d, f, E, k), _Layer(d, f, E, k)).to(dev)
+    for p in model.parameters():
+        p.data = p.data.to(torch.bfloat16).float() * 0.5  # bf16-representable weights
+    x = torch.randn((4, 64, d), device=dev).to(torch.bfloat16).float()
+    with torch.no_grad():
+        ref = model[0](x)
+    cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=k, activation="swiglu", eq_tokens=8)
+    n = replace_moe_layer(model, _Layer, _MoE, "experts", "gate", cfg, device=dev)
+    assert n == 2
+    with torch.no_grad():
+        got = model[0](x)
+    err = (got - ref).abs()
+    tol = 2e-2 + 3e-2 * ref.abs()
+    assert (err <= tol).float().mean() > 0.98  # near-tie routing flips aside
