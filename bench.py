@@ -53,7 +53,35 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--eager", action="store_true", help="no CUDA graphs (launch every kernel from Python)")
+    ap.add_argument("--kernel-table", action="store_true",
+                    help="print per-kernel CUDA times from torch.profiler (CUPTI) for a few steps and exit")
     return ap.parse_args()
+
+
+def kernel_table(blk, x, steps=5):
+    """Per-kernel device time (CUPTI via torch.profiler) - diagnosis only, never a bench value."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    for _ in range(3):
+        blk(x)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            blk(x)
+        torch.cuda.synchronize()
+    rows = {}
+    for ev in prof.events():
+        if ev.device_type.name != "CUDA":
+            continue
+        r = rows.setdefault(ev.name[:90], [0, 0.0])
+        r[0] += 1
+        r[1] += ev.device_time_total if hasattr(ev, "device_time_total") else ev.cuda_time_total
+    tot = sum(v[1] for v in rows.values())
+    for name, (n, us) in sorted(rows.items(), key=lambda kv: -kv[1][1]):
+        print(f"{us / steps:9.1f} us/step  x{n // steps:<3d} {100 * us / tot:5.1f}%  {name}", file=sys.stderr)
+    print(f"{tot / steps:9.1f} us/step total device time", file=sys.stderr)
 
 
 def peaks():
@@ -273,8 +301,23 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.barrier()
 
+    if args.kernel_table:
+        kernel_table(blk, x)
+        return
+
+    # LOCAL (single process) forward has no host sync -> CUDA graphs (one per stage group,
+    # so gemm1 keeps its own event bracket inside the timed region); EP runs eagerly
+    graphed = world == 1 and not args.eager
+    if graphed:
+        cap = blk.capture(T_local)
+        cap.x.copy_(x)
+        step = lambda marks=None: cap.replay(marks)  # noqa: E731
+        fwd_host = cap.forward_host
+    else:
+        step = lambda marks=None: blk(x, marks=marks)  # noqa: E731
+        fwd_host = blk.forward_host
     for _ in range(args.warmup):
-        blk(x)
+        step()
     torch.cuda.synchronize()
 
     # ---- device-timed region: inputs resident in HBM, L2 flushed between steps ----
@@ -290,7 +333,7 @@ def run_ours(args, rank, world, local_rank):
             flush.fill_(i)
             marks = []
             starts[i].record(stream)
-            blk(x, marks=marks)
+            step(marks)
             ends[i].record(stream)
             all_marks.append(marks)
         torch.cuda.synchronize()
@@ -313,14 +356,14 @@ def run_ours(args, rank, world, local_rank):
     x_host = x.cpu().pin_memory()
     y_host = torch.empty((T_local, d), dtype=torch.bfloat16, pin_memory=True)
     for _ in range(3):
-        blk.forward_host(x_host, y_host)
+        fwd_host(x_host, y_host)
     torch.cuda.synchronize()
     e_steps = max(3, min(args.steps, 30))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(stream)
     for _ in range(e_steps):
-        blk.forward_host(x_host, y_host)
+        fwd_host(x_host, y_host)
     e1.record(stream)
     torch.cuda.synchronize()
     e_ms = e0.elapsed_time(e1)

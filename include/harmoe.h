@@ -117,6 +117,18 @@ HM_API int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int 
                        void* stream);
 
 /*
+ * Fused planner: the whole step-2/3 stage in one single-CTA launch (histogram reduce ->
+ * hm_schedule -> hm_dispatch_layout).  Either tile_hist (+ tiles_per_rank; LOCAL layout, G ranks
+ * on this device: also writes m_all_out [G,E] and tile_off) or m_all_in [G,E] (EP: after the
+ * metadata all_gather) is given.  Outputs as hm_schedule + hm_dispatch_layout.
+ * Requires (E + 4*G*E + G*E*G + 3*E) * 4 bytes <= 200 KB.
+ */
+HM_API int hm_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_all_in, const int32_t* home, int G,
+                   int E, int q, int rebalance, int mode, int me, int32_t* m_all_out, int32_t* tile_off, int32_t* S,
+                   int32_t* iters, int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg,
+                   int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch, void* stream);
+
+/*
  * Scatter (K4): copy token rows to their scheduled buffer rows (one read of x, k 128-bit-vector
  * writes).  Token t's source rank is src_rank_base + t / tokens_per_rank; its r-th assignment to
  * expert e goes to the first dest d with cumsum_d S[src,e,d] > r (split-bucket contract).

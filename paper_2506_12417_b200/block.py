@@ -91,6 +91,43 @@ def placement_home(cfg: MoEConfig):
     return np.asarray(p.home, dtype=np.int32)
 
 
+class CapturedForward:
+    """A graph-captured block forward over static buffers (see HarMoEnyBlock.capture)."""
+
+    def __init__(self, graphs, x, y, stats):
+        self.graphs, self.x, self.y, self.stats = graphs, x, y, stats
+
+    def replay(self, marks: list | None = None, stream=None):
+        """Replay on the current stream; ``marks`` receives (last stage of group, event)."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            if marks is not None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(s)
+                marks.append(("start", ev))
+            for name, g in self.graphs:
+                g.replay()
+                if marks is not None:
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record(s)
+                    marks.append((name, ev))
+        return self.y
+
+    def __call__(self, x=None, marks=None):
+        if x is not None:
+            self.x.copy_(x)
+        return self.replay(marks)
+
+    def forward_host(self, x_host, y_host, stream=None):
+        """End-to-end call with pinned host buffers: H2D -> graphs -> D2H (stream-ordered)."""
+        s = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            self.x.copy_(x_host, non_blocking=True)
+            self.replay(stream=s)
+            y_host.copy_(self.y, non_blocking=True)
+        return y_host
+
+
 @dataclass
 class BlockStats:
     """Device tensors describing the last forward (read them after a sync)."""
@@ -172,11 +209,8 @@ class HarMoEnyBlock:
         T = x.shape[0]
         if T % G != 0:
             raise ValueError("token count must divide evenly over the logical ranks")
-        Tg = T // G
-        k = cfg.top_k
-        tiles_per_rank = (Tg + ops.TILE_M - 1) // ops.TILE_M
-        x = x.contiguous()
         s = stream if stream is not None else torch.cuda.current_stream()
+        st = {"x": x.contiguous()}
 
         def mark(name):
             if marks is not None:
@@ -185,30 +219,87 @@ class HarMoEnyBlock:
                 marks.append((name, ev))
 
         mark("start")
-        idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, G, Tg, k, cfg.renormalize,
-                                                   E=cfg.num_experts, stream=s)
-        mark("router")
-        m_all, tile_off = ops.hist_scan(tile_hist, G, tiles_per_rank, stream=s)
-        S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=s)
-        lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_LOCAL, stream=s)
-        mark("schedule")
-        xs, pos, inv = ops.permute(x, idx, lrank, tile_off, S, lay.slot_base, G, Tg, 0, T * k, with_inverse=True,
-                                   stream=s)
-        mark("permute")
-        h = ops.grouped_gemm(xs, self.w_in, self.n_in, lay, self.epi_in, stream=s)
-        mark("gemm1")
-        # FFN2 scatters its rows token-major (row_map = inverse permutation) so the
-        # combine reads each token's k expert outputs as one contiguous block
-        ys = ops.grouped_gemm(h, self.w_out, cfg.d_model, lay, ops.HM_EPI_STORE, row_map=inv, stream=s)
-        mark("gemm2")
-        y = ops.combine(ys, None, w, stream=s)
-        mark("combine")
-        self.stats = BlockStats(m_all=m_all, schedule=S, iters=iters, loads=loads,
-                                extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay, lrank=lrank,
-                                            tile_off=tile_off))
-        return y
+        for name, fn in self._stages(st, G, T // G, s):
+            fn()
+            mark(name)
+        return st["y"]
 
-    KERNELS_PER_FORWARD = 8  # router, hist_scan, schedule, layout, permute, gemm1, gemm2, combine
+    def _stages(self, st: dict, G: int, Tg: int, s):
+        """The forward as named, stream-ordered stages over a state dict (so the bench
+        and the graph capture can group them); every stage is one kernel launch."""
+        cfg = self.cfg
+        k, E = cfg.top_k, cfg.num_experts
+        T = G * Tg
+        tiles_per_rank = (Tg + ops.TILE_M - 1) // ops.TILE_M
+
+        def router():
+            st["idx"], st["w"], st["tile_hist"], st["lrank"] = ops.router_topk(
+                st["x"], self.wg, self.bias, G, Tg, k, cfg.renormalize, E=E, stream=s)
+
+        def plan():
+            # steps 2+3 fused: per-rank histograms (m_all), schedule S, layout + GEMM work list
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_LOCAL,
+                         tile_hist=st["tile_hist"], tiles_per_rank=tiles_per_rank, stream=s)
+            st["plan"] = p
+            self.stats = BlockStats(m_all=p.m_all, schedule=p.S, iters=p.iters, loads=p.loads,
+                                    extras=dict(topk_idx=st["idx"], topk_w=st["w"], layout=p.layout,
+                                                lrank=st["lrank"], tile_off=p.tile_off))
+
+        def permute():
+            p = st["plan"]
+            st["xs"], st["pos"], st["inv"] = ops.permute(st["x"], st["idx"], st["lrank"], p.tile_off, p.S,
+                                                         p.layout.slot_base, G, Tg, 0, T * k, with_inverse=True,
+                                                         stream=s)
+            self.stats.extras["pos"] = st["pos"]
+
+        def gemm1():
+            st["h"] = ops.grouped_gemm(st["xs"], self.w_in, self.n_in, st["plan"].layout, self.epi_in, stream=s)
+
+        def gemm2():
+            # FFN2 scatters its rows token-major (row_map = inverse permutation) so the
+            # combine reads each token's k expert outputs as one contiguous block
+            st["ys"] = ops.grouped_gemm(st["h"], self.w_out, cfg.d_model, st["plan"].layout, ops.HM_EPI_STORE,
+                                        row_map=st["inv"], stream=s)
+
+        def combine():
+            st["y"] = ops.combine(st["ys"], None, st["w"], stream=s)
+
+        return [("router", router), ("schedule", plan), ("permute", permute), ("gemm1", gemm1),
+                ("gemm2", gemm2), ("combine", combine)]
+
+    KERNELS_PER_FORWARD = 6  # router, plan, permute, gemm1, gemm2, combine
+
+    def capture(self, num_tokens: int, groups=(("router", "schedule", "permute"), ("gemm1",), ("gemm2",),
+                                               ("combine",))) -> "CapturedForward":
+        """CUDA-graph the forward for a fixed token count.  The LOCAL forward never
+        synchronises the host, so every kernel is captured; replay removes the launch gaps.
+        Stages are captured in ``groups`` (one graph per group) so a caller can time
+        groups with stream events between replays.  Write inputs into ``.x``."""
+        cfg = self.cfg
+        G = cfg.num_ranks
+        if num_tokens % G:
+            raise ValueError("token count must divide evenly over the logical ranks")
+        x = torch.zeros((num_tokens, cfg.d_model), dtype=torch.bfloat16, device=self.device)
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.forward(x, stream=side)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        st = {"x": x}
+        pool = torch.cuda.graph_pool_handle()
+        graphs = []
+        with torch.cuda.stream(side):
+            stages = dict(self._stages(st, G, num_tokens // G, side))
+        for grp in groups:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool, stream=side):
+                for name in grp:
+                    stages[name]()
+            graphs.append(("+".join(grp), g))
+        torch.cuda.synchronize(self.device)
+        return CapturedForward(graphs, x, st["y"], self.stats)
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """Public end-to-end call with host buffers: H2D of x (pinned -> HBM), the block,

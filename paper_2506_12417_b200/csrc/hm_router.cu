@@ -14,6 +14,8 @@
 // The rank pass uses __match_any_sync over 32-assignment chunks in (token, slot)
 // order so lrank is deterministic (no atomics), which is what makes the
 // dispatch bit-reproducible.
+#include <algorithm>
+
 #include "hm_common.cuh"
 #include "hm_internal.h"
 
@@ -22,13 +24,18 @@ namespace hm {
 namespace {
 constexpr int kRBM = 128;
 constexpr int kRBK = 64;
-constexpr int kRStages = 4;
-constexpr uint32_t kRA = kRBM * kRBK * 2;       // 16 KB
-constexpr uint32_t kRBmax = 256 * kRBK * 2;     // 32 KB (E_pad <= 256)
+constexpr int kRMaxStages = 8;
+constexpr uint32_t kRA = kRBM * kRBK * 2;  // 16 KB
 constexpr int kRThreads = 192;
 constexpr int kRKmax = 16;
-constexpr size_t kRSmem =
-    1024 + kRStages * (kRA + kRBmax) + 256 + 2 * kRBM * kRKmax * sizeof(int) + 4 * 256 * sizeof(int);
+constexpr size_t kREpiSmem = 2 * kRBM * kRKmax * sizeof(int) + 4 * 256 * sizeof(int);
+constexpr size_t kRSmemMax = 227 * 1024;
+// stages in flight: as many (A + Wg) k-blocks as fit (6 at E=128, 4 at E=256, 8 at E<=48)
+inline int router_stages(int E_pad) {
+  const size_t per = kRA + (size_t)E_pad * kRBK * 2;
+  const size_t avail = kRSmemMax - 1024 - 256 - kREpiSmem;
+  return (int)std::min<size_t>(kRMaxStages, avail / per);
+}
 }  // namespace
 
 template <int KMAX>
@@ -36,14 +43,15 @@ __global__ void __launch_bounds__(kRThreads, 1)
     router_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                   const float* __restrict__ bias, int tokens_per_rank, int tiles_per_rank, int d, int E, int E_pad,
                   int k, int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
-                  int32_t* __restrict__ tile_hist, int32_t* __restrict__ lrank) {
+                  int32_t* __restrict__ tile_hist, int32_t* __restrict__ lrank, int kRStages) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t kRBmax = (uint32_t)E_pad * kRBK * 2;  // B stage stride (multiple of 2 KB)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kRStages * kRA;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_b + kRStages * kRBmax);
-  uint64_t* empty = full + kRStages;
-  uint64_t* tfull = empty + kRStages;
+  uint64_t* empty = full + kRMaxStages;
+  uint64_t* tfull = empty + kRMaxStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
   int* s_idx = reinterpret_cast<int*>(smem_b + kRStages * kRBmax + 256);
   int* s_rank = s_idx + kRBM * kRKmax;
@@ -238,22 +246,6 @@ __global__ void __launch_bounds__(kRThreads, 1)
   }
 }
 
-// Reduce per-tile histograms to per-rank m_expert rows and exclusive per-tile offsets.
-__global__ void hist_scan_kernel(const int32_t* __restrict__ tile_hist, int tiles_per_rank, int E,
-                                 int32_t* __restrict__ hist, int32_t* __restrict__ tile_off) {
-  const int rank = blockIdx.x;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = 0;
-    for (int m = 0; m < tiles_per_rank; ++m) {
-      const int64_t i = ((int64_t)rank * tiles_per_rank + m) * E + e;
-      const int v = tile_hist[i];
-      tile_off[i] = run;
-      run += v;
-    }
-    hist[(int64_t)rank * E + e] = run;
-  }
-}
-
 int launch_router(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
                   int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,
                   cudaStream_t stream) {
@@ -271,12 +263,14 @@ int launch_router(const void* x, const void* wg, const float* bias, int n_ranks,
   rc = make_tmap_2d_bf16(&tw, wg, (uint64_t)E_pad, (uint64_t)d, (uint32_t)E_pad, kRBK);
   if (rc) return rc;
   const int grid = n_ranks * tiles_per_rank;
+  const int stages = router_stages(E_pad);
+  const size_t smem = 1024 + (size_t)stages * (kRA + (size_t)E_pad * kRBK * 2) + 256 + kREpiSmem;
 #define HM_LAUNCH_ROUTER(KM)                                                                                 \
   do {                                                                                                       \
-    cudaFuncSetAttribute(router_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRSmem);       \
-    router_kernel<KM><<<grid, kRThreads, kRSmem, stream>>>(tx, tw, bias, tokens_per_rank, tiles_per_rank, d, \
-                                                           E, E_pad, k, renormalize, topk_idx, topk_w,       \
-                                                           tile_hist, lrank);                                \
+    cudaFuncSetAttribute(router_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    router_kernel<KM><<<grid, kRThreads, smem, stream>>>(tx, tw, bias, tokens_per_rank, tiles_per_rank, d,   \
+                                                         E, E_pad, k, renormalize, topk_idx, topk_w,         \
+                                                         tile_hist, lrank, stages);                          \
   } while (0)
   if (k == 1) HM_LAUNCH_ROUTER(1);
   else if (k == 2) HM_LAUNCH_ROUTER(2);
@@ -285,13 +279,6 @@ int launch_router(const void* x, const void* wg, const float* bias, int n_ranks,
   else HM_LAUNCH_ROUTER(16);
 #undef HM_LAUNCH_ROUTER
   return check_launch("router_topk");
-}
-
-int launch_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_rank, int E, int32_t* hist,
-                     int32_t* tile_off, cudaStream_t stream) {
-  if (n_ranks < 1 || tiles_per_rank < 0 || E < 1) return set_error(HM_EINVAL, "hist_scan: bad sizes");
-  hist_scan_kernel<<<n_ranks, 256, 0, stream>>>(tile_hist, tiles_per_rank, E, hist, tile_off);
-  return check_launch("hist_scan");
 }
 
 }  // namespace hm

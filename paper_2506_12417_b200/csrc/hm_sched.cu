@@ -1,6 +1,6 @@
 // K3: HarMoEny scheduler on the GPU, plus the dispatch/GEMM layout it implies.
 //
-// schedule_kernel restates moesim/policies.py:109-141 (initial_assign +
+// dev_schedule restates moesim/policies.py:109-141 (initial_assign +
 // _rebalance_core, Alg. 2 of PAPER.md:702-745) bit for bit:
 //   t_avg = floor(sum S / G); while any t_g > t_avg:
 //     g_max = argmax t; g_from = argmax_g sum_e S[g,e,g_max];
@@ -12,16 +12,23 @@
 // in a single warp with warp-shuffle argmax (lane d owns t[d]; flows F[g][d] are
 // kept incrementally so g_from is one lane-parallel read).
 //
-// layout_kernel turns S into (a) slot_base[g,e,d], the buffer row of the first
+// dev_layout turns S into (a) slot_base[g,e,d], the buffer row of the first
 // token of every bucket, and (b) the grouped GEMM's segment list in the
 // per-GPU execution order of plan_gpu_execution (engine.py:233-234: resident
 // experts with work by (-tokens, e), then fetched experts by (-tokens, e)).
+//
+// plan_kernel fuses the whole planning stage into one launch: per-rank
+// histogram + per-tile offsets from the router's tile histograms (LOCAL) or the
+// all-gathered m_all (EP), the schedule, and the layout.
 #include <climits>
 
 #include "hm_common.cuh"
 #include "hm_internal.h"
 
 namespace hm {
+
+constexpr int kPlanThreads = 1024;
+constexpr int kLayMaxGE = 8192;  // G*E entries kept in smem by the layout
 
 __device__ __forceinline__ void warp_argmax_ll(long long& v, int& i) {
 #pragma unroll
@@ -47,21 +54,55 @@ __device__ __forceinline__ void warp_argmin_ll(long long& v, int& i) {
   }
 }
 
-template <bool kSmemS, bool kFromS>
-__global__ void __launch_bounds__(256)
-    schedule_kernel(const int32_t* __restrict__ m_all, const int32_t* __restrict__ home, int G, int E, int q,
-                    int rebalance, int32_t* __restrict__ S_out, int32_t* __restrict__ iters_out,
-                    int32_t* __restrict__ loads_out) {
-  extern __shared__ int s_dyn[];
-  __shared__ long long F[32 * 32];
-  int* S = kSmemS ? s_dyn : S_out;
+// ------------------------------------------------------------------------------------------
+// histogram reduce: m_all[r][e] = sum_tiles tile_hist, tile_off = exclusive prefix over tiles
+// (all threads of the block; 8 tile-chunks per expert lane, coalesced over experts)
+// ------------------------------------------------------------------------------------------
+__device__ void dev_hist_reduce(const int32_t* __restrict__ tile_hist, int n_ranks, int tpr, int E,
+                                int* m_out /* smem or global [n_ranks*E] */, int32_t* __restrict__ m_global,
+                                int32_t* __restrict__ tile_off, int* s_part /* [8*128] */) {
+  const int tid = threadIdx.x;
+  const int el = tid & 127, sub = tid >> 7;  // 8 sub-chunks x 128 experts (blockDim = 1024)
+  const int chunk = (tpr + 7) / 8;
+  for (int r = 0; r < n_ranks; ++r) {
+    for (int e0 = 0; e0 < E; e0 += 128) {
+      const int e = e0 + el;
+      const int m_lo = min(tpr, sub * chunk), m_hi = min(tpr, m_lo + chunk);
+      int sum = 0;
+      if (e < E) {
+#pragma unroll 4
+        for (int m = m_lo; m < m_hi; ++m) sum += tile_hist[((int64_t)r * tpr + m) * E + e];
+      }
+      s_part[sub * 128 + el] = sum;
+      __syncthreads();
+      if (e < E) {
+        int base = 0;
+        for (int s = 0; s < sub; ++s) base += s_part[s * 128 + el];
+        int run = base;
+#pragma unroll 4
+        for (int m = m_lo; m < m_hi; ++m) {
+          const int64_t i = ((int64_t)r * tpr + m) * E + e;
+          const int v = tile_hist[i];
+          tile_off[i] = run;
+          run += v;
+        }
+        if (sub == 7) {
+          m_out[r * E + e] = run;
+          if (m_global != nullptr) m_global[r * E + e] = run;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// schedule (initial_assign + rebalance); S may live in smem or global memory
+// ------------------------------------------------------------------------------------------
+__device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const int* home, int G, int E, int q,
+                             int rebalance, int32_t* iters_out, int32_t* loads_out, long long* F /* [32*32] */) {
   const int n = G * E * G;
-  if (kFromS) {
-    // rebalance an arbitrary schedule in place (policies.py:144-171)
-    if (kSmemS)
-      for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = S_out[i];
-  } else {
-    // initial_assign (policies.py:109-117)
+  if (init_from_m) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < G * E; i += blockDim.x) {
@@ -127,20 +168,15 @@ __global__ void __launch_bounds__(256)
         ++iters;
       }
     }
-    if (lane == 0) *iters_out = iters;
+    if (lane == 0 && iters_out != nullptr) *iters_out = iters;
     if (loads_out != nullptr && lane < G) loads_out[lane] = (int)t;
   }
   __syncthreads();
-  if (kSmemS)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) S_out[i] = S[i];
 }
 
 // ------------------------------------------------------------------------------------------
 // layout
 // ------------------------------------------------------------------------------------------
-constexpr int kLayThreads = 1024;
-constexpr int kLayMaxGE = 8192;  // G*E entries kept in smem
-
 // exclusive scan of v[0..n) in place by one warp; returns the total
 __device__ int warp_exclusive_scan(int* v, int n, int lane) {
   int running = 0;
@@ -159,10 +195,10 @@ __device__ int warp_exclusive_scan(int* v, int n, int lane) {
   return running;
 }
 
-// block-wide exclusive scan of cnt[0..n) -> out[0..n], out[n] = total (1024 threads)
+// block-wide exclusive scan of cnt[0..n) -> out[0..n], out[n] = total
 __device__ void block_scan_to(const int* cnt, int n, int* out, int* s_tmp /*[32]*/) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int per = (n + kLayThreads - 1) / kLayThreads;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   int local = 0;
   for (int i = lo; i < hi; ++i) local += cnt[i];
@@ -175,14 +211,15 @@ __device__ void block_scan_to(const int* cnt, int n, int* out, int* s_tmp /*[32]
   if (lane == 31) s_tmp[w] = incl;
   __syncthreads();
   if (w == 0) {
-    int x = s_tmp[lane];
+    const int nw = nt / 32;
+    const int x = lane < nw ? s_tmp[lane] : 0;
     int ii = x;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, ii, off);
       if (lane >= off) ii += y;
     }
-    s_tmp[lane] = ii - x;
+    if (lane < nw) s_tmp[lane] = ii - x;
   }
   __syncthreads();
   int run = s_tmp[w] + incl - local;
@@ -190,7 +227,7 @@ __device__ void block_scan_to(const int* cnt, int n, int* out, int* s_tmp /*[32]
     out[i] = run;
     run += cnt[i];
   }
-  if (tid == kLayThreads - 1) out[n] = run;
+  if (tid == nt - 1) out[n] = run;
   __syncthreads();
 }
 
@@ -201,26 +238,32 @@ __device__ __forceinline__ bool plan_before(bool ra, int na, int a, bool rb, int
   return a < b;
 }
 
-__global__ void __launch_bounds__(kLayThreads)
-    layout_kernel(const int32_t* __restrict__ S, const int32_t* __restrict__ home, int G, int E, int mode, int me,
-                  int32_t* __restrict__ slot_base, int4* __restrict__ segs, int32_t* __restrict__ n_seg_out,
-                  int32_t* __restrict__ mprefix, int32_t* __restrict__ fetch, int32_t* __restrict__ n_fetch_out) {
-  extern __shared__ int s_lay[];
-  const int GE = G * E;
-  int* s_n = s_lay;                 // LOCAL: n[d][e]; EP: S[g][e][me] as [g][e]
-  int* s_off = s_n + GE;            // LOCAL: off[d][e]; EP: recv row of (g,e)
-  int* s_cnt = s_off + GE;          // [GE + 1]
-  int* s_ne = s_cnt + GE + 1;       // [E]
-  int* s_nsrc = s_ne + E;           // [E]
-  int* s_ord = s_nsrc + E;          // [E]
+struct LayoutOut {
+  int32_t* slot_base;
+  int4* segs;
+  int32_t* n_seg;
+  int32_t* mprefix;
+  int32_t* fetch;
+  int32_t* n_fetch;
+};
+
+// scratch: 3*G*E + 1 + 3*E ints (dynamic smem); home: smem copy
+__device__ void dev_layout(const int* S, const int* home, int G, int E, int mode, int me, LayoutOut o, int* scratch) {
   __shared__ int s_base[33];
   __shared__ int s_nnz[33];
   __shared__ int s_tmp[32];
   __shared__ int s_scal[4];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int GE = G * E;
+  int* s_n = scratch;         // LOCAL: n[d][e]; EP: S[g][e][me] as [g][e]
+  int* s_off = s_n + GE;      // LOCAL: off[d][e]; EP: recv row of (g,e)
+  int* s_cnt = s_off + GE;    // [GE + 1]
+  int* s_ne = s_cnt + GE + 1; // [E]
+  int* s_nsrc = s_ne + E;     // [E]
+  int* s_ord = s_nsrc + E;    // [E]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
 
   if (mode == HM_LAYOUT_LOCAL) {
-    for (int i = tid; i < G * E; i += kLayThreads) {
+    for (int i = tid; i < GE; i += nt) {
       const int d = i / E, e = i - (i / E) * E;
       int s = 0;
       for (int g = 0; g < G; ++g) s += S[(g * E + e) * G + d];
@@ -228,7 +271,6 @@ __global__ void __launch_bounds__(kLayThreads)
       s_off[i] = s;
     }
     __syncthreads();
-    // per-destination exclusive scan over experts (warp d) + count of experts with work
     if (w < G) {
       const int total = warp_exclusive_scan(s_off + w * E, E, lane);
       int nz = 0;
@@ -252,21 +294,19 @@ __global__ void __launch_bounds__(kLayThreads)
       }
       s_base[G] = run;
       s_nnz[G] = runz;
-      *n_seg_out = runz;
-      *n_fetch_out = 0;
+      *o.n_seg = runz;
+      *o.n_fetch = 0;
     }
     __syncthreads();
-    // slot_base[g,e,d] = base[d] + off[d][e] + sum_{g'<g} S[g',e,d]
-    for (int i = tid; i < E * G; i += kLayThreads) {
+    for (int i = tid; i < E * G; i += nt) {
       const int e = i / G, d = i - (i / G) * G;
       int run = s_base[d] + s_off[d * E + e];
       for (int g = 0; g < G; ++g) {
-        slot_base[(g * E + e) * G + d] = run;
+        o.slot_base[(g * E + e) * G + d] = run;
         run += S[(g * E + e) * G + d];
       }
     }
-    // segments in plan order per destination
-    for (int i = tid; i < G * E; i += kLayThreads) {
+    for (int i = tid; i < GE; i += nt) {
       const int d = i / E, e = i - (i / E) * E;
       const int ne = s_n[i];
       if (ne <= 0) continue;
@@ -277,17 +317,16 @@ __global__ void __launch_bounds__(kLayThreads)
         if (n2 > 0 && plan_before(home[e2] == d, n2, e2, re, ne, e)) ++pos;
       }
       const int sidx = s_nnz[d] + pos;
-      segs[sidx] = make_int4(s_base[d] + s_off[i], ne, e, e);
+      o.segs[sidx] = make_int4(s_base[d] + s_off[i], ne, e, e);
       s_cnt[sidx] = (ne + 127) / 128;
     }
     __syncthreads();
-    block_scan_to(s_cnt, s_nnz[G], mprefix, s_tmp);
+    block_scan_to(s_cnt, s_nnz[G], o.mprefix, s_tmp);
     return;
   }
 
   // ---------------- EP mode: this process is rank `me` ----------------
-  // s_n[g*E+e] = S[g,e,me]; receive rows: chunk_off[g] + prefix_e S[g,e',me]
-  for (int i = tid; i < G * E; i += kLayThreads) {
+  for (int i = tid; i < GE; i += nt) {
     const int g = i / E, e = i - (i / E) * E;
     const int v = S[(g * E + e) * G + me];
     s_n[i] = v;
@@ -307,12 +346,14 @@ __global__ void __launch_bounds__(kLayThreads)
       run += a;
     }
     s_base[G] = run;
+    s_scal[0] = 0;  // residents with work
+    s_scal[1] = 0;  // home experts
+    s_scal[2] = 0;  // experts with work
   }
   __syncthreads();
-  // send-side slot_base[me,e,d] = send_off[d] + sum_{e'<e} S[me,e',d]  (dest-major send buffer)
+  // send side: slot_base[me,e,d] = send_off[d] + sum_{e'<e} S[me,e',d]  (dest-major send buffer)
   if (w < G) {
     const int d = w;
-    // send_off[d] = sum_{d'<d} sum_e S[me,e,d']
     int send_off = 0;
     for (int d2 = 0; d2 < d; ++d2)
       for (int e = lane; e < E; e += 32) send_off += S[(me * E + e) * G + d2];
@@ -328,12 +369,11 @@ __global__ void __launch_bounds__(kLayThreads)
         const int y = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += y;
       }
-      if (e < E) slot_base[(me * E + e) * G + d] = running + incl - x;
+      if (e < E) o.slot_base[(me * E + e) * G + d] = running + incl - x;
       running += __shfl_sync(0xffffffffu, incl, 31);
     }
   }
-  // per-expert work on me, residency, plan order
-  for (int e = tid; e < E; e += kLayThreads) {
+  for (int e = tid; e < E; e += nt) {
     int ne = 0, ns = 0;
     for (int g = 0; g < G; ++g) {
       const int v = s_n[g * E + e];
@@ -344,13 +384,7 @@ __global__ void __launch_bounds__(kLayThreads)
     s_nsrc[e] = ns;
   }
   __syncthreads();
-  if (tid == 0) {
-    s_scal[0] = 0;  // residents with work
-    s_scal[1] = 0;  // home experts
-    s_scal[2] = 0;  // experts with work
-  }
-  __syncthreads();
-  for (int e = tid; e < E; e += kLayThreads) {
+  for (int e = tid; e < E; e += nt) {
     const int ne = s_ne[e];
     const bool re = home[e] == me;
     if (re) atomicAdd(&s_scal[1], 1);
@@ -372,44 +406,114 @@ __global__ void __launch_bounds__(kLayThreads)
   const int n_work = s_scal[2];
   if (tid == 0) {
     int run = 0;
-    for (int o = 0; o < n_work; ++o) {
-      const int a = s_cnt[o];
-      s_cnt[o] = run;
+    for (int oo = 0; oo < n_work; ++oo) {
+      const int a = s_cnt[oo];
+      s_cnt[oo] = run;
       run += a;
     }
     s_scal[3] = run;  // number of segments
-    *n_seg_out = run;
-    *n_fetch_out = n_work - s_scal[0];
+    *o.n_seg = run;
+    *o.n_fetch = n_work - s_scal[0];
   }
   __syncthreads();
   const int n_res_work = s_scal[0];
   const int n_home = s_scal[1];
-  for (int e = tid; e < E; e += kLayThreads) {
-    const int o = s_ord[e];
-    if (o < 0) continue;
+  for (int e = tid; e < E; e += nt) {
+    const int oo = s_ord[e];
+    if (oo < 0) continue;
     int wslot;
     if (home[e] == me) {
       wslot = 0;
       for (int e2 = 0; e2 < e; ++e2) wslot += (home[e2] == me);
     } else {
-      wslot = n_home + (o - n_res_work);
-      fetch[o - n_res_work] = e;
+      wslot = n_home + (oo - n_res_work);
+      o.fetch[oo - n_res_work] = e;
     }
-    int sidx = s_cnt[o];
+    int sidx = s_cnt[oo];
     for (int g = 0; g < G; ++g) {
       const int v = s_n[g * E + e];
       if (v > 0) {
-        segs[sidx] = make_int4(s_base[g] + s_off[g * E + e], v, wslot, e);
+        o.segs[sidx] = make_int4(s_base[g] + s_off[g * E + e], v, wslot, e);
         ++sidx;
       }
     }
   }
   __syncthreads();
-  // reuse s_off as per-segment m-tile counts
+  // per-segment m-tile counts (s_off reused), then scan
   const int n_seg = s_scal[3];
-  for (int i = tid; i < n_seg; i += kLayThreads) s_off[i] = (segs[i].y + 127) / 128;
+  for (int i = tid; i < n_seg; i += nt) s_off[i] = (o.segs[i].y + 127) / 128;
   __syncthreads();
-  block_scan_to(s_off, n_seg, mprefix, s_tmp);
+  block_scan_to(s_off, n_seg, o.mprefix, s_tmp);
+}
+
+// ------------------------------------------------------------------------------------------
+// kernels
+// ------------------------------------------------------------------------------------------
+__global__ void hist_scan_kernel(const int32_t* __restrict__ tile_hist, int n_ranks, int tpr, int E,
+                                 int32_t* __restrict__ hist, int32_t* __restrict__ tile_off) {
+  __shared__ int s_part[8 * 128];
+  dev_hist_reduce(tile_hist, n_ranks, tpr, E, hist, nullptr, tile_off, s_part);
+}
+
+template <bool kSmemS, bool kFromS>
+__global__ void __launch_bounds__(256)
+    schedule_kernel(const int32_t* __restrict__ m_all, const int32_t* __restrict__ home, int G, int E, int q,
+                    int rebalance, int32_t* __restrict__ S_out, int32_t* __restrict__ iters_out,
+                    int32_t* __restrict__ loads_out) {
+  extern __shared__ int s_dyn[];
+  __shared__ long long F[32 * 32];
+  int* S = kSmemS ? s_dyn : S_out;
+  const int n = G * E * G;
+  if (kFromS && kSmemS)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = S_out[i];
+  dev_schedule(S, !kFromS, m_all, home, G, E, q, rebalance, iters_out, loads_out, F);
+  if (kSmemS)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) S_out[i] = S[i];
+}
+
+__global__ void __launch_bounds__(kPlanThreads)
+    layout_kernel(const int32_t* __restrict__ S, const int32_t* __restrict__ home, int G, int E, int mode, int me,
+                  LayoutOut o) {
+  extern __shared__ int s_lay[];
+  dev_layout(S, home, G, E, mode, me, o, s_lay);
+}
+
+// Whole planning stage in one launch.  kHist: m_all comes from the router's tile
+// histograms (LOCAL, n_ranks = G); otherwise from m_in (EP: the all-gathered m_all).
+template <bool kHist>
+__global__ void __launch_bounds__(kPlanThreads)
+    plan_kernel(const int32_t* __restrict__ tile_hist, int tpr, const int32_t* __restrict__ m_in,
+                const int32_t* __restrict__ home_g, int G, int E, int q, int rebalance, int mode, int me,
+                int32_t* __restrict__ m_out, int32_t* __restrict__ tile_off, int32_t* __restrict__ S_out,
+                int32_t* __restrict__ iters_out, int32_t* __restrict__ loads_out, LayoutOut o) {
+  extern __shared__ int s_dyn[];
+  __shared__ long long F[32 * 32];
+  __shared__ int s_part[8 * 128];
+  const int GE = G * E;
+  int* s_home = s_dyn;            // [E]
+  int* s_m = s_home + E;          // [G*E]
+  int* s_S = s_m + GE;            // [G*E*G]
+  int* s_scr = s_S + GE * G;      // layout scratch [3*G*E + 1 + 3*E]
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_home[i] = home_g[i];
+  if (kHist) {
+    dev_hist_reduce(tile_hist, G, tpr, E, s_m, m_out, tile_off, s_part);
+  } else {
+    for (int i = threadIdx.x; i < GE; i += blockDim.x) s_m[i] = m_in[i];
+  }
+  __syncthreads();
+  dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F);
+  for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
+  dev_layout(s_S, s_home, G, E, mode, me, o, s_scr);
+}
+
+// ------------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------------
+int launch_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_rank, int E, int32_t* hist,
+                     int32_t* tile_off, cudaStream_t stream) {
+  if (n_ranks < 1 || tiles_per_rank < 0 || E < 1) return set_error(HM_EINVAL, "hist_scan: bad sizes");
+  hist_scan_kernel<<<1, 1024, 0, stream>>>(tile_hist, n_ranks, tiles_per_rank, E, hist, tile_off);
+  return check_launch("hist_scan");
 }
 
 int launch_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int q, int rebalance, int32_t* S,
@@ -439,18 +543,49 @@ int launch_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* l
   return check_launch("rebalance");
 }
 
-int launch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
-                  int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
-                  cudaStream_t stream) {
+static int check_layout_args(int G, int E, int mode, int me) {
   if (G < 1 || G > 32 || E < 1 || E > 1024 || G * E > kLayMaxGE)
     return set_error(HM_EINVAL, "dispatch_layout: need G <= 32, E <= 1024, G*E <= 8192");
   if (mode != HM_LAYOUT_LOCAL && mode != HM_LAYOUT_EP) return set_error(HM_EINVAL, "dispatch_layout: bad mode");
   if (mode == HM_LAYOUT_EP && (me < 0 || me >= G)) return set_error(HM_EINVAL, "dispatch_layout: bad rank");
+  return HM_OK;
+}
+
+int launch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
+                  int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
+                  cudaStream_t stream) {
+  int rc = check_layout_args(G, E, mode, me);
+  if (rc) return rc;
   const size_t smem = (size_t)(3 * G * E + 1 + 3 * E) * sizeof(int);
   cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  layout_kernel<<<1, kLayThreads, smem, stream>>>(S, home, G, E, mode, me, slot_base, reinterpret_cast<int4*>(segs),
-                                               n_seg, mtile_prefix, fetch, n_fetch);
+  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
+  layout_kernel<<<1, kPlanThreads, smem, stream>>>(S, home, G, E, mode, me, o);
   return check_launch("dispatch_layout");
+}
+
+int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_in, const int32_t* home, int G, int E,
+                int q, int rebalance, int mode, int me, int32_t* m_out, int32_t* tile_off, int32_t* S, int32_t* iters,
+                int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix,
+                int32_t* fetch, int32_t* n_fetch, cudaStream_t stream) {
+  if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
+  int rc = check_layout_args(G, E, mode, me);
+  if (rc) return rc;
+  const bool hist = tile_hist != nullptr;
+  if (hist && mode != HM_LAYOUT_LOCAL) return set_error(HM_EINVAL, "plan: tile histograms imply the LOCAL layout");
+  if (!hist && m_in == nullptr) return set_error(HM_EINVAL, "plan: need tile_hist or m_all");
+  const size_t smem = (size_t)(E + G * E + G * E * G + 3 * G * E + 1 + 3 * E) * sizeof(int);
+  if (smem > 200 * 1024) return set_error(HM_EINVAL, "plan: G*E*G too large for the fused planner; use hm_schedule");
+  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
+  if (hist) {
+    cudaFuncSetAttribute(plan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    plan_kernel<true><<<1, kPlanThreads, smem, stream>>>(tile_hist, tiles_per_rank, nullptr, home, G, E, q, rebalance,
+                                                         mode, me, m_out, tile_off, S, iters, loads, o);
+  } else {
+    cudaFuncSetAttribute(plan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    plan_kernel<false><<<1, kPlanThreads, smem, stream>>>(nullptr, 0, m_in, home, G, E, q, rebalance, mode, me,
+                                                          m_out, tile_off, S, iters, loads, o);
+  }
+  return check_launch("plan");
 }
 
 }  // namespace hm

@@ -225,8 +225,8 @@ class EPHarMoEnyBlock:
             hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)
             mark("router")
             m_all = exchange_metadata(hist, self.group)
-            S, iters, loads = ops.schedule(m_all, self.home, cfg.eq_tokens, cfg.rebalance, stream=s)
-            lay = ops.dispatch_layout(S, self.home, ops.HM_LAYOUT_EP, me, stream=s)
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_EP, me, m_all=m_all, stream=s)
+            S, iters, loads, lay = p.S, p.iters, p.loads, p.layout
             self.S_host.copy_(S, non_blocking=True)
             self.fetch_host[:E].copy_(lay.fetch, non_blocking=True)
             self.fetch_host[E:].copy_(lay.n_fetch, non_blocking=True)

@@ -128,6 +128,36 @@ def dispatch_layout(S, home, mode: int, me: int = 0, stream=None) -> Layout:
     return Layout(slot_base, segs, n_seg, mprefix, fetch, n_fetch)
 
 
+class Plan:
+    """Device-side result of hm_plan (m_all, tile offsets, schedule, layout)."""
+
+    __slots__ = ("m_all", "tile_off", "S", "iters", "loads", "layout")
+
+    def __init__(self, m_all, tile_off, S, iters, loads, layout):
+        self.m_all, self.tile_off, self.S, self.iters, self.loads, self.layout = m_all, tile_off, S, iters, loads, layout
+
+
+def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, tile_hist=None,
+         tiles_per_rank: int = 0, m_all=None, stream=None) -> Plan:
+    """Fused planner: (hist reduce) + schedule + layout in one launch."""
+    _require_cuda(home, tile_hist, m_all)
+    dev = home.device
+    i32 = dict(dtype=torch.int32, device=dev)
+    m_out = torch.empty((G, E), **i32) if tile_hist is not None else m_all
+    tile_off = torch.empty_like(tile_hist) if tile_hist is not None else None
+    S = torch.empty((G, E, G), **i32)
+    iters = torch.empty(1, **i32)
+    loads = torch.empty(G, **i32)
+    cap = G * E
+    lay = Layout(torch.zeros((G, E, G), **i32), torch.empty((cap, 4), **i32), torch.empty(1, **i32),
+                 torch.empty(cap + 1, **i32), torch.empty(E, **i32), torch.empty(1, **i32))
+    _lib.call("hm_plan", _ptr(tile_hist), int(tiles_per_rank), _ptr(m_all), _ptr(home), G, E, int(q),
+              int(bool(rebalance)), int(mode), int(me), _ptr(m_out) if tile_hist is not None else None,
+              _ptr(tile_off), _ptr(S), _ptr(iters), _ptr(loads), _ptr(lay.slot_base), _ptr(lay.segs),
+              _ptr(lay.n_seg), _ptr(lay.mtile_prefix), _ptr(lay.fetch), _ptr(lay.n_fetch), _stream(stream))
+    return Plan(m_out, tile_off, S, iters, loads, lay)
+
+
 def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per_rank: int, src_rank_base: int,
             out_rows: int, out=None, with_inverse: bool = False, stream=None):
     """K4.  Returns (out [out_rows, d] bf16, pos [T,k] i32, inv [out_rows] i32 | None)."""

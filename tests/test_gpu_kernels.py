@@ -294,6 +294,24 @@ def test_block_output_independent_of_schedule():
     assert np.array_equal(ys[0], ys[1])
 
 
+def test_graph_capture_matches_eager():
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    cfg = MoEConfig(logical_ranks=2, eq_tokens=2, placement="blocked", d_model=256, num_experts=32, d_ff=256,
+                    top_k=4, activation="swiglu")
+    blk = _block(cfg, seed=21, dev=dev, zipf_s=1.3)
+    x = torch.randn((768, 256), device=dev).to(torch.bfloat16)
+    y_eager = blk(x).clone()
+    cap = blk.capture(768)
+    for _ in range(2):
+        y = cap(x)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_eager)
+    x2 = torch.randn((768, 256), device=dev).to(torch.bfloat16)
+    assert torch.equal(cap(x2).clone(), blk(x2))
+
+
 def test_dispatch_positions_follow_contract():
     """pos[t,j] lands in the scheduled destination's region (split-bucket contract)."""
     from paper_2506_12417_b200.block import MoEConfig
