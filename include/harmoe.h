@@ -59,6 +59,10 @@ extern "C" {
 #define HM_LAYOUT_EP 1    /* this process is rank `me`: send buffer [dest][expert][rank], */
                           /* receive buffer [source][expert][rank] (NCCL all_to_all chunks) */
 
+/* diagnostics: %globaltimer stamps (ns) of the last hm_plan launch: start, after the histogram
+ * reduce, after the schedule, after the layout (host buffer of 4 int64; synchronises the device) */
+HM_API int hm_debug_plan_phases(long long* out4);
+
 HM_API int hm_version(void);
 HM_API const char* hm_last_error(void);
 HM_API int hm_num_sms(void);
@@ -135,6 +139,8 @@ HM_API int hm_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* 
  *   out [rows, d] bf16, pos [T, k] int32 (row index of each assignment in `out`),
  *   inv [rows] int32 or NULL: inverse map, inv[pos[t,j]] = t*k + j (lets the FFN2 epilogue write
  *   its rows token-major so the combine streams contiguous memory).
+ *   out == NULL: index-only scatter (pos + inv, no row copies); the FFN1 GEMM then gathers the
+ *   rows itself (hm_grouped_gemm a_gather = inv, a_gather_div = k).
  */
 HM_API int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
                const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base,
@@ -143,13 +149,17 @@ HM_API int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lra
 /*
  * Grouped expert GEMM (K5), tcgen05/TMEM/TMA: for every segment, out[rows] = epi(A[rows] W[wslot]^T).
  *   A [a_rows, K] bf16; W [w_rows, K] bf16 with w_rows = slots*N; out [a_rows, N] (or N/2 for SWIGLU).
- *   row_map [a_rows] int32 or NULL: output row of A-row r is row_map[r] (scatter epilogue).
+ *   row_map [rows] int32 or NULL: output row of buffer row r is row_map[r] (scatter epilogue).
+ *   a_gather [rows] int32 or NULL: fused scatter - buffer row r reads A row a_gather[r] / a_gather_div
+ *   (TMA tile::gather4 straight from the token activations; with the inverse permutation of
+ *   hm_permute and div = k this is the token of each assignment).  A is then [a_rows, K].
  *   slot_ready [slots] int32 or NULL: tiles of slot s >= ready_from_slot wait for slot_ready[s] >= epoch.
  * Requires N % 256 == 0, K % 64 == 0.
  */
 HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
                     const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out, const int32_t* row_map,
-                    const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream);
+                    const int32_t* a_gather, int a_gather_div, const int32_t* slot_ready, int ready_from_slot,
+                    int epoch, void* stream);
 
 /*
  * Async expert fetch (K6): copy `bytes` from src (peer HBM through UVA/NVLink, or pinned host

@@ -246,6 +246,9 @@ class HarMoEnyBlock:
                                                 lrank=st["lrank"], tile_off=p.tile_off))
 
         def permute():
+            # 128-bit row copies into the segment-contiguous buffer.  (The fused alternative -
+            # FFN1 gathering rows with TMA tile::gather4, hm_grouped_gemm a_gather - is correct
+            # but measured ~2.7x slower on B200: one gather4 moves 512 B per TMA instruction.)
             p = st["plan"]
             st["xs"], st["pos"], st["inv"] = ops.permute(st["x"], st["idx"], st["lrank"], p.tile_off, p.S,
                                                          p.layout.slot_base, G, Tg, 0, T * k, with_inverse=True,

@@ -77,6 +77,7 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
 int launch_hist_scan(const int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
 int launch_schedule(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, cudaStream_t);
 int launch_rebalance(int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
+int read_plan_phases(long long*);
 int launch_plan(const int32_t*, int, const int32_t*, const int32_t*, int, int, int, int, int, int, int32_t*, int32_t*,
                 int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
 int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
@@ -151,9 +152,10 @@ int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, con
 
 int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
                     const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out,
-                    const int32_t* row_map, const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream) {
-  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, row_map,
-                             slot_ready, ready_from_slot, epoch, as_stream(stream));
+                    const int32_t* row_map, const int32_t* a_gather, int a_gather_div, const int32_t* slot_ready,
+                    int ready_from_slot, int epoch, void* stream) {
+  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, row_map, a_gather,
+                             a_gather_div, slot_ready, ready_from_slot, epoch, as_stream(stream));
 }
 
 int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_flag, int epoch, void* stream) {
@@ -173,6 +175,8 @@ int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_fla
   publish_flag_kernel<<<1, 1, 0, s>>>(ready_flag, epoch);
   return check_launch("fetch_expert flag");
 }
+
+int hm_debug_plan_phases(long long* out4) { return read_plan_phases(out4); }
 
 int hm_ipc_get_handle(const void* dev_ptr, void* handle_out) {
   cudaIpcMemHandle_t h;

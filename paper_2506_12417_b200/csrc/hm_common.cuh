@@ -99,6 +99,27 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       : "memory");
 }
 
+// TMA gather4: 4 arbitrary rows (r0..r3) x one box-width of columns starting at c0, into
+// 4 consecutive 128-byte smem rows (the map's box is {cols, 1}; swizzle follows the smem address).
+__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)),
+      "l"(cache_hint)
+      : "memory");
+}
+
+// Bulk L2 prefetch of one 2-D box (no smem, no barrier): lets a CTA put its whole
+// future working set in flight at once instead of stage-by-stage.
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // L2 eviction-priority policies for cp.async.bulk (createpolicy)
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;

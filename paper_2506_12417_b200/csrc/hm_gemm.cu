@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                         const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
                         const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K, int ldo,
-                        const int* __restrict__ row_map, const int* __restrict__ slot_ready, int ready_from_slot,
-                        int epoch) {
+                        const int* __restrict__ row_map, const int* __restrict__ a_gather, int a_gather_div,
+                        int a_gather_rows, const int* __restrict__ slot_ready, int ready_from_slot, int epoch) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -153,33 +153,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int KB = K / kBK;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer =====
-      const uint64_t pol_a = l2_policy_evict_normal();
-      const uint64_t pol_b = l2_policy_evict_last();
-      TileCursor cur{segs, mp, NB};
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        int4 seg;
-        int m, nb;
-        cur.seek(t, seg, m, nb);
-        const int row0 = seg.x + m * kBM;
-        const int brow = seg.z * N + nb * kBN;
-        if (slot_ready != nullptr && seg.z >= ready_from_slot) {
-          // K6: fetched expert weights land asynchronously; wait for this slot's epoch
-          while (ld_acquire_gpu(slot_ready + seg.z) < epoch) __nanosleep(64);
-          asm volatile("fence.proxy.async.global;" ::: "memory");
+    // ===== TMA producer (one lane; the whole warp when A rows are gathered) =====
+    const uint64_t pol_a = l2_policy_evict_normal();
+    const uint64_t pol_b = l2_policy_evict_last();
+    const bool gather = a_gather != nullptr;
+    TileCursor cur{segs, mp, NB};
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int4 seg;
+      int m, nb;
+      cur.seek(t, seg, m, nb);
+      const int row0 = seg.x + m * kBM;
+      const int brow = seg.z * N + nb * kBN;
+      int gr[4];
+      if (gather) {
+        // lane l gathers tile rows 4l..4l+3: A row = a_gather[buffer row] / div (the token);
+        // rows past the segment repeat a valid row (their results are never stored)
+        const int valid = min(kBM, seg.y - m * kBM);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int rr = min(lane * 4 + j, valid - 1);
+          gr[j] = min(__ldg(a_gather + row0 + rr) / a_gather_div, a_gather_rows - 1);
         }
-        for (int kb = 0; kb < KB; ++kb) {
+      }
+      if (lane == 0 && slot_ready != nullptr && seg.z >= ready_from_slot) {
+        // K6: fetched expert weights land asynchronously; wait for this slot's epoch
+        while (ld_acquire_gpu(slot_ready + seg.z) < epoch) __nanosleep(64);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      for (int kb = 0; kb < KB; ++kb) {
+        if (lane == 0) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kABytes + kBBytes);
-          tma_load_2d(smem_a + stage * kABytes, &tmap_a, &full[stage], kb * kBK, row0, pol_a);
+          if (!gather) tma_load_2d(smem_a + stage * kABytes, &tmap_a, &full[stage], kb * kBK, row0, pol_a);
           tma_load_2d(smem_b + stage * kBBytes, &tmap_b, &full[stage], kb * kBK, brow, pol_b);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        }
+        if (gather) {
+          __syncwarp();
+          tma_gather4(smem_a + stage * kABytes + lane * 512, &tmap_a, &full[stage], kb * kBK, gr[0], gr[1], gr[2],
+                      gr[3], pol_a);
+        }
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
         }
       }
     }
@@ -278,14 +295,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                         const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
-                        void* out, const int32_t* row_map, const int32_t* slot_ready, int ready_from_slot, int epoch,
-                        cudaStream_t stream) {
+                        void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
+                        const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream) {
   if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
     return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
+  if (a_gather != nullptr && a_gather_div < 1) return set_error(HM_EINVAL, "grouped_gemm: a_gather_div must be >= 1");
   if (a_rows <= 0) return HM_OK;
   CUtensorMap ta, tb;
-  int rc = make_tmap_2d_bf16(&ta, A, (uint64_t)a_rows, (uint64_t)K, kBM, kBK);
+  // gathered A: 1-row boxes fetched four at a time by tile::gather4
+  int rc = make_tmap_2d_bf16(&ta, A, (uint64_t)a_rows, (uint64_t)K, a_gather != nullptr ? 1 : kBM, kBK);
   if (rc) return rc;
   rc = make_tmap_2d_bf16(&tb, W, (uint64_t)w_rows, (uint64_t)K, kBN, kBK);
   if (rc) return rc;
@@ -297,7 +316,8 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
   do {                                                                                                       \
     cudaFuncSetAttribute(grouped_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem); \
     grouped_gemm_kernel<EPI><<<grid, kGemmThreads, kGemmSmem, stream>>>(                                    \
-        ta, tb, s4, mtile_prefix, n_seg, o, N, K, ldo, row_map, slot_ready, ready_from_slot, epoch);         \
+        ta, tb, s4, mtile_prefix, n_seg, o, N, K, ldo, row_map, a_gather, a_gather_div, (int)a_rows,        \
+        slot_ready, ready_from_slot, epoch);                                                                \
   } while (0)
   switch (epilogue) {
     case kEpiStore: HM_GEMM(kEpiStore); break;

@@ -65,6 +65,35 @@ __global__ void __launch_bounds__(kPermWarps * 32)
   }
 }
 
+// Index-only scatter (the rows are gathered later by the FFN1 GEMM's TMA gather4):
+// one thread per assignment computes its buffer row and the inverse map.
+__global__ void __launch_bounds__(256)
+    permute_index_kernel(const int32_t* __restrict__ topk_idx, const int32_t* __restrict__ lrank,
+                         const int32_t* __restrict__ tile_off, const int32_t* __restrict__ S,
+                         const int32_t* __restrict__ slot_base, int64_t n_assign, int k, int tokens_per_rank,
+                         int tiles_per_rank, int src_rank_base, int G, int E, int32_t* __restrict__ pos,
+                         int32_t* __restrict__ inv) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n_assign) return;
+  const int64_t t = a / k;
+  const int lr = (int)(t / tokens_per_rank);
+  const int tin = (int)(t - (int64_t)lr * tokens_per_rank);
+  const int g = src_rank_base + lr;
+  const int tile = lr * tiles_per_rank + tin / 128;
+  const int e = __ldg(topk_idx + a);
+  const int r = __ldg(tile_off + (int64_t)tile * E + e) + __ldg(lrank + a);
+  const int32_t* srow = S + ((int64_t)g * E + e) * G;
+  int c = 0, d = 0;
+  for (; d < G - 1; ++d) {
+    const int s = __ldg(srow + d);
+    if (c + s > r) break;
+    c += s;
+  }
+  const int p = __ldg(slot_base + ((int64_t)g * E + e) * G + d) + (r - c);
+  pos[a] = p;
+  if (inv != nullptr) inv[p] = (int32_t)a;
+}
+
 // Gather combine: rows addressed through pos (EP path: rows come back through the
 // all_to_all in the send layout).
 template <int VEC>
@@ -158,6 +187,13 @@ int launch_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank,
   const int n16 = d / 8;
   const int vec = (n16 + 31) / 32;
   const int tiles_per_rank = (tokens_per_rank + 127) / 128;
+  if (out == nullptr) {
+    const int64_t n_assign = T * k;
+    permute_index_kernel<<<(unsigned)((n_assign + 255) / 256), 256, 0, stream>>>(
+        topk_idx, lrank, tile_off, S, slot_base, n_assign, k, tokens_per_rank, tiles_per_rank, src_rank_base, G, E,
+        pos, inv);
+    return check_launch("permute_index");
+  }
   const unsigned grid = (unsigned)((T + kPermWarps - 1) / kPermWarps);
   auto* xs = reinterpret_cast<const uint4*>(x);
   auto* o = reinterpret_cast<uint4*>(out);

@@ -26,7 +26,8 @@ constexpr int kRBM = 128;
 constexpr int kRBK = 64;
 constexpr int kRMaxStages = 8;
 constexpr uint32_t kRA = kRBM * kRBK * 2;  // 16 KB
-constexpr int kRThreads = 192;
+constexpr int kREpiWarps = 16;
+constexpr int kRThreads = 64 + kREpiWarps * 32;
 constexpr int kRKmax = 16;
 constexpr size_t kREpiSmem = 2 * kRBM * kRKmax * sizeof(int) + 4 * 256 * sizeof(int);
 constexpr size_t kRSmemMax = 227 * 1024;
@@ -87,9 +88,16 @@ __global__ void __launch_bounds__(kRThreads, 1)
     if (lane == 0) {
       const uint64_t pol_x = l2_policy_evict_first();
       const uint64_t pol_w = l2_policy_evict_last();
+      // the whole x tile (128 rows x d) is requested from HBM up front; the staged
+      // TMA loads below then hit L2 instead of exposing DRAM latency per stage
+      // every CTA reads the same Wg: rotate the K order per CTA so concurrent CTAs hit
+      // different Wg slices (no L2 hot spot); the fp32 sum order is fixed per tile
+      const int k0 = (int)(blockIdx.x % (unsigned)KB);
+      for (int i = kRStages; i < KB; ++i) tma_prefetch_l2_2d(&tmap_x, ((i + k0) % KB) * kRBK, row0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < KB; ++kb) {
+      for (int i = 0; i < KB; ++i) {
+        const int kb = (i + k0) % KB;
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], kRA + b_bytes);
         tma_load_2d(smem_a + stage * kRA, &tmap_x, &full[stage], kb * kRBK, row0, pol_x);
@@ -123,12 +131,17 @@ __global__ void __launch_bounds__(kRThreads, 1)
     }
   } else {
     // ===== epilogue: softmax + top-k + histogram/rank =====
-    const int etid = threadIdx.x - 64;  // 0..127
-    const int q = warp & 3;
+    // 16 warps: 4 per TMEM lane quarter (hardware: warp id % 4); "part" p of a quarter scans
+    // the 32-expert chunks p, p+4, ... of its 32 token rows, then part 0 merges the 4 partial
+    // (top-k, max, sum-exp) results and runs the rank pass.
+    const int ew = warp - 2;           // 0..15
+    const int q = warp & 3;            // lane quarter
+    const int part = ew >> 2;          // 0..3
+    const int etid = threadIdx.x - 64; // 0..511
     const int r = q * 32 + lane;
     const bool valid = r < rows;
     const int64_t t = (int64_t)row0 + r;
-    for (int i = etid; i < 4 * E_pad; i += 128) s_cnt[i] = 0;
+    for (int i = etid; i < 4 * E_pad; i += kREpiWarps * 32) s_cnt[i] = 0;
 
     mbar_wait(&tfull[0], 0);
     tc_fence_after();
@@ -142,15 +155,20 @@ __global__ void __launch_bounds__(kRThreads, 1)
       ti[j] = 0x7fffffff;
     }
     const int nchunk = (E + 31) / 32;
-    for (int c = 0; c < nchunk; ++c) {
+    float vals[32];
+    float lsum = 0.0f;
+    // single pass per chunk: logits stay in registers for the partial sum-exp
+    if (part < nchunk) {
+      const int c = part;
       uint32_t a[32];
       tmem_ld_32x32b_x32(taddr + c * 32, a);
       tmem_ld_wait();
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) {
         const int e = c * 32 + jj;
+        float v = -INFINITY;
         if (e < E) {
-          float v = __uint_as_float(a[jj]);
+          v = __uint_as_float(a[jj]);
           if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
           float cv = v;
           int ci = e;
@@ -168,21 +186,103 @@ __global__ void __launch_bounds__(kRThreads, 1)
             }
           }
         }
+        vals[jj] = v;
       }
+      // running partial sum of exp(v - m) with m = this part's running max (tv[0])
+      const float m = tv[0];
+      float cs = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        if (c * 32 + jj < E) cs = __fadd_rn(cs, expf(__fsub_rn(vals[jj], m)));
+      lsum = cs;
     }
-    const float mx = tv[0];
-    float sum = 0.0f;
-    for (int c = 0; c < nchunk; ++c) {
+    for (int c = part + 4; c < nchunk; c += 4) {
+      // second chunk of this part (E > 128): rescale the running sum to the new max
       uint32_t a[32];
       tmem_ld_32x32b_x32(taddr + c * 32, a);
       tmem_ld_wait();
+      const float m_old = tv[0];
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj) {
         const int e = c * 32 + jj;
+        float v = -INFINITY;
         if (e < E) {
-          float v = __uint_as_float(a[jj]);
+          v = __uint_as_float(a[jj]);
           if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
-          sum = __fadd_rn(sum, expf(__fsub_rn(v, mx)));
+          float cv = v;
+          int ci = e;
+          bool ins = false;
+#pragma unroll
+          for (int j = 0; j < KMAX; ++j) {
+            if (j < k && (ins || cv > tv[j])) {
+              const float tf = tv[j];
+              const int tix = ti[j];
+              tv[j] = cv;
+              ti[j] = ci;
+              cv = tf;
+              ci = tix;
+              ins = true;
+            }
+          }
+        }
+        vals[jj] = v;
+      }
+      const float m = tv[0];
+      float cs = (m_old == -INFINITY) ? 0.0f : __fmul_rn(lsum, expf(__fsub_rn(m_old, m)));
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        if (c * 32 + jj < E) cs = __fadd_rn(cs, expf(__fsub_rn(vals[jj], m)));
+      lsum = cs;
+    }
+    // partials -> smem (aliases the drained pipeline stages): [part][field][row]
+    float* pf = reinterpret_cast<float*>(smem);
+    int* pi = reinterpret_cast<int*>(smem);
+    const int nf = 2 + 2 * KMAX;
+    {
+      const int b = part * nf * kRBM;
+      pf[b + 0 * kRBM + r] = tv[0];
+      pf[b + 1 * kRBM + r] = lsum;
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        pf[b + (2 + j) * kRBM + r] = tv[j];
+        pi[b + (2 + KMAX + j) * kRBM + r] = ti[j];
+      }
+    }
+    named_bar_sync(2, kREpiWarps * 32);
+    if (part == 0) {
+    // merge: global max / sum-exp, and a 4-way merge of the sorted partial lists
+    float mx = -INFINITY;
+#pragma unroll
+    for (int pp = 0; pp < 4; ++pp) mx = fmaxf(mx, pf[pp * nf * kRBM + r]);
+    float sum = 0.0f;
+#pragma unroll
+    for (int pp = 0; pp < 4; ++pp) {
+      const float pm = pf[pp * nf * kRBM + r];
+      if (pm != -INFINITY) sum = __fadd_rn(sum, __fmul_rn(pf[pp * nf * kRBM + kRBM + r], expf(__fsub_rn(pm, mx))));
+    }
+    {
+      int head[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        if (j < k) {
+          float bv = -INFINITY;
+          int bi = 0x7fffffff, bp = 0;
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) {
+            if (head[pp] < k) {
+              const float v = pf[pp * nf * kRBM + (2 + head[pp]) * kRBM + r];
+              const int id = pi[pp * nf * kRBM + (2 + KMAX + head[pp]) * kRBM + r];
+              if (v > bv || (v == bv && id < bi)) {
+                bv = v;
+                bi = id;
+                bp = pp;
+              }
+            }
+          }
+          tv[j] = bv;
+          ti[j] = bi;
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp) head[pp] += (pp == bp);
         }
       }
     }
@@ -236,6 +336,7 @@ __global__ void __launch_bounds__(kRThreads, 1)
     for (int e = etid; e < E; e += 128)
       tile_hist[(int64_t)tile * E + e] =
           s_cnt[e] + s_cnt[E_pad + e] + s_cnt[2 * E_pad + e] + s_cnt[3 * E_pad + e];
+    }  // part == 0
   }
 
   tc_fence_before();

@@ -30,6 +30,23 @@ namespace hm {
 constexpr int kPlanThreads = 1024;
 constexpr int kLayMaxGE = 8192;  // G*E entries kept in smem by the layout
 
+// phase timestamps of the last plan_kernel (diagnostics: hm_debug_plan_phases)
+__device__ unsigned long long g_phase_ns[8];
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+int read_plan_phases(long long* out8) {
+  unsigned long long h[8];
+  const cudaError_t e = cudaMemcpyFromSymbol(h, g_phase_ns, sizeof(h));
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "read plan phases: %s", cudaGetErrorString(e));
+  for (int i = 0; i < 8; ++i) out8[i] = (long long)h[i];
+  return HM_OK;
+}
+
 __device__ __forceinline__ void warp_argmax_ll(long long& v, int& i) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -63,6 +80,24 @@ __device__ void dev_hist_reduce(const int32_t* __restrict__ tile_hist, int n_ran
                                 int32_t* __restrict__ tile_off, int* s_part /* [8*128] */) {
   const int tid = threadIdx.x;
   const int el = tid & 127, sub = tid >> 7;  // 8 sub-chunks x 128 experts (blockDim = 1024)
+  if (n_ranks >= 2 && tpr <= 32) {
+    // few tiles per rank: the 8 thread groups take whole ranks, each thread scans one expert
+    for (int r = sub; r < n_ranks; r += 8)
+      for (int e = el; e < E; e += 128) {
+        int run = 0;
+#pragma unroll 4
+        for (int m = 0; m < tpr; ++m) {
+          const int64_t i = ((int64_t)r * tpr + m) * E + e;
+          const int v = tile_hist[i];
+          tile_off[i] = run;
+          run += v;
+        }
+        m_out[r * E + e] = run;
+        if (m_global != nullptr) m_global[r * E + e] = run;
+      }
+    __syncthreads();
+    return;
+  }
   const int chunk = (tpr + 7) / 8;
   for (int r = 0; r < n_ranks; ++r) {
     for (int e0 = 0; e0 < E; e0 += 128) {
@@ -99,8 +134,53 @@ __device__ void dev_hist_reduce(const int32_t* __restrict__ tile_hist, int n_ran
 // ------------------------------------------------------------------------------------------
 // schedule (initial_assign + rebalance); S may live in smem or global memory
 // ------------------------------------------------------------------------------------------
+// Fast rebalance loop: every count < 2^21, so (value, index) pairs pack into 32-bit keys
+// and each argmax/argmin is ONE warp redux (lowest index wins ties: the index is stored
+// inverted for max, plain for min).  St is S transposed to [g][d][e] so the e_max scan
+// reads consecutive words.  Same decisions as the 64-bit loop below (and the reference).
+__device__ int rebalance_fast(int* S, int* St, long long* F, int G, int E, int q, int lane, int& t_lane,
+                              int t_avg) {
+  int t = t_lane;
+  int iters = 0;
+  for (;;) {
+    if (__ballot_sync(0xffffffffu, lane < G && t > t_avg) == 0u) break;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, lane < G ? ((unsigned)t << 5) | (31u - lane) : 0u);
+    const int g_max = 31 - (int)(kmax & 31u);
+    const unsigned kf =
+        __reduce_max_sync(0xffffffffu, lane < G ? ((unsigned)F[lane * 32 + g_max] << 5) | (31u - lane) : 0u);
+    const int g_from = 31 - (int)(kf & 31u);
+    const int* col = St + (g_from * G + g_max) * E;
+    unsigned kb = 0u;
+    for (int e = lane; e < E; e += 32) kb = max(kb, ((unsigned)col[e] << 10) | (1023u - e));
+    kb = __reduce_max_sync(0xffffffffu, kb);
+    const int t_move = (int)(kb >> 10);
+    const int e_max = 1023 - (int)(kb & 1023u);
+    if (t_move < q) break;
+    const unsigned kmin = __reduce_min_sync(0xffffffffu, lane < G ? ((unsigned)t << 5) | lane : 0xffffffffu);
+    const int g_min = (int)(kmin & 31u);
+    const int vmin = (int)(kmin >> 5);
+    if (g_min == g_max || (long long)vmin + q > t_avg) break;
+    const int t_s = min(t_move, t_avg - vmin);
+    if (lane == 0) {
+      S[(g_from * E + e_max) * G + g_max] -= t_s;
+      S[(g_from * E + e_max) * G + g_min] += t_s;
+      St[(g_from * G + g_max) * E + e_max] -= t_s;
+      St[(g_from * G + g_min) * E + e_max] += t_s;
+      F[g_from * 32 + g_max] -= t_s;
+      F[g_from * 32 + g_min] += t_s;
+    }
+    if (lane == g_max) t -= t_s;
+    if (lane == g_min) t += t_s;
+    __syncwarp();
+    ++iters;
+  }
+  t_lane = t;
+  return iters;
+}
+
 __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const int* home, int G, int E, int q,
-                             int rebalance, int32_t* iters_out, int32_t* loads_out, long long* F /* [32*32] */) {
+                             int rebalance, int32_t* iters_out, int32_t* loads_out, long long* F /* [32*32] */,
+                             int* St = nullptr /* [G*G*E] scratch for the fast loop */) {
   const int n = G * E * G;
   if (init_from_m) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = 0;
@@ -117,6 +197,11 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
     for (int e = 0; e < E; ++e) f += S[(g * E + e) * G + d];
     F[g * 32 + d] = f;
   }
+  if (St != nullptr && rebalance)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int g = i / (G * E), r = i - g * (G * E), d = r / E, e = r - d * E;
+      St[i] = S[(g * E + e) * G + d];
+    }
   __syncthreads();
 
   if (threadIdx.x < 32) {
@@ -129,7 +214,11 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
     for (int off = 16; off > 0; off >>= 1) total += __shfl_xor_sync(0xffffffffu, total, off);
     const long long t_avg = total / G;
     int iters = 0;
-    if (rebalance) {
+    if (rebalance && St != nullptr && total < (1ll << 21) && E <= 1024) {
+      int ti = (int)t;
+      iters = rebalance_fast(S, St, F, G, E, q, lane, ti, (int)t_avg);
+      t = ti;
+    } else if (rebalance) {
       for (;;) {
         const unsigned over = __ballot_sync(0xffffffffu, lane < G && t > t_avg);
         if (over == 0u) break;
@@ -231,13 +320,6 @@ __device__ void block_scan_to(const int* cnt, int n, int* out, int* s_tmp /*[32]
   __syncthreads();
 }
 
-// plan order key: residents first, then more tokens first, then lower expert id
-__device__ __forceinline__ bool plan_before(bool ra, int na, int a, bool rb, int nb, int b) {
-  if (ra != rb) return ra;
-  if (na != nb) return na > nb;
-  return a < b;
-}
-
 struct LayoutOut {
   int32_t* slot_base;
   int4* segs;
@@ -247,7 +329,24 @@ struct LayoutOut {
   int32_t* n_fetch;
 };
 
-// scratch: 3*G*E + 1 + 3*E ints (dynamic smem); home: smem copy
+// plan-order sort key (ascending = execution order): residents first, then more tokens,
+// then lower expert id (engine.py:233-234); experts without work sort last
+__device__ __forceinline__ unsigned long long plan_key(bool resident, int n, int e) {
+  if (n <= 0) return ~0ull;
+  return ((unsigned long long)(resident ? 0 : 1) << 62) | ((unsigned long long)(0x7fffffff - n) << 20) |
+         (unsigned long long)e;
+}
+
+// number of keys[0..n) below `key`, one warp
+__device__ __forceinline__ int warp_rank(const unsigned long long* keys, int n, unsigned long long key, int lane) {
+  int c = 0;
+  for (int j = lane; j < n; j += 32) c += keys[j] < key;
+  return (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+}
+
+constexpr int layout_scratch_ints(int G, int E) { return 5 * G * E + 3 + 3 * E + 2; }
+
+// scratch: layout_scratch_ints(G, E) ints (dynamic smem); home: smem copy
 __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode, int me, LayoutOut o, int* scratch) {
   __shared__ int s_base[33];
   __shared__ int s_nnz[33];
@@ -260,6 +359,8 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
   int* s_ne = s_cnt + GE + 1; // [E]
   int* s_nsrc = s_ne + E;     // [E]
   int* s_ord = s_nsrc + E;    // [E]
+  unsigned long long* s_key =  // [GE] plan-order keys (8-byte aligned)
+      reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_ord + E) + 7) & ~uintptr_t(7));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
 
   if (mode == HM_LAYOUT_LOCAL) {
@@ -298,6 +399,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       *o.n_fetch = 0;
     }
     __syncthreads();
+    if (tid == 0) g_phase_ns[4] = globaltimer_ns();
     for (int i = tid; i < E * G; i += nt) {
       const int e = i / G, d = i - (i / G) * G;
       int run = s_base[d] + s_off[d * E + e];
@@ -308,20 +410,26 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
     }
     for (int i = tid; i < GE; i += nt) {
       const int d = i / E, e = i - (i / E) * E;
-      const int ne = s_n[i];
-      if (ne <= 0) continue;
-      const bool re = home[e] == d;
-      int pos = 0;
-      for (int e2 = 0; e2 < E; ++e2) {
-        const int n2 = s_n[d * E + e2];
-        if (n2 > 0 && plan_before(home[e2] == d, n2, e2, re, ne, e)) ++pos;
-      }
-      const int sidx = s_nnz[d] + pos;
-      o.segs[sidx] = make_int4(s_base[d] + s_off[i], ne, e, e);
-      s_cnt[sidx] = (ne + 127) / 128;
+      s_key[i] = plan_key(home[e] == d, s_n[i], e);
     }
     __syncthreads();
+    // one warp per (dest, expert): rank = number of smaller plan keys of that dest
+    for (int p = w; p < GE; p += nt / 32) {
+      const unsigned long long key = s_key[p];
+      if (key == ~0ull) continue;  // warp-uniform
+      const int d = p / E, e = p - (p / E) * E;
+      const int pos = warp_rank(s_key + d * E, E, key, lane);
+      if (lane == 0) {
+        const int ne = s_n[p];
+        const int sidx = s_nnz[d] + pos;
+        o.segs[sidx] = make_int4(s_base[d] + s_off[p], ne, e, e);
+        s_cnt[sidx] = (ne + 127) / 128;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) g_phase_ns[5] = globaltimer_ns();
     block_scan_to(s_cnt, s_nnz[G], o.mprefix, s_tmp);
+    if (tid == 0) g_phase_ns[6] = globaltimer_ns();
     return;
   }
 
@@ -382,24 +490,26 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
     }
     s_ne[e] = ne;
     s_nsrc[e] = ns;
-  }
-  __syncthreads();
-  for (int e = tid; e < E; e += nt) {
-    const int ne = s_ne[e];
+    s_key[e] = plan_key(home[e] == me, ne, e);
     const bool re = home[e] == me;
     if (re) atomicAdd(&s_scal[1], 1);
     if (ne > 0) {
       atomicAdd(&s_scal[2], 1);
       if (re) atomicAdd(&s_scal[0], 1);
-      int pos = 0;
-      for (int e2 = 0; e2 < E; ++e2) {
-        const int n2 = s_ne[e2];
-        if (n2 > 0 && plan_before(home[e2] == me, n2, e2, re, ne, e)) ++pos;
-      }
+    }
+  }
+  __syncthreads();
+  // one warp per expert: position in the plan order
+  for (int e = w; e < E; e += nt / 32) {
+    const unsigned long long key = s_key[e];
+    if (key == ~0ull) {
+      if (lane == 0) s_ord[e] = -1;
+      continue;
+    }
+    const int pos = warp_rank(s_key, E, key, lane);
+    if (lane == 0) {
       s_ord[e] = pos;
       s_cnt[pos] = s_nsrc[e];
-    } else {
-      s_ord[e] = -1;
     }
   }
   __syncthreads();
@@ -466,7 +576,7 @@ __global__ void __launch_bounds__(256)
   const int n = G * E * G;
   if (kFromS && kSmemS)
     for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = S_out[i];
-  dev_schedule(S, !kFromS, m_all, home, G, E, q, rebalance, iters_out, loads_out, F);
+  dev_schedule(S, !kFromS, m_all, home, G, E, q, rebalance, iters_out, loads_out, F, kSmemS ? s_dyn + n : nullptr);
   if (kSmemS)
     for (int i = threadIdx.x; i < n; i += blockDim.x) S_out[i] = S[i];
 }
@@ -494,6 +604,8 @@ __global__ void __launch_bounds__(kPlanThreads)
   int* s_m = s_home + E;          // [G*E]
   int* s_S = s_m + GE;            // [G*E*G]
   int* s_scr = s_S + GE * G;      // layout scratch [3*G*E + 1 + 3*E]
+  int* s_St = s_scr + layout_scratch_ints(G, E);  // [G*G*E] transposed S for the fast rebalance loop
+  if (threadIdx.x == 0) g_phase_ns[0] = globaltimer_ns();
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_home[i] = home_g[i];
   if (kHist) {
     dev_hist_reduce(tile_hist, G, tpr, E, s_m, m_out, tile_off, s_part);
@@ -501,9 +613,12 @@ __global__ void __launch_bounds__(kPlanThreads)
     for (int i = threadIdx.x; i < GE; i += blockDim.x) s_m[i] = m_in[i];
   }
   __syncthreads();
-  dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F);
+  if (threadIdx.x == 0) g_phase_ns[1] = globaltimer_ns();
+  dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F, s_St);
+  if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
   for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
   dev_layout(s_S, s_home, G, E, mode, me, o, s_scr);
+  if (threadIdx.x == 0) g_phase_ns[3] = globaltimer_ns();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -520,7 +635,7 @@ int launch_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int
                     int32_t* iters, int32_t* loads, cudaStream_t stream) {
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
   if (G < 1 || G > 32 || E < 1) return set_error(HM_EINVAL, "schedule: need 1 <= G <= 32 and E >= 1");
-  const size_t sbytes = (size_t)G * E * G * sizeof(int);
+  const size_t sbytes = (size_t)2 * G * E * G * sizeof(int);  // S + transposed copy for the fast loop
   if (sbytes <= 200 * 1024) {
     cudaFuncSetAttribute(schedule_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
     schedule_kernel<true, false><<<1, 256, sbytes, stream>>>(m_all, home, G, E, q, rebalance, S, iters, loads);
@@ -533,7 +648,7 @@ int launch_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int
 int launch_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* loads, cudaStream_t stream) {
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
   if (G < 1 || G > 32 || E < 1) return set_error(HM_EINVAL, "rebalance: need 1 <= G <= 32 and E >= 1");
-  const size_t sbytes = (size_t)G * E * G * sizeof(int);
+  const size_t sbytes = (size_t)2 * G * E * G * sizeof(int);  // S + transposed copy for the fast loop
   if (sbytes <= 200 * 1024) {
     cudaFuncSetAttribute(schedule_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
     schedule_kernel<true, true><<<1, 256, sbytes, stream>>>(nullptr, nullptr, G, E, q, 1, S, iters, loads);
@@ -556,7 +671,7 @@ int launch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode,
                   cudaStream_t stream) {
   int rc = check_layout_args(G, E, mode, me);
   if (rc) return rc;
-  const size_t smem = (size_t)(3 * G * E + 1 + 3 * E) * sizeof(int);
+  const size_t smem = (size_t)layout_scratch_ints(G, E) * sizeof(int);
   cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
   layout_kernel<<<1, kPlanThreads, smem, stream>>>(S, home, G, E, mode, me, o);
@@ -573,7 +688,7 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   const bool hist = tile_hist != nullptr;
   if (hist && mode != HM_LAYOUT_LOCAL) return set_error(HM_EINVAL, "plan: tile histograms imply the LOCAL layout");
   if (!hist && m_in == nullptr) return set_error(HM_EINVAL, "plan: need tile_hist or m_all");
-  const size_t smem = (size_t)(E + G * E + G * E * G + 3 * G * E + 1 + 3 * E) * sizeof(int);
+  const size_t smem = (size_t)(E + G * E + 2 * G * E * G + layout_scratch_ints(G, E)) * sizeof(int);
   if (smem > 200 * 1024) return set_error(HM_EINVAL, "plan: G*E*G too large for the fused planner; use hm_schedule");
   LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
   if (hist) {

@@ -159,13 +159,17 @@ def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, 
 
 
 def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per_rank: int, src_rank_base: int,
-            out_rows: int, out=None, with_inverse: bool = False, stream=None):
-    """K4.  Returns (out [out_rows, d] bf16, pos [T,k] i32, inv [out_rows] i32 | None)."""
+            out_rows: int, out=None, with_inverse: bool = False, index_only: bool = False, stream=None):
+    """K4.  Returns (out [out_rows, d] bf16 | None, pos [T,k] i32, inv [out_rows] i32 | None).
+    index_only: no row copies (the FFN1 GEMM gathers rows through inv)."""
     _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base)
     T, d = x.shape
     k = topk_idx.shape[1]
     G, E, _ = S.shape
-    if out is None:
+    if index_only:
+        out = None
+        with_inverse = True
+    elif out is None:
         out = torch.empty((max(out_rows, 1), d), dtype=x.dtype, device=x.device)
     pos = torch.empty((T, k), dtype=torch.int32, device=x.device)
     inv = torch.empty(max(out_rows, 1), dtype=torch.int32, device=x.device) if with_inverse else None
@@ -175,21 +179,27 @@ def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per
 
 
 def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=None, slot_ready=None,
-                 ready_from_slot: int = 0, epoch: int = 0, stream=None):
+                 ready_from_slot: int = 0, epoch: int = 0, a_gather=None, a_gather_div: int = 1, out_rows=None,
+                 stream=None):
     """K5.  A [rows, K] bf16, W [slots*N, K] bf16 -> out [rows, N or N/2] bf16
-    (row r written to row_map[r] when a row map is given)."""
+    (row r written to row_map[r] when a row map is given).  With a_gather, buffer row r
+    reads A[a_gather[r] // a_gather_div] (TMA gather4) and out has ``out_rows`` rows."""
     if isinstance(layout_or_segs, Layout):
         segs, n_seg, mprefix = layout_or_segs.segs, layout_or_segs.n_seg, layout_or_segs.mtile_prefix
     else:
         segs, n_seg, mprefix = layout_or_segs
-    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready, row_map)
+    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready, row_map, a_gather)
     rows, K = A.shape
+    if a_gather is not None:
+        rows_out = out_rows if out_rows is not None else a_gather.numel()
+    else:
+        rows_out = rows
     ncols = N // 2 if epilogue == HM_EPI_SWIGLU else N
     if out is None:
-        out = torch.empty((rows, ncols), dtype=torch.bfloat16, device=A.device)
+        out = torch.empty((max(rows_out, 1), ncols), dtype=torch.bfloat16, device=A.device)
     _lib.call("hm_grouped_gemm", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(segs), _ptr(n_seg), _ptr(mprefix),
-              int(epilogue), _ptr(out), _ptr(row_map), _ptr(slot_ready), int(ready_from_slot), int(epoch),
-              _stream(stream))
+              int(epilogue), _ptr(out), _ptr(row_map), _ptr(a_gather), int(a_gather_div), _ptr(slot_ready),
+              int(ready_from_slot), int(epoch), _stream(stream))
     return out
 
 

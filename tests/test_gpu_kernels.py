@@ -201,8 +201,14 @@ def test_grouped_gemm(epi, N, K):
     # scatter epilogue: row r lands at row_map[r]
     perm = torch.randperm(rows, device=dev, generator=g).to(torch.int32)
     out_s = ops.grouped_gemm(A, W, N, lay, code, row_map=perm)
+    # fused gather (TMA gather4): buffer row r reads src row gidx[r] // 3
+    src = torch.randn((123, K), device=dev, generator=g).to(torch.bfloat16)
+    gidx = torch.randint(0, 123 * 3, (rows,), device=dev, generator=g).to(torch.int32)
+    out_g = ops.grouped_gemm(src, W, N, lay, code, a_gather=gidx, a_gather_div=3)
+    out_ref_g = ops.grouped_gemm(src[(gidx // 3).long()].contiguous(), W, N, lay, code)
     torch.cuda.synchronize()
     assert torch.equal(out_s[perm.long()], out)
+    assert torch.equal(out_g, out_ref_g)
     ref = []
     r0 = 0
     for n, s in zip(counts, wslots):
