@@ -293,6 +293,237 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ==========================================================================================
+// 2-CTA variant: a cluster of 2 CTAs (one TPC) computes 256 x 256 tiles with
+// tcgen05.mma.cta_group::2 (UMMA M=256).  CTA r loads A rows [128r, 128r+128) and B rows
+// (N) [128r, 128r+128) of the tile into its own smem; the leader (r=0) issues the MMAs,
+// which read both CTAs' smem and write each CTA's 128 x 256 fp32 slice of D into its
+// own TMEM.  Per CTA and k-block this moves 32 KB instead of 48 KB through L2 -> SMEM,
+// and the freed smem buys 6 pipeline stages instead of 4.
+//   full[s]   leader only: both CTAs' TMA count complete_tx bytes on it (peer via mapa)
+//   empty[s]  per CTA: the leader's tcgen05.commit multicasts to both
+//   tfull[a]  per CTA: multicast commit after the last k-block of a tile
+//   tempty[a] leader only: 8 epilogue warps of each CTA arrive (peer remotely)
+// Tiles are 256-row pair tiles of each segment; the cursor derives them from the
+// 128-row prefix on the fly (pair tiles of a segment = ceil(m128 / 2)).
+// ==========================================================================================
+constexpr int k2Stages = 6;
+constexpr uint32_t k2Half = 128 * kBK * 2;  // 16 KB: one CTA's half of A or of B per stage
+constexpr size_t kGemm2Smem = 1024 + k2Stages * 2 * k2Half + 256 + kMaxSmemSegs * 20 + 16 + kEpiWarps * kStgBytes;
+
+struct PairCursor {
+  const int4* segs;
+  const int* mp;  // 128-row tile prefix
+  int NB;
+  int s = 0;
+  int base = 0;  // pair-tile index (x NB) where segment s starts
+  __device__ __forceinline__ int pair_tiles(int i) const { return (mp[i + 1] - mp[i] + 1) >> 1; }
+  __device__ __forceinline__ void seek(int t, int4& seg, int& m, int& nb) {
+    int span = pair_tiles(s) * NB;
+    while (base + span <= t) {
+      base += span;
+      ++s;
+      span = pair_tiles(s) * NB;
+    }
+    seg = segs[s];
+    const int ms = pair_tiles(s);
+    const int local = t - base;
+    nb = local / ms;
+    m = local - nb * ms;
+  }
+};
+
+template <int kEpi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                             const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
+                             const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K,
+                             int ldo, const int* __restrict__ row_map, const int* __restrict__ slot_ready,
+                             int ready_from_slot, int epoch) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * 2 * k2Half);
+  uint64_t* empty = full + k2Stages;
+  uint64_t* tfull = empty + k2Stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int4* s_segs = reinterpret_cast<int4*>(smem + k2Stages * 2 * k2Half + 256);
+  int* s_mp = reinterpret_cast<int*>(s_segs + kMaxSmemSegs);
+  uint8_t* s_stage = reinterpret_cast<uint8_t*>(s_mp + kMaxSmemSegs + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int n_seg = *n_seg_ptr;
+  const bool seg_in_smem = n_seg <= kMaxSmemSegs;
+  if (seg_in_smem) {
+    for (int i = threadIdx.x; i < n_seg; i += blockDim.x) s_segs[i] = segs_g[i];
+    for (int i = threadIdx.x; i <= n_seg; i += blockDim.x) s_mp[i] = mprefix_g[i];
+  }
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < k2Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * kEpiWarps);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+  }
+  if (warp == 1) tmem_alloc_2cta<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int NB = N / kBN;
+  const int4* segs = seg_in_smem ? s_segs : segs_g;
+  const int* mp = seg_in_smem ? s_mp : mprefix_g;
+  int total = 0;
+  for (int i = lane; i < n_seg; i += 32) total += (mp[i + 1] - mp[i] + 1) >> 1;
+  total = (int)__reduce_add_sync(0xffffffffu, (unsigned)total) * NB;
+  const int KB = K / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs) =====
+      const uint64_t pol_a = l2_policy_evict_normal();
+      const uint64_t pol_b = l2_policy_evict_last();
+      const uint32_t full_leader = mapa_shared(full, 0);
+      PairCursor cur{segs, mp, NB};
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total; t += npairs) {
+        int4 seg;
+        int m, nb;
+        cur.seek(t, seg, m, nb);
+        const int row0 = seg.x + m * 2 * kBM + (int)rank * kBM;
+        const int brow = seg.z * N + nb * kBN + (int)rank * (kBN / 2);
+        if (slot_ready != nullptr && seg.z >= ready_from_slot) {
+          while (ld_acquire_gpu(slot_ready + seg.z) < epoch) __nanosleep(64);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 4 * k2Half);
+          uint8_t* sa = smem + stage * 2 * k2Half;
+          tma_load_2d_2cta(sa, &tmap_a, full_leader + stage * 8, kb * kBK, row0, pol_a);
+          tma_load_2d_2cta(sa + k2Half, &tmap_b, full_leader + stage * 8, kb * kBK, brow, pol_b);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (leader CTA) =====
+      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, kBN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = pair; t < total; t += npairs, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * 2 * k2Half);
+          const uint64_t a0 = make_sdesc_sw128(sa);
+          const uint64_t b0 = make_sdesc_sw128(sa + k2Half);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16_2cta(d_tmem, a0 + (uint64_t)(k * 2), b0 + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+          umma_commit_2cta_multicast(&empty[stage], 0x3);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2cta_multicast(&tfull[acc], 0x3);
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..9 of both CTAs, each CTA drains its own 128 rows =====
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    constexpr int kOutCols = (kEpi == kEpiSwiGLU) ? kBN / 2 : kBN;
+    constexpr int kHalfCols = kOutCols / 2;
+    const uint32_t stg = smem_u32(s_stage + ew * kStgBytes);
+    const uint32_t my_srow = stg + lane * kStgPitch;
+    const uint32_t tempty_leader = mapa_shared(tempty, 0);
+    PairCursor cur{segs, mp, NB};
+    int i = 0;
+    for (int t = pair; t < total; t += npairs, ++i) {
+      int4 seg;
+      int m, nb;
+      cur.seek(t, seg, m, nb);
+      const int rows = max(0, min(kBM, seg.y - m * 2 * kBM - (int)rank * kBM));  // this CTA's valid rows
+      const int r_in_tile = q * 32 + lane;
+      const bool valid = r_in_tile < rows;
+      int64_t row = (int64_t)seg.x + m * 2 * kBM + rank * kBM + r_in_tile;
+      if (row_map != nullptr && valid) row = __ldg(row_map + row);
+      const int64_t obase = row * ldo + (int64_t)nb * kOutCols + half * kHalfCols;
+      const int nvalid = max(0, min(32, rows - q * 32));
+      const int acc = i & 1;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+      for (int c0 = 0; c0 < kHalfCols; c0 += kStgCols) {
+        uint32_t a[32], u[32];
+        const int col = half * kHalfCols + c0;
+        tmem_ld_32x32b_x32(taddr + col, a);
+        if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + 128 + col, u);
+        tmem_ld_wait();
+        stage_row<kEpi>(my_srow, a, u);
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2);
+          const int piece = lane & 3;
+          const int64_t ob = __shfl_sync(0xffffffffu, obase, rr);
+          if (rr < nvalid) {
+            const uint4 v = ld_shared_v4(stg + rr * kStgPitch + piece * 16);
+            st_global_v4(out + ob + c0 + piece * 8, v.x, v.y, v.z, v.w);
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2cta<kTmemCols>(tmem_base);
+  }
+}
+
+static bool use_2cta() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HM_GEMM_1CTA");
+    v = (e != nullptr && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                         const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
@@ -312,6 +543,40 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
   const int grid = num_sms();
   const int4* s4 = reinterpret_cast<const int4*>(segs);
   auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+  if (a_gather == nullptr && use_2cta()) {
+    CUtensorMap tb2;  // each CTA of the pair loads 128 of the tile's 256 weight rows
+    rc = make_tmap_2d_bf16(&tb2, W, (uint64_t)w_rows, (uint64_t)K, kBN / 2, kBK);
+    if (rc) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(grid & ~1));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kGemm2Smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaSuccess;
+#define HM_GEMM2(EPI)                                                                                              \
+  do {                                                                                                             \
+    cudaFuncSetAttribute(grouped_gemm_2cta_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
+                         (int)kGemm2Smem);                                                                         \
+    e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI>, ta, tb2, s4, mtile_prefix, n_seg, o, N, K, ldo,    \
+                           row_map, slot_ready, ready_from_slot, epoch);                                           \
+  } while (0)
+    switch (epilogue) {
+      case kEpiStore: HM_GEMM2(kEpiStore); break;
+      case kEpiRelu: HM_GEMM2(kEpiRelu); break;
+      case kEpiSwiGLU: HM_GEMM2(kEpiSwiGLU); break;
+      default: return set_error(HM_EINVAL, "grouped_gemm: unknown epilogue");
+    }
+#undef HM_GEMM2
+    if (e != cudaSuccess) return set_error(HM_ECUDA, "grouped_gemm (2-CTA) launch: %s", cudaGetErrorString(e));
+    return check_launch("grouped_gemm_2cta");
+  }
 #define HM_GEMM(EPI)                                                                                         \
   do {                                                                                                       \
     cudaFuncSetAttribute(grouped_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem); \
