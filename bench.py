@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs (launch every kernel from Python)")
+    ap.add_argument("--e2e-chunks", type=int, default=2,
+                    help="token chunks of the pinned-host pipeline (H2D / compute / D2H overlap) for e2e")
     ap.add_argument("--kernel-table", action="store_true",
                     help="print per-kernel CUDA times from torch.profiler (CUPTI) for a few steps and exit")
     return ap.parse_args()
@@ -107,7 +109,7 @@ class ClockSampler:
             try:
                 self.proc = subprocess.Popen(
                     ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                     "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
                 self.t = threading.Thread(target=self._read, daemon=True)
                 self.t.start()
             except OSError:
@@ -312,7 +314,11 @@ def run_ours(args, rank, world, local_rank):
         cap = blk.capture(T_local)
         cap.x.copy_(x)
         step = lambda marks=None: cap.replay(marks)  # noqa: E731
-        fwd_host = cap.forward_host
+        if args.e2e_chunks > 1:
+            pipe = blk.host_pipeline(T_local, args.e2e_chunks)
+            fwd_host = pipe.run
+        else:
+            fwd_host = cap.forward_host
     else:
         step = lambda marks=None: blk(x, marks=marks)  # noqa: E731
         fwd_host = blk.forward_host
@@ -418,7 +424,10 @@ def run_ours(args, rank, world, local_rank):
                      "frac": achieved / tc, "traffic": traffic,
                      "kernel": "grouped_gemm_kernel<SwiGLU> (expert FFN1)",
                      "work_per_launch": f"{f1 / 1e9:.1f} GFLOP = 2 * {T_total // world * k} rows * {d} * {2 * f if act == 'swiglu' else f}"},
-        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes},
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "path": (f"HarMoEnyBlock.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, block, "
+                         f"HBM -> pinned y; copies overlapped with compute by token chunks")
+                if graphed and args.e2e_chunks > 1 else "forward_host (pinned H2D -> block -> D2H)"},
         "gpu_launches": HarMoEnyBlock.KERNELS_PER_FORWARD * args.steps,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,

@@ -128,6 +128,57 @@ class CapturedForward:
         return y_host
 
 
+class HostPipeline:
+    """End-to-end forward from pinned host memory: the batch is cut into ``n_chunks``
+    token chunks whose H2D copy, block forward (a captured graph per chunk) and D2H copy
+    run on three streams, so PCIe traffic in both directions overlaps the kernels.
+    Tokens are independent in the MoE block, so the output equals the unchunked forward
+    (each chunk is routed, scheduled and combined on its own)."""
+
+    def __init__(self, block: "HarMoEnyBlock", num_tokens: int, n_chunks: int = 4):
+        if num_tokens % n_chunks or (num_tokens // n_chunks) % block.cfg.num_ranks:
+            raise ValueError("chunk size must divide evenly (and over the logical ranks)")
+        self.n, self.chunk = n_chunks, num_tokens // n_chunks
+        # one graph per chunk (all stages): minimal host work per launch
+        all_stages = (("router", "schedule", "permute", "gemm1", "gemm2", "combine"),)
+        self.caps = [block.capture(self.chunk, groups=all_stages) for _ in range(n_chunks)]
+        dev = block.device
+        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
+        ev = lambda: [torch.cuda.Event() for _ in range(n_chunks)]  # noqa: E731
+        self.ev_in, self.ev_out, self.ev_back = ev(), ev(), ev()
+        self.started = False
+
+    def run(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        """Enqueue one forward; the caller's stream waits for the last D2H.  Successive runs
+        are chained only through the per-chunk buffer events, so the H2D of run i+1 overlaps
+        the tail of run i (host buffers follow the usual async rule: do not overwrite x_host
+        or read y_host before synchronising)."""
+        cur = torch.cuda.current_stream()
+        if not self.started:
+            for s in (self.h2d, self.comp, self.d2h):
+                s.wait_stream(cur)
+        for c, cap in enumerate(self.caps):
+            rows = slice(c * self.chunk, (c + 1) * self.chunk)
+            with torch.cuda.stream(self.h2d):
+                if self.started:
+                    self.h2d.wait_event(self.ev_out[c])  # previous forward of this chunk read x
+                cap.x.copy_(x_host[rows], non_blocking=True)
+                self.ev_in[c].record(self.h2d)
+            self.comp.wait_event(self.ev_in[c])
+            if self.started:
+                self.comp.wait_event(self.ev_back[c])  # previous D2H of this chunk read y
+            cap.replay(stream=self.comp)
+            self.ev_out[c].record(self.comp)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.ev_out[c])
+                y_host[rows].copy_(cap.y, non_blocking=True)
+                self.ev_back[c].record(self.d2h)
+        self.started = True
+        cur.wait_stream(self.d2h)
+        cur.wait_stream(self.comp)
+        return y_host
+
+
 @dataclass
 class BlockStats:
     """Device tensors describing the last forward (read them after a sync)."""
@@ -303,6 +354,10 @@ class HarMoEnyBlock:
             graphs.append(("+".join(grp), g))
         torch.cuda.synchronize(self.device)
         return CapturedForward(graphs, x, st["y"], self.stats)
+
+    def host_pipeline(self, num_tokens: int, n_chunks: int = 4) -> HostPipeline:
+        """Pinned-host end-to-end forward with H2D / compute / D2H overlapped by chunks."""
+        return HostPipeline(self, num_tokens, n_chunks)
 
     def forward_host(self, x_host: torch.Tensor, y_host: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """Public end-to-end call with host buffers: H2D of x (pinned -> HBM), the block,

@@ -90,14 +90,12 @@ __global__ void __launch_bounds__(kRThreads, 1)
       const uint64_t pol_w = l2_policy_evict_last();
       // the whole x tile (128 rows x d) is requested from HBM up front; the staged
       // TMA loads below then hit L2 instead of exposing DRAM latency per stage
-      // every CTA reads the same Wg: rotate the K order per CTA so concurrent CTAs hit
-      // different Wg slices (no L2 hot spot); the fp32 sum order is fixed per tile
-      const int k0 = (int)(blockIdx.x % (unsigned)KB);
-      for (int i = kRStages; i < KB; ++i) tma_prefetch_l2_2d(&tmap_x, ((i + k0) % KB) * kRBK, row0);
+      // fixed K order for every tile: a token's logits do not depend on its position in
+      // the batch (chunked / micro-batched forwards route identically)
+      for (int kb = kRStages; kb < KB; ++kb) tma_prefetch_l2_2d(&tmap_x, kb * kRBK, row0);
       int stage = 0;
       uint32_t phase = 0;
-      for (int i = 0; i < KB; ++i) {
-        const int kb = (i + k0) % KB;
+      for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], kRA + b_bytes);
         tma_load_2d(smem_a + stage * kRA, &tmap_x, &full[stage], kb * kRBK, row0, pol_x);

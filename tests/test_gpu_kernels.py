@@ -318,6 +318,25 @@ def test_graph_capture_matches_eager():
     assert torch.equal(cap(x2).clone(), blk(x2))
 
 
+def test_host_pipeline_matches_device_forward():
+    """Chunked pinned-host pipeline (H2D/compute/D2H overlap) == one device forward:
+    tokens are independent and routing is batch-position invariant."""
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    cfg = MoEConfig(eq_tokens=2, d_model=256, num_experts=32, d_ff=256, top_k=4, activation="swiglu")
+    blk = _block(cfg, seed=4, dev=dev, zipf_s=1.1)
+    x = torch.randn((1024, 256), device=dev).to(torch.bfloat16)
+    y_ref = blk(x).cpu()
+    pipe = blk.host_pipeline(1024, n_chunks=4)
+    x_host = x.cpu().pin_memory()
+    y_host = torch.empty((1024, 256), dtype=torch.bfloat16, pin_memory=True)
+    for _ in range(3):
+        pipe.run(x_host, y_host)
+        torch.cuda.synchronize()
+        assert torch.equal(y_host, y_ref)
+
+
 def test_dispatch_positions_follow_contract():
     """pos[t,j] lands in the scheduled destination's region (split-bucket contract)."""
     from paper_2506_12417_b200.block import MoEConfig
