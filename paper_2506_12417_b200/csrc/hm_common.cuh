@@ -235,8 +235,11 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* local, uint32_t rank
   return r;
 }
 
+// Remote arrive with default (.release.cta) semantics: orders only this thread's shared /
+// tcgen05 traffic (callers fence tcgen05 first).  A .cluster-scope release would add a
+// MEMBAR.ALL.GPU that drains every outstanding global store of the epilogue per tile.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <uint32_t kCols>

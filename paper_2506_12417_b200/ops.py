@@ -149,7 +149,8 @@ def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, 
     iters = torch.empty(1, **i32)
     loads = torch.empty(G, **i32)
     cap = G * E
-    lay = Layout(torch.zeros((G, E, G), **i32), torch.empty((cap, 4), **i32), torch.empty(1, **i32),
+    # slot_base rows the permute reads (every source in LOCAL, row `me` in EP) are all written
+    lay = Layout(torch.empty((G, E, G), **i32), torch.empty((cap, 4), **i32), torch.empty(1, **i32),
                  torch.empty(cap + 1, **i32), torch.empty(E, **i32), torch.empty(1, **i32))
     _lib.call("hm_plan", _ptr(tile_hist), int(tiles_per_rank), _ptr(m_all), _ptr(home), G, E, int(q),
               int(bool(rebalance)), int(mode), int(me), _ptr(m_out) if tile_hist is not None else None,

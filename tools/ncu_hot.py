@@ -13,14 +13,24 @@ def main():
     rep, kre = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 25
     view = "cuda" if "--cuda" in sys.argv else "sass"
+    skip = [a for a in sys.argv if a.startswith("--skip=")]
+    extra = ["--launch-skip", skip[0].split("=")[1], "--launch-count", "1"] if skip else []
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kre}",
-                          "--print-source", view], capture_output=True, text=True).stdout
+                          "--print-source", view] + extra, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr_i = next(i for i, r in enumerate(rows) if "Source" in r and ("Address" in r or "Line No" in r or "#" in r))
     h = rows[hdr_i]
     si = h.index("Source")
     wi = h.index("Warp Stall Sampling (All Samples)")
-    body = [r for r in rows[hdr_i + 1:] if len(r) > wi]
+    body = []
+    for r in rows[hdr_i + 1:]:
+        if len(r) <= wi:
+            continue
+        try:
+            float(r[wi] or 0)
+        except ValueError:
+            break  # next kernel's header: first instance only
+        body.append(r)
     # first kernel instance only
     tot = sum(float(r[wi] or 0) for r in body)
     ranked = sorted(range(len(body)), key=lambda i: -float(body[i][wi] or 0))[:top]
