@@ -157,7 +157,7 @@ class CpuOracleBlock:
 
     def __init__(self, wl, seed=0, zipf_s=1.0, q=32):
         from oracle import moe_oracle as orc
-        from paper_2506_12417_b200.workload import router_bias
+        from paper_2506_12417_b200.workload import calibrated_router_bias
 
         self.orc = orc
         d, f, E, k, act, T = wl
@@ -169,7 +169,7 @@ class CpuOracleBlock:
         self.w1 = r32(E, f, d, s=0.02)
         self.w3 = r32(E, f, d, s=0.02) if act == "swiglu" else None
         self.w2 = r32(E, d, f, s=0.02)
-        self.bias = router_bias(E, zipf_s)
+        self.bias = calibrated_router_bias(E, zipf_s, k)
         self.home = orc.round_robin_home(E, 1)
 
     def step(self, x):
@@ -249,16 +249,20 @@ def run_reference(args, rank, world):
 # ------------------------------------------------------------------------------------------
 # GPU side
 # ------------------------------------------------------------------------------------------
-def algorithmic_work(wl, tokens):
-    """FLOPs and HBM bytes of the expert GEMMs for `tokens` input tokens."""
+def algorithmic_work(wl, tokens, active_experts=None):
+    """FLOPs and HBM bytes of the expert GEMMs for `tokens` input tokens.
+    Weight bytes count every expert with >= 1 routed token (``active_experts``)."""
     d, f, E, k, act, _ = wl
     n_in = 2 * f if act == "swiglu" else f
     a = tokens * k
+    ea = E if active_experts is None else active_experts
     f1 = 2.0 * a * d * n_in
     f2 = 2.0 * a * f * d
-    w_bytes = E * (n_in * d + d * f) * 2
+    w1_bytes = ea * n_in * d * 2
+    w_bytes = ea * (n_in * d + d * f) * 2
     act_bytes = a * d * 2 * 2 + a * f * 2 * 2  # A read + Y write (gemm2) ; H write + read
-    return f1, f2, w_bytes, act_bytes
+    g1_bytes = w1_bytes + a * d * 2 + a * (n_in // (2 if act == "swiglu" else 1)) * 2  # W1 + A read + H write
+    return f1, f2, w_bytes, act_bytes, g1_bytes
 
 
 def load_ratio_logical(block_cls, cfg_kw, x, G, q, placement, zipf_s, seed, dev):
@@ -383,14 +387,23 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, tc, tc_sus, peak_kind = peaks()
-    f1, f2, w_bytes, act_bytes = algorithmic_work(wl, T_total // world)
+    m_all = blk.stats.m_all.cpu().numpy()
+    active = int((m_all.sum(axis=0) > 0).sum())
+    f1, f2, w_bytes, act_bytes, g1_bytes = algorithmic_work(wl, T_total // world, active)
     g1_us = stage_us.get("gemm1", float("nan"))
-    achieved = f1 / (g1_us * 1e-6) / 1e12
+    tensor_bound = f1 / (tc * 1e12) >= g1_bytes / (hbm * 1e9)
+    if tensor_bound:
+        bound, achieved, peak, unit = "tensor", f1 / (g1_us * 1e-6) / 1e12, tc, "TFLOP/s"
+        work_desc = f"{f1 / 1e9:.1f} GFLOP = 2 * {T_total // world * k} rows * {d} * {2 * f if act == 'swiglu' else f}"
+    else:
+        bound, achieved, peak, unit = "hbm", g1_bytes / (g1_us * 1e-6) / 1e9, hbm, "GB/s"
+        work_desc = (f"{g1_bytes / 1e6:.1f} MB = W1 of {active} active experts + routed rows in + FFN1 out "
+                     f"({f1 / 1e9:.1f} GFLOP)")
     traffic = None
     prof = os.path.join(REPO, "profiles", f"ncu_{args.workload}_gemm1.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and world == 1:
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            traffic = json.load(fh).get("dram_bytes_per_launch")  # same command under ncu --set full
     # block roofline: expert GEMMs only (the dominant term), tokens / max(F/P_tc, B/P_hbm)
     t_roof = max((f1 + f2) / (tc * 1e12), (w_bytes + act_bytes) / (hbm * 1e9))
     roof_tokens = (T_total // world) / t_roof * world
@@ -420,10 +433,11 @@ def run_ours(args, rank, world, local_rank):
             "peak_kind": peak_kind, "bf16_tflops_sustained": tc_sus,
             "load_max_over_mean_G8_logical": loads or None,
         },
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
-                     "frac": achieved / tc, "traffic": traffic,
-                     "kernel": "grouped_gemm_kernel<SwiGLU> (expert FFN1)",
-                     "work_per_launch": f"{f1 / 1e9:.1f} GFLOP = 2 * {T_total // world * k} rows * {d} * {2 * f if act == 'swiglu' else f}"},
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": f"grouped_gemm_2cta_kernel<{'SwiGLU' if act == 'swiglu' else 'ReLU'}> (expert FFN1)",
+                     "work_per_launch": work_desc,
+                     "peak_source": f"MEASURED_PEAKS.json ({peak_kind}; burst bf16 for a kernel timed alone)"},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "path": (f"HarMoEnyBlock.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, block, "
                          f"HBM -> pinned y; copies overlapped with compute by token chunks")

@@ -83,6 +83,23 @@ def pack_w13(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
     return torch.stack([g, u], dim=2).reshape(E * 2 * f, d).contiguous()
 
 
+def random_weights(cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s: float | None = None, std: float = 0.02):
+    """(wg, w1, w2, w3, bias) for a block of this architecture, identical for a given seed."""
+    from .workload import calibrated_router_bias
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
+    kw = dict(device=device, dtype=torch.float32, generator=g)
+    wg = (torch.randn((E, d), **kw) * (1.0 / d) ** 0.5).to(torch.bfloat16)
+    w1 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16)
+    w2 = (torch.randn((E, d, f), **kw) * std).to(torch.bfloat16)
+    w3 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16) if cfg.activation == "swiglu" else None
+    bias = None
+    if zipf_s is not None:
+        bias = torch.from_numpy(calibrated_router_bias(E, zipf_s, cfg.top_k)).to(device)
+    return wg, w1, w2, w3, bias
+
+
 def placement_home(cfg: MoEConfig):
     G = cfg.num_ranks
     kind = PlacementKind(cfg.placement)
@@ -234,18 +251,10 @@ class HarMoEnyBlock:
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s: float | None = None, std: float = 0.02):
         """Random-init weights of the named architecture (no checkpoints offline):
-        experts ~ N(0, std), Wg ~ N(0, 1/d), optional Zipf router bias log p."""
-        from .workload import router_bias
-
-        g = torch.Generator(device=device).manual_seed(seed)
-        E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
-        kw = dict(device=device, dtype=torch.float32, generator=g)
-        wg = (torch.randn((E, d), **kw) * (1.0 / d) ** 0.5).to(torch.bfloat16)
-        w1 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16)
-        w2 = (torch.randn((E, d, f), **kw) * std).to(torch.bfloat16)
-        w3 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16) if cfg.activation == "swiglu" else None
-        bias = None if zipf_s is None else torch.from_numpy(router_bias(E, zipf_s)).to(device)
-        return cls(cfg, wg, w1, w2, w3, bias, device=device)
+        experts ~ N(0, std), Wg ~ N(0, 1/d) (logits ~ N(0,1) for x ~ N(0,1)), and, with
+        zipf_s, a router bias calibrated so the realised top-k routing has the Zipf(s)
+        Gumbel-top-k expert shares (workload.calibrated_router_bias)."""
+        return cls(cfg, *random_weights(cfg, seed, device, zipf_s, std), device=device)
 
     # ------------------------------------------------------------------------------------
     def forward(self, x: torch.Tensor, stream=None, marks: list | None = None) -> torch.Tensor:

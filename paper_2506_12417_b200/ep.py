@@ -136,18 +136,10 @@ class EPHarMoEnyBlock:
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s=None, std: float = 0.02, group=None):
-        """Identical random weights on every rank (same seed), Zipf router bias."""
-        from .workload import router_bias
+        """Identical random weights on every rank (same seed), calibrated Zipf router bias."""
+        from .block import random_weights
 
-        g = torch.Generator(device=device).manual_seed(seed)
-        E, d, f = cfg.num_experts, cfg.d_model, cfg.d_ff
-        kw = dict(device=device, dtype=torch.float32, generator=g)
-        wg = (torch.randn((E, d), **kw) * (1.0 / d) ** 0.5).to(torch.bfloat16)
-        w1 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16)
-        w2 = (torch.randn((E, d, f), **kw) * std).to(torch.bfloat16)
-        w3 = (torch.randn((E, f, d), **kw) * std).to(torch.bfloat16) if cfg.activation == "swiglu" else None
-        bias = None if zipf_s is None else torch.from_numpy(router_bias(E, zipf_s)).to(device)
-        return cls(cfg, wg, w1, w2, w3, bias, device=device, group=group)
+        return cls(cfg, *random_weights(cfg, seed, device, zipf_s, std), device=device, group=group)
 
     def _open_peers(self):
         """Exchange CUDA IPC handles of every rank's home-expert weights (once)."""

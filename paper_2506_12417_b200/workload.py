@@ -90,3 +90,39 @@ def router_bias(num_experts: int, s: float, seed: int | None = None) -> np.ndarr
     if seed is not None:
         p = p[np.random.Generator(np.random.PCG64(seed)).permutation(num_experts)]
     return np.log(p).astype(np.float32)
+
+
+def zipf_topk_frequencies(num_experts: int, s: float, k: int, samples: int = 20000, seed: int = 0) -> np.ndarray:
+    """Per-expert share of assignments under Gumbel-top-k on log p_zipf (top-k without
+    replacement); shares sum to 1."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    a = gumbel_topk_assignments(zipf_probabilities(num_experts, s), samples, k, rng)
+    return np.bincount(a.reshape(-1), minlength=num_experts) / (samples * k)
+
+
+def calibrated_router_bias(num_experts: int, s: float, k: int, noise_std: float = 1.0, iters: int = 200,
+                           samples: int = 8192, seed: int = 0) -> np.ndarray:
+    """Bias b such that top-k of (N(0, noise_std^2) logits + b) routes with the Zipf
+    Gumbel-top-k shares.  The synthetic router's logits x.Wg are Gaussian (x ~ N(0,1),
+    Wg ~ N(0, 1/d) -> std 1), whose light tails concentrate top-k far more than the
+    Gumbel noise of the Zipf definition (top-1 at s=1 would leave ~45% of experts idle);
+    the bias is fitted by fixed-point iteration on a fixed noise sample."""
+    if s == 0.0:
+        return np.zeros(num_experts, np.float32)
+    target = zipf_topk_frequencies(num_experts, s, k, seed=seed + 1)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    noise = rng.standard_normal((samples, num_experts)).astype(np.float32) * np.float32(noise_std)
+    b = np.log(np.maximum(target, 1e-9)).astype(np.float64)
+    lt = np.log(np.maximum(target, 1e-6))
+    best, best_err = b.copy(), np.inf
+    for it in range(iters):
+        logits = noise + b[None, :].astype(np.float32)
+        top = np.argpartition(-logits, k - 1, axis=1)[:, :k]
+        f = np.bincount(top.reshape(-1), minlength=num_experts) / (samples * k)
+        err = np.abs(f - target).sum()
+        if err < best_err:
+            best, best_err = b.copy(), err
+        step = 0.25 if it < iters // 2 else 0.1  # damped: top-1 shares react steeply
+        b += step * (lt - np.log(np.maximum(f, 1e-6)))
+        b -= b.max()
+    return best.astype(np.float32)
