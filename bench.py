@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="qwen128", choices=sorted(WORKLOADS))
+    ap.add_argument("--layers", type=int, default=1, help="MoE decoder layers per step (BASELINE config 4)")
     ap.add_argument("--zipf", type=float, default=1.0)
     ap.add_argument("--q", type=int, default=32)
     ap.add_argument("--placement", default="round_robin")
@@ -297,6 +298,12 @@ def run_ours(args, rank, world, local_rank):
     else:
         cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, **cfg_kw)
         blk = HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
+    if args.layers > 1:  # BASELINE config 4: decoder stack, one step = all layers
+        from paper_2506_12417_b200.stack import MoEStack
+
+        del blk
+        blk = MoEStack.random(cfg, args.layers, seed=0, device=dev, zipf_s=args.zipf)
+    stats0 = (lambda: blk.stats[0]) if args.layers > 1 else (lambda: blk.stats)
     T_local = T_total // world
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn((T_local, d), device=dev, generator=g).to(torch.bfloat16)
@@ -387,7 +394,7 @@ def run_ours(args, rank, world, local_rank):
     if rank != 0:
         return
     hbm, tc, tc_sus, peak_kind = peaks()
-    m_all = blk.stats.m_all.cpu().numpy()
+    m_all = stats0().m_all.cpu().numpy()
     active = int((m_all.sum(axis=0) > 0).sum())
     f1, f2, w_bytes, act_bytes, g1_bytes = algorithmic_work(wl, T_total // world, active)
     g1_us = stage_us.get("gemm1", float("nan"))
@@ -405,7 +412,7 @@ def run_ours(args, rank, world, local_rank):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")  # same command under ncu --set full
     # block roofline: expert GEMMs only (the dominant term), tokens / max(F/P_tc, B/P_hbm)
-    t_roof = max((f1 + f2) / (tc * 1e12), (w_bytes + act_bytes) / (hbm * 1e9))
+    t_roof = max((f1 + f2) / (tc * 1e12), (w_bytes + act_bytes) / (hbm * 1e9)) * args.layers
     roof_tokens = (T_total // world) / t_roof * world
     loads = {}
     if world == 1 and args.gpus == 1:
@@ -422,8 +429,12 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {
-            "workload": f"{args.workload} MoE layer (BASELINE configs[1]), {T_total} tokens, Zipf s={args.zipf} router "
-                        f"bias, random-init weights",
+            "workload": (f"{args.workload} MoE layer" + (f" x {args.layers}-layer decoder stack (BASELINE configs[3])"
+                                                          if args.layers > 1 else
+                                                          (" (BASELINE configs[1])" if args.workload == "qwen128"
+                                                           else "")) +
+                         f", {T_total} tokens, calibrated Zipf s={args.zipf} routing, random-init weights"),
+            "layers": args.layers,
             "d_model": d, "d_ff": f, "experts": E, "top_k": k, "activation": act, "tokens": T_total,
             "q": args.q, "placement": args.placement, "parallelism": f"ep{world}" if world > 1 else "single-gpu",
             "l2": "flushed between timed steps (256 MB write)",
@@ -442,7 +453,7 @@ def run_ours(args, rank, world, local_rank):
                 "path": (f"HarMoEnyBlock.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, block, "
                          f"HBM -> pinned y; copies overlapped with compute by token chunks")
                 if graphed and args.e2e_chunks > 1 else "forward_host (pinned H2D -> block -> D2H)"},
-        "gpu_launches": HarMoEnyBlock.KERNELS_PER_FORWARD * args.steps,
+        "gpu_launches": blk.KERNELS_PER_FORWARD * args.steps,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
     }

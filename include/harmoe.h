@@ -179,10 +179,11 @@ HM_API int hm_ipc_close(void* dev_ptr);
 /*
  * Combine (K7): y[t] = sum_j w[t,j] * Y[pos[t,j]] in fp32, slots in order j = 0..k-1, bf16 out.
  * pos == NULL means Y is token-major [T*k, d] (row t*k + j), the layout the FFN2 epilogue writes
- * through row_map.
+ * through row_map.  residual [T, d] bf16 or NULL: decoder residual fused in, the fp32
+ * accumulation starts from it (y = x + sum_j w Y_j).
  */
-HM_API int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y,
-               void* stream);
+HM_API int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d,
+                      const void* residual, void* y, void* stream);
 
 #ifdef __cplusplus
 }

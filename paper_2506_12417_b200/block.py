@@ -51,6 +51,7 @@ class MoEConfig:
     placement: str = "round_robin"
     logical_ranks: int = 1  # LOCAL mode: number of simulated GPUs (world_size must be 1)
     fetch_source: str = "peer"  # EP mode: "peer" (NVLink) or "host" (pinned host memory)
+    residual: bool = False  # decoder-layer residual y = x + MoE(x), fused into the combine kernel
 
     def __post_init__(self):
         if self.eq_tokens < 1:
@@ -325,7 +326,7 @@ class HarMoEnyBlock:
                                         row_map=st["inv"], stream=s)
 
         def combine():
-            st["y"] = ops.combine(st["ys"], None, st["w"], stream=s)
+            st["y"] = ops.combine(st["ys"], None, st["w"], residual=st["x"] if cfg.residual else None, stream=s)
 
         return [("router", router), ("schedule", plan), ("permute", permute), ("gemm1", gemm1),
                 ("gemm2", gemm2), ("combine", combine)]
@@ -333,16 +334,19 @@ class HarMoEnyBlock:
     KERNELS_PER_FORWARD = 6  # router, plan, permute, gemm1, gemm2, combine
 
     def capture(self, num_tokens: int, groups=(("router", "schedule", "permute"), ("gemm1",), ("gemm2",),
-                                               ("combine",))) -> "CapturedForward":
+                                               ("combine",)), x_static: torch.Tensor | None = None,
+                pool=None) -> "CapturedForward":
         """CUDA-graph the forward for a fixed token count.  The LOCAL forward never
         synchronises the host, so every kernel is captured; replay removes the launch gaps.
         Stages are captured in ``groups`` (one graph per group) so a caller can time
-        groups with stream events between replays.  Write inputs into ``.x``."""
+        groups with stream events between replays.  Write inputs into ``.x`` (or pass
+        ``x_static``, e.g. the previous layer's static output)."""
         cfg = self.cfg
         G = cfg.num_ranks
         if num_tokens % G:
             raise ValueError("token count must divide evenly over the logical ranks")
-        x = torch.zeros((num_tokens, cfg.d_model), dtype=torch.bfloat16, device=self.device)
+        x = x_static if x_static is not None else torch.zeros((num_tokens, cfg.d_model), dtype=torch.bfloat16,
+                                                              device=self.device)
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
@@ -351,7 +355,7 @@ class HarMoEnyBlock:
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize(self.device)
         st = {"x": x}
-        pool = torch.cuda.graph_pool_handle()
+        pool = pool if pool is not None else torch.cuda.graph_pool_handle()
         graphs = []
         with torch.cuda.stream(side):
             stages = dict(self._stages(st, G, num_tokens // G, side))

@@ -84,7 +84,7 @@ int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, 
                   int32_t*, int32_t*, cudaStream_t);
 int launch_permute(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int,
                    int, int, int, int, int, int, void*, int32_t*, int32_t*, cudaStream_t);
-int launch_combine(const void*, const int32_t*, const float*, int, int, int, void*, cudaStream_t);
+int launch_combine(const void*, const int32_t*, const float*, int, int, int, const void*, void*, cudaStream_t);
 
 __global__ void publish_flag_kernel(int32_t* flag, int epoch) {
   __threadfence_system();
@@ -200,8 +200,9 @@ int hm_ipc_close(void* dev_ptr) {
   return HM_OK;
 }
 
-int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y, void* stream) {
-  return launch_combine(Y, pos, topk_w, T, k, d, y, as_stream(stream));
+int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, const void* residual,
+               void* y, void* stream) {
+  return launch_combine(Y, pos, topk_w, T, k, d, residual, y, as_stream(stream));
 }
 
 }  // extern "C"

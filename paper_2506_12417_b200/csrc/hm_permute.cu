@@ -99,15 +99,27 @@ __global__ void __launch_bounds__(256)
 template <int VEC>
 __global__ void __launch_bounds__(kPermWarps * 32)
     combine_kernel(const uint4* __restrict__ Y, const int32_t* __restrict__ pos, const float* __restrict__ w,
-                   int64_t T, int k, int n16, uint4* __restrict__ y) {
+                   int64_t T, int k, int n16, const uint4* __restrict__ residual, uint4* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
   if (t >= T) return;
   float acc[VEC][8];
 #pragma unroll
-  for (int i = 0; i < VEC; ++i)
+  for (int i = 0; i < VEC; ++i) {
+    const int c = i * 32 + lane;
+    if (residual != nullptr && c < n16) {
+      const uint4 rv = ld_global_nc_v4(residual + t * n16 + c);
+      const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
-    for (int c = 0; c < 8; ++c) acc[i][c] = 0.0f;
+      for (int h = 0; h < 4; ++h) {
+        acc[i][2 * h] = bf16lo(rr[h]);
+        acc[i][2 * h + 1] = bf16hi(rr[h]);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) acc[i][h] = 0.0f;
+    }
+  }
   for (int j = 0; j < k; ++j) {
     const int64_t p = __ldg(pos + t * k + j);
     const float wj = __ldg(w + t * k + j);
@@ -142,7 +154,7 @@ __global__ void __launch_bounds__(kPermWarps * 32)
 template <int KT>
 __global__ void __launch_bounds__(kPermWarps * 32)
     combine_dense_kernel(const uint4* __restrict__ Y, const float* __restrict__ w, int64_t T, int k, int n16,
-                         uint4* __restrict__ y) {
+                         const uint4* __restrict__ residual, uint4* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
   if (t >= T) return;
@@ -158,8 +170,19 @@ __global__ void __launch_bounds__(kPermWarps * 32)
     for (int j = 0; j < (KT > 0 ? KT : 16); ++j)
       if (j < kk) u[j] = ld_global_nc_v4(base + (int64_t)j * n16 + c);
     float acc[8];
+    if (residual != nullptr) {
+      // decoder residual fused in: y = x + sum_j w_j Y_j (accumulation starts from x)
+      const uint4 rv = ld_global_nc_v4(residual + t * n16 + c);
+      const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
-    for (int h = 0; h < 8; ++h) acc[h] = 0.0f;
+      for (int h = 0; h < 4; ++h) {
+        acc[2 * h] = bf16lo(rr[h]);
+        acc[2 * h + 1] = bf16hi(rr[h]);
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) acc[h] = 0.0f;
+    }
 #pragma unroll
     for (int j = 0; j < (KT > 0 ? KT : 16); ++j) {
       if (j < kk) {
@@ -211,8 +234,8 @@ int launch_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank,
   return check_launch("permute");
 }
 
-int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, void* y,
-                   cudaStream_t stream) {
+int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d, const void* residual,
+                   void* y, cudaStream_t stream) {
   if (d <= 0 || d % 8 != 0 || d > 8192) return set_error(HM_EINVAL, "combine: need d %% 8 == 0 and d <= 8192");
   if (T < 0 || k < 1) return set_error(HM_EINVAL, "combine: bad sizes");
   if (T == 0) return HM_OK;
@@ -221,9 +244,11 @@ int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T
   const unsigned grid = (unsigned)((T + kPermWarps - 1) / kPermWarps);
   auto* Ys = reinterpret_cast<const uint4*>(Y);
   auto* o = reinterpret_cast<uint4*>(y);
+  auto* res = reinterpret_cast<const uint4*>(residual);
   if (pos == nullptr) {
     if (k > 16) return set_error(HM_EINVAL, "combine: dense layout needs k <= 16");
-#define HM_DENSE(KT) combine_dense_kernel<KT><<<grid, kPermWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, o)
+#define HM_DENSE(KT) \
+  combine_dense_kernel<KT><<<grid, kPermWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, res, o)
     if (k == 1) HM_DENSE(1);
     else if (k == 2) HM_DENSE(2);
     else if (k == 4) HM_DENSE(4);
@@ -232,7 +257,7 @@ int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T
 #undef HM_DENSE
     return check_launch("combine_dense");
   }
-#define HM_COMB(V) combine_kernel<V><<<grid, kPermWarps * 32, 0, stream>>>(Ys, pos, topk_w, T, k, n16, o)
+#define HM_COMB(V) combine_kernel<V><<<grid, kPermWarps * 32, 0, stream>>>(Ys, pos, topk_w, T, k, n16, res, o)
   if (vec <= 1) HM_COMB(1);
   else if (vec <= 2) HM_COMB(2);
   else if (vec <= 4) HM_COMB(4);

@@ -243,7 +243,7 @@ class EPHarMoEnyBlock:
             mark("gemm2")
             ys = return_tokens(yr, send_counts, recv_counts, self.group)
             mark("combine_a2a")
-            y = ops.combine(ys, pos, w, stream=s)
+            y = ops.combine(ys, pos, w, residual=x if cfg.residual else None, stream=s)
             mark("combine")
         self.stats = BlockStats(m_all=m_all, schedule=S, iters=iters, loads=loads,
                                 extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay, n_fetch=n_fetch,

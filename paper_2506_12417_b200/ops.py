@@ -212,12 +212,12 @@ def fetch_expert(dst, src, ready_flag=None, epoch: int = 0, stream=None):
               None if ready_flag is None else ready_flag.data_ptr(), int(epoch), _stream(stream))
 
 
-def combine(Y, pos, topk_w, out=None, stream=None):
-    """K7.  y [T, d] bf16 = sum_j w[t,j] * Y[pos[t,j]]; pos=None: Y is token-major [T*k, d]."""
-    _require_cuda(Y, pos, topk_w)
+def combine(Y, pos, topk_w, out=None, residual=None, stream=None):
+    """K7.  y [T, d] bf16 = (residual +) sum_j w[t,j] * Y[pos[t,j]]; pos=None: Y is token-major [T*k, d]."""
+    _require_cuda(Y, pos, topk_w, residual)
     T, k = topk_w.shape
     d = Y.shape[1]
     if out is None:
         out = torch.empty((T, d), dtype=torch.bfloat16, device=Y.device)
-    _lib.call("hm_combine", _ptr(Y), _ptr(pos), _ptr(topk_w), T, k, d, _ptr(out), _stream(stream))
+    _lib.call("hm_combine", _ptr(Y), _ptr(pos), _ptr(topk_w), T, k, d, _ptr(residual), _ptr(out), _stream(stream))
     return out

@@ -337,6 +337,41 @@ def test_host_pipeline_matches_device_forward():
         assert torch.equal(y_host, y_ref)
 
 
+def test_stack_matches_oracle_and_graph():
+    """BASELINE config 4: 3-layer decoder stack h += MoE_l(h) (residual fused in the combine)
+    vs the oracle applied layer by layer on the GPU's own routing; graph replay == eager."""
+    from paper_2506_12417_b200.block import MoEConfig
+    from paper_2506_12417_b200.stack import MoEStack
+
+    dev = _cuda()
+    cfg = MoEConfig(logical_ranks=2, eq_tokens=2, placement="blocked", d_model=256, num_experts=16, d_ff=256,
+                    top_k=2, activation="swiglu")
+    st = MoEStack.random(cfg, 3, seed=3, device=dev, zipf_s=1.0, std=0.05)
+    x = torch.randn((512, 256), device=dev).to(torch.bfloat16)
+    y = st(x).clone()
+    torch.cuda.synchronize()
+    E, f, d = 16, 256, 256
+    h_gpu = x
+    for blk in st.layers:
+        # each layer checked on the GPU's own input (near-tie routing flips would otherwise
+        # compound across layers); residual: kernel accumulates x + sum_j w Y_j in fp32
+        h_next = blk(h_gpu).clone()
+        torch.cuda.synchronize()
+        w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, d)
+        y_moe, idx_ref, _, _ = orc.moe_block(bits(h_gpu), bits(blk.wg[:E]), blk.bias.cpu().numpy(),
+                                             w13[:, :, 0].reshape(E, f, d), bits(blk.w_out).reshape(E, d, f), 2,
+                                             "swiglu", True, w13[:, :, 1].reshape(E, f, d))
+        ok = np.all(blk.stats.extras["topk_idx"].cpu().numpy() == idx_ref, axis=1)
+        assert ok.mean() > 0.97
+        ref = orc.bf16_to_f32(bits(h_gpu)) + orc.bf16_to_f32(y_moe)
+        assert_close(orc.bf16_to_f32(bits(h_next))[ok], ref[ok], "stack layer")
+        h_gpu = h_next
+    assert torch.equal(h_gpu, y)  # chained layer calls == stack forward
+    cap = st.capture(512)
+    cap.x.copy_(x)
+    assert torch.equal(cap.replay().clone(), y)
+
+
 def test_dispatch_positions_follow_contract():
     """pos[t,j] lands in the scheduled destination's region (split-bucket contract)."""
     from paper_2506_12417_b200.block import MoEConfig
