@@ -172,7 +172,8 @@ HM_API int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* re
  * handle (host buffer), open a peer's handle in this process, close it.  The expert-parallel
  * layer exchanges handles once at setup so every rank can fetch any home expert directly.
  */
-HM_API int hm_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 B, host */);
+HM_API int hm_ipc_get_handle(const void* dev_ptr, void* handle_out /* 64 B, host */,
+                             size_t* offset_out /* dev_ptr - allocation base, or NULL */);
 HM_API int hm_ipc_open(const void* handle /* 64 B, host */, void** dev_ptr_out);
 HM_API int hm_ipc_close(void* dev_ptr);
 

@@ -39,7 +39,7 @@ SIGNATURES = {
     "hm_fetch_expert": [_vp, _vp, ctypes.c_size_t, _vp, _i32, _vp],
     "hm_combine": [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_debug_plan_phases": [_vp],
-    "hm_ipc_get_handle": [_vp, _vp],
+    "hm_ipc_get_handle": [_vp, _vp, ctypes.POINTER(ctypes.c_size_t)],
     "hm_ipc_open": [_vp, ctypes.POINTER(ctypes.c_void_p)],
     "hm_ipc_close": [_vp],
 }

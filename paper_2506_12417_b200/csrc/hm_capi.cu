@@ -43,6 +43,7 @@ int num_sms() {
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+static PFN_cuMemGetAddressRange_v3020 g_addr_range = nullptr;
 static std::once_flag g_driver_once;
 
 static void load_driver_entry_points() {
@@ -55,6 +56,10 @@ static void load_driver_entry_points() {
   if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
       q == cudaDriverEntryPointSuccess)
     g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(fn);
+  fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_addr_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
 }
 
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
@@ -178,11 +183,22 @@ int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_fla
 
 int hm_debug_plan_phases(long long* out4) { return read_plan_phases(out4); }
 
-int hm_ipc_get_handle(const void* dev_ptr, void* handle_out) {
+int hm_ipc_get_handle(const void* dev_ptr, void* handle_out, size_t* offset_out) {
+  std::call_once(g_driver_once, load_driver_entry_points);
   cudaIpcMemHandle_t h;
   const cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));
   if (e != cudaSuccess) return set_error(HM_ECUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
   memcpy(handle_out, &h, sizeof(h));
+  // the handle names the whole allocation (e.g. a caching-allocator block): report where
+  // dev_ptr sits inside it so the peer can add it to the base cudaIpcOpenMemHandle returns
+  if (offset_out != nullptr) {
+    if (g_addr_range == nullptr) return set_error(HM_ECUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    const CUresult r = g_addr_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr));
+    if (r != CUDA_SUCCESS) return set_error(HM_ECUDA, "cuMemGetAddressRange failed (%d)", (int)r);
+    *offset_out = (size_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  }
   return HM_OK;
 }
 

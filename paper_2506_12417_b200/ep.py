@@ -42,11 +42,23 @@ def ep_counts(S: np.ndarray, me: int):
     return flows[me, :].tolist(), flows[:, me].tolist()
 
 
+def _host_staged(t: torch.Tensor, group) -> bool:
+    """gloo has no device collectives: stage CUDA tensors through host memory.  Only the
+    test harness runs EP ranks over gloo (several ranks sharing one GPU); production
+    runs one rank per GPU over NCCL."""
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
 def exchange_metadata(hist_local: torch.Tensor, group=None) -> torch.Tensor:
     """Step 2: all_gather of the local histogram [1, E] -> m_all [G, E]."""
     G = dist.get_world_size(group)
+    src = hist_local.reshape(1, -1).contiguous()
+    if _host_staged(src, group):
+        parts = [torch.empty_like(src, device="cpu") for _ in range(G)]
+        dist.all_gather(parts, src.cpu(), group=group)
+        return torch.cat(parts).to(hist_local.device)
     out = torch.empty((G, hist_local.shape[-1]), dtype=hist_local.dtype, device=hist_local.device)
-    dist.all_gather_into_tensor(out, hist_local.reshape(1, -1).contiguous(), group=group)
+    dist.all_gather_into_tensor(out, src, group=group)
     return out
 
 
@@ -55,8 +67,15 @@ def exchange_tokens(send_buf: torch.Tensor, send_counts, recv_counts, group=None
     rows = int(sum(recv_counts))
     if out is None:
         out = torch.empty((max(rows, 1), send_buf.shape[1]), dtype=send_buf.dtype, device=send_buf.device)
-    dist.all_to_all_single(out[:rows], send_buf[: int(sum(send_counts))], output_split_sizes=list(recv_counts),
-                           input_split_sizes=list(send_counts), group=group)
+    src = send_buf[: int(sum(send_counts))]
+    if _host_staged(src, group):  # raw bytes (gloo has no bf16 / int16 kernels)
+        h_out = torch.empty((rows, send_buf.shape[1] * send_buf.element_size()), dtype=torch.uint8)
+        dist.all_to_all_single(h_out, src.cpu().view(torch.uint8), output_split_sizes=list(recv_counts),
+                               input_split_sizes=list(send_counts), group=group)
+        out[:rows].copy_(h_out.view(send_buf.dtype))
+        return out
+    dist.all_to_all_single(out[:rows], src, output_split_sizes=list(recv_counts), input_split_sizes=list(send_counts),
+                           group=group)
     return out
 
 
@@ -147,21 +166,24 @@ class EPHarMoEnyBlock:
         hs = []
         for t in (self.w_in, self.w_out):
             buf = ctypes.create_string_buffer(64)
-            _lib.check(L.hm_ipc_get_handle(t.data_ptr(), buf), "hm_ipc_get_handle")
-            hs.append(bytes(buf.raw))
+            off = ctypes.c_size_t(0)
+            _lib.check(L.hm_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)), "hm_ipc_get_handle")
+            hs.append((bytes(buf.raw), int(off.value)))
         allh = [None] * self.G
         dist.all_gather_object(allh, hs, group=self.group)
         self.peer_in, self.peer_out = [], []
+        self._ipc_bases = []
         for g in range(self.G):
             if g == self.me:
                 self.peer_in.append(self.w_in.data_ptr())
                 self.peer_out.append(self.w_out.data_ptr())
                 continue
             ptrs = []
-            for h in allh[g]:
+            for h, off in allh[g]:
                 p = ctypes.c_void_p()
                 _lib.check(L.hm_ipc_open(h, ctypes.byref(p)), "hm_ipc_open")
-                ptrs.append(p.value)
+                self._ipc_bases.append(p.value)
+                ptrs.append(p.value + off)  # the handle maps the allocation base
             self.peer_in.append(ptrs[0])
             self.peer_out.append(ptrs[1])
 
