@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs (launch every kernel from Python)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = test harness for the multi-rank path on fewer GPUs (not a measurement)")
     ap.add_argument("--e2e-chunks", type=int, default=2,
                     help="token chunks of the pinned-host pipeline (H2D / compute / D2H overlap) for e2e")
     ap.add_argument("--kernel-table", action="store_true",
@@ -443,6 +445,7 @@ def run_ours(args, rank, world, local_rank):
             "block_roofline_frac": value / roof_tokens,
             "peak_kind": peak_kind, "bf16_tflops_sustained": tc_sus,
             "load_max_over_mean_G8_logical": loads or None,
+            "load_max_over_mean_this_run": stats0().load_imbalance(),
         },
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
@@ -473,8 +476,15 @@ def main():
     if world > 1:
         import torch
 
-        torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.backend == "gloo":
+            # test harness only: several EP ranks share the visible GPU(s), exchanges are
+            # host-staged; never a bench number
+            local_rank = local_rank % torch.cuda.device_count()
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_ours(args, rank, world, local_rank)
     finally:
