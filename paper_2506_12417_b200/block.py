@@ -153,17 +153,21 @@ class HostPipeline:
     Tokens are independent in the MoE block, so the output equals the unchunked forward
     (each chunk is routed, scheduled and combined on its own)."""
 
-    def __init__(self, block: "HarMoEnyBlock", num_tokens: int, n_chunks: int = 4):
+    def __init__(self, block: "HarMoEnyBlock", num_tokens: int, n_chunks: int = 4, n_sets: int = 2):
         if num_tokens % n_chunks or (num_tokens // n_chunks) % block.cfg.num_ranks:
             raise ValueError("chunk size must divide evenly (and over the logical ranks)")
         self.n, self.chunk = n_chunks, num_tokens // n_chunks
-        # one graph per chunk (all stages): minimal host work per launch
+        # one graph per chunk (all stages): minimal host work per launch.  ``n_sets`` buffer
+        # sets ping-pong between successive runs, so run i+1's H2D / forward never wait for
+        # run i's forward / D2H of the same chunk.
         all_stages = (("router", "schedule", "permute", "gemm1", "gemm2", "combine"),)
-        self.caps = [block.capture(self.chunk, groups=all_stages) for _ in range(n_chunks)]
+        self.sets = [[block.capture(self.chunk, groups=all_stages) for _ in range(n_chunks)] for _ in range(n_sets)]
         dev = block.device
         self.h2d, self.comp, self.d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
-        ev = lambda: [torch.cuda.Event() for _ in range(n_chunks)]  # noqa: E731
+        ev = lambda: [[torch.cuda.Event() for _ in range(n_chunks)] for _ in range(n_sets)]  # noqa: E731
         self.ev_in, self.ev_out, self.ev_back = ev(), ev(), ev()
+        self.used = [False] * n_sets
+        self.run_i = 0
         self.started = False
 
     def run(self, x_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
@@ -175,22 +179,26 @@ class HostPipeline:
         if not self.started:
             for s in (self.h2d, self.comp, self.d2h):
                 s.wait_stream(cur)
-        for c, cap in enumerate(self.caps):
+        b = self.run_i % len(self.sets)
+        ev_in, ev_out, ev_back = self.ev_in[b], self.ev_out[b], self.ev_back[b]
+        for c, cap in enumerate(self.sets[b]):
             rows = slice(c * self.chunk, (c + 1) * self.chunk)
             with torch.cuda.stream(self.h2d):
-                if self.started:
-                    self.h2d.wait_event(self.ev_out[c])  # previous forward of this chunk read x
+                if self.used[b]:
+                    self.h2d.wait_event(ev_out[c])  # the last forward on this buffer set read x
                 cap.x.copy_(x_host[rows], non_blocking=True)
-                self.ev_in[c].record(self.h2d)
-            self.comp.wait_event(self.ev_in[c])
-            if self.started:
-                self.comp.wait_event(self.ev_back[c])  # previous D2H of this chunk read y
+                ev_in[c].record(self.h2d)
+            self.comp.wait_event(ev_in[c])
+            if self.used[b]:
+                self.comp.wait_event(ev_back[c])  # the last D2H from this buffer set read y
             cap.replay(stream=self.comp)
-            self.ev_out[c].record(self.comp)
+            ev_out[c].record(self.comp)
             with torch.cuda.stream(self.d2h):
-                self.d2h.wait_event(self.ev_out[c])
+                self.d2h.wait_event(ev_out[c])
                 y_host[rows].copy_(cap.y, non_blocking=True)
-                self.ev_back[c].record(self.d2h)
+                ev_back[c].record(self.d2h)
+        self.used[b] = True
+        self.run_i += 1
         self.started = True
         cur.wait_stream(self.d2h)
         cur.wait_stream(self.comp)
