@@ -401,8 +401,13 @@ def run_ours(args, rank, world, local_rank):
     f1, f2, w_bytes, act_bytes, g1_bytes = algorithmic_work(wl, T_total // world, active)
     g1_us = stage_us.get("gemm1", float("nan"))
     tensor_bound = f1 / (tc * 1e12) >= g1_bytes / (hbm * 1e9)
+    # the GEMM runs inside a loop of back-to-back steps: once that loop lasts long enough for
+    # the 1 kW power cap to engage, the sustained cuBLAS figure is the honest denominator
+    long_region = t_step >= 100.0 or "sw_power_cap" in ((sampler.summary() or {}).get("reasons") or [])
+    tc_used = tc_sus if (long_region and tc_sus) else tc
+    peak_src = "sustained (timed loop >= 0.1 s / power-capped)" if tc_used != tc else "burst (short timed loop)"
     if tensor_bound:
-        bound, achieved, peak, unit = "tensor", f1 / (g1_us * 1e-6) / 1e12, tc, "TFLOP/s"
+        bound, achieved, peak, unit = "tensor", f1 / (g1_us * 1e-6) / 1e12, tc_used, "TFLOP/s"
         work_desc = f"{f1 / 1e9:.1f} GFLOP = 2 * {T_total // world * k} rows * {d} * {2 * f if act == 'swiglu' else f}"
     else:
         bound, achieved, peak, unit = "hbm", g1_bytes / (g1_us * 1e-6) / 1e9, hbm, "GB/s"
@@ -414,7 +419,7 @@ def run_ours(args, rank, world, local_rank):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")  # same command under ncu --set full
     # block roofline: expert GEMMs only (the dominant term), tokens / max(F/P_tc, B/P_hbm)
-    t_roof = max((f1 + f2) / (tc * 1e12), (w_bytes + act_bytes) / (hbm * 1e9)) * args.layers
+    t_roof = max((f1 + f2) / (tc_used * 1e12), (w_bytes + act_bytes) / (hbm * 1e9)) * args.layers
     roof_tokens = (T_total // world) / t_roof * world
     loads = {}
     if world == 1 and args.gpus == 1:
@@ -451,7 +456,8 @@ def run_ours(args, rank, world, local_rank):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"grouped_gemm_2cta_kernel<{'SwiGLU' if act == 'swiglu' else 'ReLU'}> (expert FFN1)",
                      "work_per_launch": work_desc,
-                     "peak_source": f"MEASURED_PEAKS.json ({peak_kind}; burst bf16 for a kernel timed alone)"},
+                     "peak_source": f"MEASURED_PEAKS.json ({peak_kind}; bf16 {peak_src}; burst {tc}, "
+                                    f"sustained {tc_sus} TFLOP/s; HBM {hbm} GB/s)"},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "path": (f"HarMoEnyBlock.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, block, "
                          f"HBM -> pinned y; copies overlapped with compute by token chunks")
