@@ -99,6 +99,41 @@ __device__ void dev_hist_reduce(const int32_t* __restrict__ tile_hist, int n_ran
     return;
   }
   const int chunk = (tpr + 7) / 8;
+  if (chunk <= 16) {
+    // one batch of independent loads per thread (one memory round trip instead of a chain)
+    for (int r = 0; r < n_ranks; ++r)
+      for (int e0 = 0; e0 < E; e0 += 128) {
+        const int e = e0 + el;
+        const int m_lo = min(tpr, sub * chunk), m_hi = min(tpr, m_lo + chunk);
+        int v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = (e < E && m_lo + j < m_hi) ? tile_hist[((int64_t)r * tpr + m_lo + j) * E + e] : 0;
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sum += v[j];
+        s_part[sub * 128 + el] = sum;
+        __syncthreads();
+        if (e < E) {
+          int run = 0;
+          for (int s = 0; s < sub; ++s) run += s_part[s * 128 + el];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (m_lo + j < m_hi) {
+              tile_off[((int64_t)r * tpr + m_lo + j) * E + e] = run;
+              run += v[j];
+            }
+          if (sub == 7) {
+            int total = 0;
+            for (int s = 0; s < 8; ++s) total += s_part[s * 128 + el];
+            m_out[r * E + e] = total;
+            if (m_global != nullptr) m_global[r * E + e] = total;
+          }
+        }
+        __syncthreads();
+      }
+    return;
+  }
   for (int r = 0; r < n_ranks; ++r) {
     for (int e0 = 0; e0 < E; e0 += 128) {
       const int e = e0 + el;
@@ -559,7 +594,8 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
 // ------------------------------------------------------------------------------------------
 // kernels
 // ------------------------------------------------------------------------------------------
-__global__ void hist_scan_kernel(const int32_t* __restrict__ tile_hist, int n_ranks, int tpr, int E,
+__global__ void __launch_bounds__(1024) hist_scan_kernel(const int32_t* __restrict__ tile_hist, int n_ranks, int tpr,
+                                                         int E,
                                  int32_t* __restrict__ hist, int32_t* __restrict__ tile_off) {
   __shared__ int s_part[8 * 128];
   dev_hist_reduce(tile_hist, n_ranks, tpr, E, hist, nullptr, tile_off, s_part);
