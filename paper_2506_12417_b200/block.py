@@ -26,6 +26,7 @@ eq_tokens, d_model, num_experts, ...)``; eq_tokens is the threshold q
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -256,6 +257,11 @@ class HarMoEnyBlock:
         self.home = torch.from_numpy(self.home_np).to(device)
         self.device = device
         self.stats = BlockStats()
+        # fused scatter (HM_FUSED_SCATTER=1): FFN1 gathers token rows itself with cp.async
+        # loader warps instead of a permuted copy.  Measured on B200 (Qwen-128, 16k tokens):
+        # +2.5% in short runs, -2% once the 1 kW power cap engages (the gather burns more
+        # power per FLOP), so the copy-permute stays the default.
+        self.fused_scatter = os.environ.get("HM_FUSED_SCATTER", "0") == "1"
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s: float | None = None, std: float = 0.02):
@@ -314,18 +320,26 @@ class HarMoEnyBlock:
                                     extras=dict(topk_idx=st["idx"], topk_w=st["w"], layout=p.layout,
                                                 lrank=st["lrank"], tile_off=p.tile_off))
 
+        fused = self.fused_scatter
+
         def permute():
-            # 128-bit row copies into the segment-contiguous buffer.  (The fused alternative -
-            # FFN1 gathering rows with TMA tile::gather4, hm_grouped_gemm a_gather - is correct
-            # but measured ~2.7x slower on B200: one gather4 moves 512 B per TMA instruction.)
+            # fused: index-only scatter (buffer positions + inverse map); the FFN1 GEMM then
+            # gathers each buffer row straight from x with cp.async loader warps, so the
+            # permuted copy of x (T*k rows, 2x512 MB of HBM traffic at Qwen-128) is never
+            # written.  Otherwise: 128-bit row copies into the segment-contiguous buffer.
             p = st["plan"]
             st["xs"], st["pos"], st["inv"] = ops.permute(st["x"], st["idx"], st["lrank"], p.tile_off, p.S,
                                                          p.layout.slot_base, G, Tg, 0, T * k, with_inverse=True,
-                                                         stream=s)
+                                                         index_only=fused, stream=s)
             self.stats.extras["pos"] = st["pos"]
 
         def gemm1():
-            st["h"] = ops.grouped_gemm(st["xs"], self.w_in, self.n_in, st["plan"].layout, self.epi_in, stream=s)
+            if fused:
+                st["h"] = ops.grouped_gemm(st["x"], self.w_in, self.n_in, st["plan"].layout, self.epi_in,
+                                           a_gather=st["inv"], a_gather_div=k, out_rows=T * k, stream=s)
+            else:
+                st["h"] = ops.grouped_gemm(st["xs"], self.w_in, self.n_in, st["plan"].layout, self.epi_in,
+                                           stream=s)
 
         def gemm2():
             # FFN2 scatters its rows token-major (row_map = inverse permutation) so the

@@ -333,13 +333,35 @@ struct PairCursor {
   }
 };
 
-template <int kEpi>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// kGather: the A tile is not TMA-loaded from a permuted buffer but gathered straight from
+// the token activations by 4 extra "A-loader" warps with 16-byte cp.async (manual 128B
+// swizzle), buffer row r reading token a_gather[r] / a_gather_div.  The copy of the
+// scatter (K4) is never written.  Loader warps fence the generic-proxy writes for the
+// tensor core (fence.proxy.async) and arrive on the leader's full barrier, which then
+// counts 1 (B expect_tx) + 8 (4 loader warps x 2 CTAs) arrivals.
+constexpr int kALoadWarps = 4;
+constexpr int kALookahead = 2;  // cp.async groups in flight per loader thread (4 measured slower)
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int kEpi, bool kGather>
+__global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kGemmThreads, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                              const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
                              const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K,
                              int ldo, const int* __restrict__ row_map, const int* __restrict__ slot_ready,
-                             int ready_from_slot, int epoch) {
+                             int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
+                             const int* __restrict__ a_gather, int a_gather_div, int a_src_rows) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * 2 * k2Half);
@@ -364,7 +386,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < k2Stages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], kGather ? 1 + 2 * kALoadWarps : 1);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -372,7 +394,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tempty[s], 2 * kEpiWarps);
     }
     fence_mbar_init();
-    tma_prefetch_desc(&tmap_a);
+    if (!kGather) tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
   }
   if (warp == 1) tmem_alloc_2cta<kTmemCols>(tmem_slot);
@@ -411,9 +433,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 4 * k2Half);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], (kGather ? 2 : 4) * k2Half);
           uint8_t* sa = smem + stage * 2 * k2Half;
-          tma_load_2d_2cta(sa, &tmap_a, full_leader + stage * 8, kb * kBK, row0, pol_a);
+          if (!kGather) tma_load_2d_2cta(sa, &tmap_a, full_leader + stage * 8, kb * kBK, row0, pol_a);
           tma_load_2d_2cta(sa + k2Half, &tmap_b, full_leader + stage * 8, kb * kBK, brow, pol_b);
           if (++stage == k2Stages) {
             stage = 0;
@@ -451,6 +473,61 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         umma_commit_2cta_multicast(&tfull[acc], 0x3);
       }
+    }
+  } else if (kGather && warp >= 2 + kEpiWarps) {
+    // ===== A-loaders (gather mode): loader warp lw fills tile rows [32lw, 32lw+32); 8 lanes
+    // copy one row's 128-byte k-block segment (16 B each), so every cp.async instruction
+    // moves 4 whole rows = 4 full cache lines =====
+    const int lw = warp - (2 + kEpiWarps);  // 0..3
+    const int c = lane & 7;                 // 16-byte chunk of the row segment
+    const int sub = lane >> 3;              // row within a group of 4
+    const uint32_t full_leader = mapa_shared(full, 0);
+    PairCursor cur{segs, mp, NB};
+    int stage = 0, sig_stage = 0, pending = 0;
+    uint32_t phase = 0;
+    for (int t = pair; t < total; t += npairs) {
+      int4 seg;
+      int m, nb;
+      cur.seek(t, seg, m, nb);
+      const int rows = max(0, min(kBM, seg.y - m * 2 * kBM - (int)rank * kBM));
+      const int rbase = seg.x + m * 2 * kBM + (int)rank * kBM;
+      const char* src[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = lw * 32 + i * 4 + sub;
+        int src_row = 0;  // rows past the segment read any valid row (results never stored)
+        if (r < rows) src_row = min(__ldg(a_gather + rbase + r) / a_gather_div, a_src_rows - 1);
+        src[i] = reinterpret_cast<const char*>(a_src + (int64_t)src_row * K) + c * 16;
+      }
+      for (int kb = 0; kb < KB; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t dst = smem_u32(smem + stage * 2 * k2Half);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = lw * 32 + i * 4 + sub;
+          cp_async16(dst + r * 128 + ((c ^ (r & 7)) << 4), src[i] + kb * 128);
+        }
+        cp_async_commit();
+        if (++pending > kALookahead) {
+          cp_async_wait<kALookahead>();
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(full_leader + sig_stage * 8);
+          if (++sig_stage == k2Stages) sig_stage = 0;
+          --pending;
+        }
+        if (++stage == k2Stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    __syncwarp();
+    for (; pending > 0; --pending) {
+      if (lane == 0) mbar_arrive_cluster(full_leader + sig_stage * 8);
+      if (++sig_stage == k2Stages) sig_stage = 0;
     }
   } else {
     // ===== epilogue: warps 2..9 of both CTAs, each CTA drains its own 128 rows =====
@@ -543,13 +620,14 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
   const int grid = num_sms();
   const int4* s4 = reinterpret_cast<const int4*>(segs);
   auto* o = reinterpret_cast<__nv_bfloat16*>(out);
-  if (a_gather == nullptr && use_2cta()) {
+  if (use_2cta()) {
     CUtensorMap tb2;  // each CTA of the pair loads 128 of the tile's 256 weight rows
     rc = make_tmap_2d_bf16(&tb2, W, (uint64_t)w_rows, (uint64_t)K, kBN / 2, kBK);
     if (rc) return rc;
+    const bool gather = a_gather != nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(grid & ~1));
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(kGemmThreads + (gather ? kALoadWarps * 32 : 0));
     cfg.dynamicSmemBytes = kGemm2Smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -560,17 +638,22 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaSuccess;
-#define HM_GEMM2(EPI)                                                                                              \
-  do {                                                                                                             \
-    cudaFuncSetAttribute(grouped_gemm_2cta_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,               \
-                         (int)kGemm2Smem);                                                                         \
-    e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI>, ta, tb2, s4, mtile_prefix, n_seg, o, N, K, ldo,    \
-                           row_map, slot_ready, ready_from_slot, epoch);                                           \
+    const auto* a_src = reinterpret_cast<const __nv_bfloat16*>(A);
+#define HM_GEMM2(EPI, G)                                                                                          \
+  do {                                                                                                            \
+    cudaFuncSetAttribute(grouped_gemm_2cta_kernel<EPI, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                         (int)kGemm2Smem);                                                                        \
+    e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, s4, mtile_prefix, n_seg, o, N, K,     \
+                           ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
+                           (int)a_rows);                                                                          \
   } while (0)
-    switch (epilogue) {
-      case kEpiStore: HM_GEMM2(kEpiStore); break;
-      case kEpiRelu: HM_GEMM2(kEpiRelu); break;
-      case kEpiSwiGLU: HM_GEMM2(kEpiSwiGLU); break;
+    switch (epilogue * 2 + (gather ? 1 : 0)) {
+      case kEpiStore * 2: HM_GEMM2(kEpiStore, false); break;
+      case kEpiStore * 2 + 1: HM_GEMM2(kEpiStore, true); break;
+      case kEpiRelu * 2: HM_GEMM2(kEpiRelu, false); break;
+      case kEpiRelu * 2 + 1: HM_GEMM2(kEpiRelu, true); break;
+      case kEpiSwiGLU * 2: HM_GEMM2(kEpiSwiGLU, false); break;
+      case kEpiSwiGLU * 2 + 1: HM_GEMM2(kEpiSwiGLU, true); break;
       default: return set_error(HM_EINVAL, "grouped_gemm: unknown epilogue");
     }
 #undef HM_GEMM2

@@ -281,6 +281,23 @@ def test_block_matches_oracle(arch, G):
         assert np.array_equal(m_all[g], orc.histogram(idx[g * (T // G):(g + 1) * (T // G)], E))
 
 
+def test_fused_scatter_block_identical():
+    """FFN1 gathering rows from x (cp.async loader warps) == copy-permute + TMA path, bitwise."""
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    cfg = MoEConfig(logical_ranks=2, eq_tokens=2, placement="blocked", d_model=256, num_experts=32, d_ff=256,
+                    top_k=4, activation="swiglu")
+    blk = _block(cfg, seed=8, dev=dev, zipf_s=1.2)
+    x = torch.randn((1024, 256), device=dev).to(torch.bfloat16)
+    blk.fused_scatter = False
+    y0 = blk(x).clone()
+    blk.fused_scatter = True
+    y1 = blk(x).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1)
+
+
 def test_block_output_independent_of_schedule():
     """Rebalancing moves work between (logical) GPUs but never changes the math:
     the block output is bit-identical with rebalancing on and off."""
