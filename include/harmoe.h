@@ -101,6 +101,14 @@ HM_API int hm_schedule(const int32_t* m_all, const int32_t* home, int G, int E, 
                 int32_t* iters, int32_t* loads, void* stream);
 
 /*
+ * Batched scheduler: B independent routing matrices m_all [B,G,E] (e.g. every layer of every
+ * batch of a recorded trace, moesim trace format workload.py:213-232) scheduled by one launch,
+ * one CTA per instance.  S [B,G,E,G], iters [B], loads [B,G] (or NULL).
+ */
+HM_API int hm_schedule_batched(const int32_t* m_all, const int32_t* home, int B, int G, int E, int q, int rebalance,
+                               int32_t* S, int32_t* iters, int32_t* loads, void* stream);
+
+/*
  * In-place rebalance of an arbitrary schedule S [G,E,G] int32 (policies.py:144-171, the
  * drop-in for moesim.rebalance / rebalance_with_stats).  Same tie and stop rules as hm_schedule.
  */

@@ -29,6 +29,8 @@ from .policies import (
     round_robin_placement,
     threshold_bound,
 )
+from .costmodel import MeasuredCostModel
+from .trace import Trace, TraceBatch, TraceParseError, read_trace, write_trace
 from .workload import skew_probabilities, zipf_probabilities, zipf_routing_matrix
 
 __version__ = "0.1.0"
@@ -53,5 +55,5 @@ __all__ = [
     "SchedulingPolicy", "blocked_placement", "estimate_token_threshold", "initial_assign", "rebalance",
     "rebalance_with_stats", "round_robin_placement", "threshold_bound", "skew_probabilities",
     "zipf_probabilities", "zipf_routing_matrix", "HarMoEnyBlock", "MoEConfig", "BlockStats", "replace_moe_layer",
-    "HarMoEnyLayer",
+    "HarMoEnyLayer", "MeasuredCostModel", "Trace", "TraceBatch", "TraceParseError", "read_trace", "write_trace",
 ]

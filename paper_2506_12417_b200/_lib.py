@@ -31,6 +31,7 @@ SIGNATURES = {
     "hm_hist_scan": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_schedule": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "hm_rebalance": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
+    "hm_schedule_batched": [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "hm_plan": [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32] + [_vp] * 12,
     "hm_dispatch_layout": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "hm_permute": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],

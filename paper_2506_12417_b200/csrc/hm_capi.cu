@@ -82,6 +82,8 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
 int launch_hist_scan(const int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
 int launch_schedule(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, cudaStream_t);
 int launch_rebalance(int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
+int launch_schedule_batched(const int32_t*, const int32_t*, int, int, int, int, int, int32_t*, int32_t*, int32_t*,
+                            cudaStream_t);
 int read_plan_phases(long long*);
 int launch_plan(const int32_t*, int, const int32_t*, const int32_t*, int, int, int, int, int, int, int32_t*, int32_t*,
                 int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
@@ -135,6 +137,11 @@ int hm_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_all_i
             int32_t* n_fetch, void* stream) {
   return launch_plan(tile_hist, tiles_per_rank, m_all_in, home, G, E, q, rebalance, mode, me, m_all_out, tile_off, S,
                      iters, loads, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch, as_stream(stream));
+}
+
+int hm_schedule_batched(const int32_t* m_all, const int32_t* home, int B, int G, int E, int q, int rebalance,
+                        int32_t* S, int32_t* iters, int32_t* loads, void* stream) {
+  return launch_schedule_batched(m_all, home, B, G, E, q, rebalance, S, iters, loads, as_stream(stream));
 }
 
 int hm_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* loads, void* stream) {

@@ -608,8 +608,14 @@ __global__ void __launch_bounds__(256)
                     int32_t* __restrict__ loads_out) {
   extern __shared__ int s_dyn[];
   __shared__ long long F[32 * 32];
-  int* S = kSmemS ? s_dyn : S_out;
   const int n = G * E * G;
+  // batched launches: CTA b schedules instance b (a layer of a trace, ...)
+  const int b = blockIdx.x;
+  if (m_all != nullptr) m_all += (int64_t)b * G * E;
+  S_out += (int64_t)b * n;
+  iters_out += b;
+  if (loads_out != nullptr) loads_out += (int64_t)b * G;
+  int* S = kSmemS ? s_dyn : S_out;
   if (kFromS && kSmemS)
     for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = S_out[i];
   dev_schedule(S, !kFromS, m_all, home, G, E, q, rebalance, iters_out, loads_out, F, kSmemS ? s_dyn + n : nullptr);
@@ -667,18 +673,25 @@ int launch_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_rank, 
   return check_launch("hist_scan");
 }
 
-int launch_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int q, int rebalance, int32_t* S,
-                    int32_t* iters, int32_t* loads, cudaStream_t stream) {
+int launch_schedule_batched(const int32_t* m_all, const int32_t* home, int B, int G, int E, int q, int rebalance,
+                            int32_t* S, int32_t* iters, int32_t* loads, cudaStream_t stream) {
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
   if (G < 1 || G > 32 || E < 1) return set_error(HM_EINVAL, "schedule: need 1 <= G <= 32 and E >= 1");
+  if (B < 0) return set_error(HM_EINVAL, "schedule: batch count must be >= 0");
+  if (B == 0) return HM_OK;
   const size_t sbytes = (size_t)2 * G * E * G * sizeof(int);  // S + transposed copy for the fast loop
   if (sbytes <= 200 * 1024) {
     cudaFuncSetAttribute(schedule_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sbytes);
-    schedule_kernel<true, false><<<1, 256, sbytes, stream>>>(m_all, home, G, E, q, rebalance, S, iters, loads);
+    schedule_kernel<true, false><<<B, 256, sbytes, stream>>>(m_all, home, G, E, q, rebalance, S, iters, loads);
   } else {
-    schedule_kernel<false, false><<<1, 256, 0, stream>>>(m_all, home, G, E, q, rebalance, S, iters, loads);
+    schedule_kernel<false, false><<<B, 256, 0, stream>>>(m_all, home, G, E, q, rebalance, S, iters, loads);
   }
   return check_launch("schedule");
+}
+
+int launch_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int q, int rebalance, int32_t* S,
+                    int32_t* iters, int32_t* loads, cudaStream_t stream) {
+  return launch_schedule_batched(m_all, home, 1, G, E, q, rebalance, S, iters, loads, stream);
 }
 
 int launch_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* loads, cudaStream_t stream) {

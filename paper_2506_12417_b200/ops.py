@@ -90,6 +90,21 @@ def schedule(m_all, home, q: int, rebalance: bool = True, stream=None):
     return S, iters, loads
 
 
+def schedule_batched(m_all, home, q: int, rebalance: bool = True, stream=None):
+    """K3 over B instances in one launch: m_all [B,G,E] i32 -> S [B,G,E,G], iters [B], loads [B,G]."""
+    _require_cuda(m_all, home)
+    if m_all.dtype != torch.int32 or home.dtype != torch.int32:
+        raise ValueError("schedule expects int32 m_all and home")
+    B, G, E = m_all.shape
+    dev = m_all.device
+    S = torch.empty((B, G, E, G), dtype=torch.int32, device=dev)
+    iters = torch.empty(B, dtype=torch.int32, device=dev)
+    loads = torch.empty((B, G), dtype=torch.int32, device=dev)
+    _lib.call("hm_schedule_batched", _ptr(m_all), _ptr(home), B, G, E, int(q), int(bool(rebalance)), _ptr(S),
+              _ptr(iters), _ptr(loads), _stream(stream))
+    return S, iters, loads
+
+
 def rebalance_(S, q: int, stream=None):
     """In-place rebalance of S [G,E,G] i32; returns (iters, loads) device tensors."""
     _require_cuda(S)

@@ -16,6 +16,10 @@ scheduler kernel are pinned to the reference, not to a restatement:
 * plan_order.npz      - plan_gpu_execution (engine.py:204-275) order/timing on
                         random work lists with the unit cost model
                         (test_engine.py:30-43)
+* trace_g4_e16.jsonl  - a trace written by the reference's write_trace
+                        (workload.py:183-232), resampled alpha, 5 batches x 3 layers
+* trace_g4_e16_schedules.npz - the reference build_schedule (engine.py:287-299)
+                        of every (batch, layer) of that trace, per placement and q
 
 The inputs are stored alongside the outputs, so the fixtures do not depend on
 numpy RNG stream stability.
@@ -163,10 +167,38 @@ def plan_order(n=400):
     )
 
 
+def trace_files():
+    """A reference-written trace (workload.py:183-232) plus the reference's schedule of every
+    (batch, layer) instance (engine.py:287-299, rebalance on, round-robin and blocked)."""
+    from moesim import ModelSpec, SchedulerConfig, SkewSpec, WorkloadSpec, generate_trace, write_trace
+    from moesim.engine import build_schedule
+    from moesim.policies import PlacementKind, SchedulingPolicy
+
+    model = ModelSpec(num_layers=3, num_experts=16, d_model=64, d_ff=128, dtype_bytes=2)
+    spec = WorkloadSpec(num_batches=5, tokens_per_gpu_per_batch=700,
+                        skew=SkewSpec(alpha=0.0, skewed_experts=(0, 5), mode="resample_uniform",
+                                      resample_lo=0.3, resample_hi=0.95), seed=7)
+    G = 4
+    trace = generate_trace(spec, model, num_gpus=G)
+    path = os.path.join(HERE, "trace_g4_e16.jsonl")
+    write_trace(trace, path)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+    out = {}
+    for pl in ("round_robin", "blocked"):
+        for q in (1, 17):
+            kind = PlacementKind.ROUND_ROBIN if pl == "round_robin" else PlacementKind.BLOCKED
+            cfg = SchedulerConfig(token_threshold_q=q, policy=SchedulingPolicy.REBALANCE, placement=kind)
+            home = (round_robin_placement if pl == "round_robin" else blocked_placement)(16, G)
+            S = [build_schedule(m, home, cfg, SimFlags()).counts for b in trace.batches for m in b.layers]
+            out[f"S_{pl}_q{q}"] = np.stack(S).astype(np.int64)
+            out[f"home_{pl}"] = np.asarray(home.home, np.int64)
+    return out
+
+
 def main():
     print("moesim", moesim.__version__, "numpy", np.__version__)
     for name, fn in [("fig4", fig4), ("acceptance_c2", acceptance_c2), ("baseline_shapes", baseline_shapes),
-                     ("plan_order", plan_order)]:
+                     ("plan_order", plan_order), ("trace_g4_e16_schedules", trace_files)]:
         d = fn()
         path = os.path.join(HERE, name + ".npz")
         np.savez_compressed(path, **d)
