@@ -194,6 +194,65 @@ HM_API int hm_ipc_close(void* dev_ptr);
 HM_API int hm_combine(const void* Y, const int32_t* pos, const float* topk_w, int T, int k, int d,
                       const void* residual, void* y, void* stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Expert parallelism over NVSwitch peer memory (ep.py transport "p2p"): every rank's receive
+ * buffer, token-index buffer, output buffer and flags are mapped into every other rank once
+ * (hm_ipc_*); the replicated schedule S then places every row without any host round trip
+ * (SURVEY.md §8(e)).  Replaces the NCCL all_to_all pair of engine.py:342-375 / PAPER.md:606-616.
+ * ---------------------------------------------------------------------------------------- */
+
+/*
+ * From S [G,E,G]: dst_delta[d] = row of this rank's assignments in d's receive buffer minus their
+ * row in the send layout of hm_dispatch_layout (HM_LAYOUT_EP), and recv_split [G+1] = first
+ * receive row of each source (flows of engine._exchange_byte_vectors, engine.py:278-284).
+ */
+HM_API int hm_ep_offsets(const int32_t* S, int G, int E, int me, int32_t* dst_delta, int32_t* recv_split,
+                         void* stream);
+
+/*
+ * Fused scatter + dispatch (Alg.1 step 4 + the all_to_all): token row t is read once and
+ * stored into dst_rows[d] (receive buffer of destination rank d, a peer pointer) at its
+ * receive row, and t*k + j into dst_tok[d] at the same row.  dst_rows / dst_tok: device arrays
+ * of G pointers.  pos [T*k] (or NULL) gets the send-layout row, as hm_permute would.
+ */
+HM_API int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+                            const int32_t* S, const int32_t* slot_base, const int32_t* dst_delta, int tokens, int me,
+                            int G, int E, int k, int d, const uint64_t* dst_rows, const uint64_t* dst_tok,
+                            int32_t* pos, void* stream);
+
+/*
+ * hm_grouped_gemm whose output rows go to other ranks (FFN2 + the return all_to_all): the rows
+ * of a segment starting at receive row r0 belong to source g with out_split[g] <= r0 <
+ * out_split[g+1], and land in out_ptrs[g] (device array of n_out peer pointers) at row
+ * row_map[r].  2-CTA kernel only.
+ */
+HM_API int hm_grouped_gemm_remote(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                                  const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix,
+                                  int epilogue, const uint64_t* out_ptrs, const int32_t* out_split, int n_out,
+                                  const int32_t* row_map, const int32_t* slot_ready, int ready_from_slot, int epoch,
+                                  void* stream);
+
+/*
+ * Device-driven K6 (engine.py:253-265): copy expert fetch[i] (i < *n_fetch, plan order, from the
+ * layout's fetch list) from src_in[e] / src_out[e] (device arrays of E pointers: the home rank's
+ * HBM through IPC, or pinned host memory) into cache slot first_slot + i of dst_in / dst_out
+ * (slot strides in_bytes / out_bytes), publishing ready_in / ready_out[slot] = value as each
+ * block lands.  counters [2*n_slots] int32 scratch (zeroed by the call); ctas <= 0: default.
+ */
+HM_API int hm_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const uint64_t* src_in,
+                            const uint64_t* src_out, size_t in_bytes, size_t out_bytes, void* dst_in, void* dst_out,
+                            int first_slot, int n_slots, int32_t* ready_in, int32_t* ready_out, int32_t* counters,
+                            int value, int ctas, void* stream);
+
+/*
+ * Stream-ordered flags: hm_stream_signal writes `value` to each of n device addresses
+ * (flags: HOST array of device pointers, typically peers' flag words) after all prior work
+ * on the stream, with a system-scope fence; hm_stream_wait blocks the stream until each of the
+ * n consecutive int32 at `flags` is >= value.  Neither occupies an SM.
+ */
+HM_API int hm_stream_signal(void* const* flags, int n, uint32_t value, void* stream);
+HM_API int hm_stream_wait(const int32_t* flags, int n, uint32_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,14 @@ SIGNATURES = {
                         _vp],
     "hm_fetch_expert": [_vp, _vp, ctypes.c_size_t, _vp, _i32, _vp],
     "hm_combine": [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp],
+    "hm_ep_offsets": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
+    "hm_dispatch_push": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
+    "hm_grouped_gemm_remote": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _i32,
+                               _i32, _vp],
+    "hm_fetch_experts": [_vp, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_size_t, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
+                         _i32, _i32, _vp],
+    "hm_stream_signal": [ctypes.POINTER(ctypes.c_void_p), _i32, ctypes.c_uint32, _vp],
+    "hm_stream_wait": [_vp, _i32, ctypes.c_uint32, _vp],
     "hm_debug_plan_phases": [_vp],
     "hm_ipc_get_handle": [_vp, _vp, ctypes.POINTER(ctypes.c_size_t)],
     "hm_ipc_open": [_vp, ctypes.POINTER(ctypes.c_void_p)],

@@ -53,10 +53,18 @@ class MoEConfig:
     logical_ranks: int = 1  # LOCAL mode: number of simulated GPUs (world_size must be 1)
     fetch_source: str = "peer"  # EP mode: "peer" (NVLink) or "host" (pinned host memory)
     residual: bool = False  # decoder-layer residual y = x + MoE(x), fused into the combine kernel
+    # EP mode: "nccl" (all_to_all_single; split sizes need S on the host once per layer) or "p2p"
+    # (one-sided pushes into peers' buffers over NVLink/NVSwitch, no host round trip)
+    transport: str = "nccl"
+    max_tokens_per_rank: int = 16384  # p2p: capacity of the peer-mapped buffers
 
     def __post_init__(self):
         if self.eq_tokens < 1:
             raise ValueError("token_threshold_q must be >= 1")
+        if self.transport not in ("nccl", "p2p"):
+            raise ValueError("transport must be 'nccl' or 'p2p'")
+        if self.max_tokens_per_rank < 1:
+            raise ValueError("max_tokens_per_rank must be >= 1")
         if self.activation not in ("swiglu", "relu"):
             raise ValueError("activation must be 'swiglu' or 'relu'")
         if self.renormalize is None:

@@ -44,6 +44,7 @@ int num_sms() {
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
 static PFN_cuMemGetAddressRange_v3020 g_addr_range = nullptr;
+static PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
 static std::once_flag g_driver_once;
 
 static void load_driver_entry_points() {
@@ -60,6 +61,10 @@ static void load_driver_entry_points() {
   if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
       q == cudaDriverEntryPointSuccess)
     g_addr_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(fn);
 }
 
 int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
@@ -92,6 +97,12 @@ int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, 
 int launch_permute(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int,
                    int, int, int, int, int, int, void*, int32_t*, int32_t*, cudaStream_t);
 int launch_combine(const void*, const int32_t*, const float*, int, int, int, const void*, void*, cudaStream_t);
+int launch_ep_offsets(const int32_t*, int, int, int, int32_t*, int32_t*, cudaStream_t);
+int launch_dispatch_push(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
+                         const int32_t*, int, int, int, int, int, int, const unsigned long long*,
+                         const unsigned long long*, int32_t*, cudaStream_t);
+int launch_fetch_experts(const int32_t*, const int32_t*, const unsigned long long*, const unsigned long long*, size_t,
+                         size_t, void*, void*, int, int, int32_t*, int32_t*, int32_t*, int, int, cudaStream_t);
 
 __global__ void publish_flag_kernel(int32_t* flag, int epoch) {
   __threadfence_system();
@@ -168,6 +179,68 @@ int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows
                     int ready_from_slot, int epoch, void* stream) {
   return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, row_map, a_gather,
                              a_gather_div, slot_ready, ready_from_slot, epoch, as_stream(stream));
+}
+
+int hm_grouped_gemm_remote(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                           const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
+                           const uint64_t* out_ptrs, const int32_t* out_split, int n_out, const int32_t* row_map,
+                           const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream) {
+  if (out_ptrs == nullptr) return set_error(HM_EINVAL, "grouped_gemm_remote: out_ptrs is required");
+  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, nullptr, row_map,
+                             nullptr, 1, slot_ready, ready_from_slot, epoch, as_stream(stream),
+                             reinterpret_cast<const unsigned long long*>(out_ptrs), out_split, n_out);
+}
+
+int hm_ep_offsets(const int32_t* S, int G, int E, int me, int32_t* dst_delta, int32_t* recv_split, void* stream) {
+  return launch_ep_offsets(S, G, E, me, dst_delta, recv_split, as_stream(stream));
+}
+
+int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+                     const int32_t* S, const int32_t* slot_base, const int32_t* dst_delta, int tokens, int me, int G,
+                     int E, int k, int d, const uint64_t* dst_rows, const uint64_t* dst_tok, int32_t* pos,
+                     void* stream) {
+  return launch_dispatch_push(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, tokens, me, G, E, k, d,
+                              reinterpret_cast<const unsigned long long*>(dst_rows),
+                              reinterpret_cast<const unsigned long long*>(dst_tok), pos, as_stream(stream));
+}
+
+int hm_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const uint64_t* src_in, const uint64_t* src_out,
+                     size_t in_bytes, size_t out_bytes, void* dst_in, void* dst_out, int first_slot, int n_slots,
+                     int32_t* ready_in, int32_t* ready_out, int32_t* counters, int value, int ctas, void* stream) {
+  return launch_fetch_experts(fetch, n_fetch, reinterpret_cast<const unsigned long long*>(src_in),
+                              reinterpret_cast<const unsigned long long*>(src_out), in_bytes, out_bytes, dst_in,
+                              dst_out, first_slot, n_slots, ready_in, ready_out, counters, value, ctas,
+                              as_stream(stream));
+}
+
+int hm_stream_signal(void* const* flags, int n, uint32_t value, void* stream) {
+  std::call_once(g_driver_once, load_driver_entry_points);
+  if (n < 0 || (n > 0 && flags == nullptr)) return set_error(HM_EINVAL, "stream_signal: bad flag list");
+  cudaStream_t s = as_stream(stream);
+  for (int i = 0; i < n; ++i) {
+    if (g_write32 != nullptr) {
+      const CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flags[i]),
+                                   (cuuint32_t)value, CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (r != CUDA_SUCCESS) return set_error(HM_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+    } else {
+      publish_flag_kernel<<<1, 1, 0, s>>>(reinterpret_cast<int32_t*>(flags[i]), (int)value);
+      const int rc = check_launch("stream_signal");
+      if (rc) return rc;
+    }
+  }
+  return HM_OK;
+}
+
+int hm_stream_wait(const int32_t* flags, int n, uint32_t value, void* stream) {
+  std::call_once(g_driver_once, load_driver_entry_points);
+  if (g_wait32 == nullptr) return set_error(HM_ECUDA, "cuStreamWaitValue32 unavailable");
+  cudaStream_t s = as_stream(stream);
+  for (int i = 0; i < n; ++i) {
+    const CUresult r = g_wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flags + i),
+                                (cuuint32_t)value, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return set_error(HM_ECUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+  }
+  return HM_OK;
 }
 
 int hm_fetch_expert(void* dst, const void* src, size_t bytes, int32_t* ready_flag, int epoch, void* stream) {

@@ -179,7 +179,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if (lane == 0 && slot_ready != nullptr && seg.z >= ready_from_slot) {
         // K6: fetched expert weights land asynchronously; wait for this slot's epoch
-        while (ld_acquire_gpu(slot_ready + seg.z) < epoch) __nanosleep(64);
+        long long spins = 0;  // watchdog, as in the 2-CTA kernel
+        while (ld_acquire_gpu(slot_ready + seg.z) < epoch) {
+          __nanosleep(128);
+          if (++spins > (1ll << 26)) __trap();
+        }
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       for (int kb = 0; kb < KB; ++kb) {
@@ -361,7 +365,9 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
                              const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K,
                              int ldo, const int* __restrict__ row_map, const int* __restrict__ slot_ready,
                              int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
-                             const int* __restrict__ a_gather, int a_gather_div, int a_src_rows) {
+                             const int* __restrict__ a_gather, int a_gather_div, int a_src_rows,
+                             const unsigned long long* __restrict__ out_ptrs, const int* __restrict__ out_split,
+                             int n_out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * 2 * k2Half);
@@ -428,7 +434,13 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         const int row0 = seg.x + m * 2 * kBM + (int)rank * kBM;
         const int brow = seg.z * N + nb * kBN + (int)rank * (kBN / 2);
         if (slot_ready != nullptr && seg.z >= ready_from_slot) {
-          while (ld_acquire_gpu(slot_ready + seg.z) < epoch) __nanosleep(64);
+          // watchdog: a fetch that never lands is a bug upstream; fail the launch instead of
+          // hanging the device (~10 s)
+          long long spins = 0;
+          while (ld_acquire_gpu(slot_ready + seg.z) < epoch) {
+            __nanosleep(128);
+            if (++spins > (1ll << 26)) __trap();
+          }
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         for (int kb = 0; kb < KB; ++kb) {
@@ -552,6 +564,15 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       if (row_map != nullptr && valid) row = __ldg(row_map + row);
       const int64_t obase = row * ldo + (int64_t)nb * kOutCols + half * kHalfCols;
       const int nvalid = max(0, min(32, rows - q * 32));
+      // remote output (EP over peer memory): the segment's rows belong to source rank g, the
+      // one whose receive range [out_split[g], out_split[g+1]) holds the segment; its rows are
+      // stored straight into that rank's token-major output over NVLink
+      __nv_bfloat16* obuf = out;
+      if (out_ptrs != nullptr) {
+        int g = 0;
+        while (g + 1 < n_out && __ldg(out_split + g + 1) <= seg.x) ++g;
+        obuf = reinterpret_cast<__nv_bfloat16*>(__ldg(out_ptrs + g));
+      }
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
           const int64_t ob = __shfl_sync(0xffffffffu, obase, rr);
           if (rr < nvalid) {
             const uint4 v = ld_shared_v4(stg + rr * kStgPitch + piece * 16);
-            st_global_v4(out + ob + c0 + piece * 8, v.x, v.y, v.z, v.w);
+            st_global_v4(obuf + ob + c0 + piece * 8, v.x, v.y, v.z, v.w);
           }
         }
         __syncwarp();
@@ -604,11 +625,16 @@ static bool use_2cta() {
 int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                         const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
-                        const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream) {
+                        const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
+                        const unsigned long long* out_ptrs, const int32_t* out_split, int n_out) {
   if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
     return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
   if (a_gather != nullptr && a_gather_div < 1) return set_error(HM_EINVAL, "grouped_gemm: a_gather_div must be >= 1");
+  if (out_ptrs != nullptr && (out_split == nullptr || n_out < 1))
+    return set_error(HM_EINVAL, "grouped_gemm: remote output needs out_split and n_out >= 1");
+  if (out_ptrs != nullptr && !use_2cta())
+    return set_error(HM_EINVAL, "grouped_gemm: remote output needs the 2-CTA kernel (unset HM_GEMM_1CTA)");
   if (a_rows <= 0) return HM_OK;
   CUtensorMap ta, tb;
   // gathered A: 1-row boxes fetched four at a time by tile::gather4
@@ -645,7 +671,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
                          (int)kGemm2Smem);                                                                        \
     e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, s4, mtile_prefix, n_seg, o, N, K,     \
                            ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
-                           (int)a_rows);                                                                          \
+                           (int)a_rows, out_ptrs, out_split, n_out);                                              \
   } while (0)
     switch (epilogue * 2 + (gather ? 1 : 0)) {
       case kEpiStore * 2: HM_GEMM2(kEpiStore, false); break;

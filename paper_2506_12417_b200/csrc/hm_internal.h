@@ -23,7 +23,9 @@ int make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_
 int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                         const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
-                        const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream);
+                        const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
+                        const unsigned long long* out_ptrs = nullptr, const int32_t* out_split = nullptr,
+                        int n_out = 0);
 
 int launch_router(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
                   int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,

@@ -1,0 +1,213 @@
+// Expert parallelism over NVSwitch peer memory: one-sided, no host synchronisation.
+//
+// The NCCL path (ep.py, transport "nccl") needs S on the host for the all_to_all split
+// sizes.  With every rank's buffers mapped into every other rank (CUDA IPC, once at set-up)
+// the replicated schedule S is all a sender needs to place its rows directly in the
+// receiver's buffer ("a one-sided push using the replicated S needs no
+// host-side count exchange"):
+//
+//   ep_offsets_kernel    flows = S.sum(e); per destination d the delta between this rank's
+//                        send-layout row and the row of the same assignment in d's receive
+//                        buffer ([source][expert][rank], hm_sched.cu dev_layout EP mode), and
+//                        the receive-row split per source.
+//   dispatch_push_kernel K4 fused with the dispatch all-to-all: each token row is read once
+//                        and stored (128-bit, NVLink) into every scheduled destination's
+//                        receive buffer, with its token-major index (t*k + j) beside it.
+//   fetch_kernel         K6 driven from the device: copies the plan's fetch list (peer HBM
+//                        over NVLink, or pinned host memory) into the cache slots in plan
+//                        order and publishes a ready flag per slot (the FFN GEMM producer
+//                        waits per slot), so the fetch list never visits the host.
+//
+// The FFN2 GEMM stores its rows straight into the source rank's token-major output
+// (hm_gemm.cu remote epilogue), which is the combine all-to-all fused into the GEMM.
+#include "hm_common.cuh"
+#include "hm_internal.h"
+
+namespace hm {
+
+// ------------------------------------------------------------------------------------------
+// offsets: dst_delta[d] = (sum_{g<me} flows[g][d]) - (sum_{d'<d} flows[me][d'])
+//          recv_split[g] = sum_{g'<g} flows[g'][me]   (g = 0..G)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+    ep_offsets_kernel(const int32_t* __restrict__ S, int G, int E, int me, int32_t* __restrict__ dst_delta,
+                      int32_t* __restrict__ recv_split) {
+  __shared__ int flows[32 * 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // one warp per (g, d) pair: flows[g][d] = sum_e S[g,e,d]
+  for (int p = w; p < G * G; p += nw) {
+    const int g = p / G, d = p - (p / G) * G;
+    int s = 0;
+    for (int e = lane; e < E; e += 32) s += __ldg(S + ((int64_t)g * E + e) * G + d);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) flows[p] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < G) {
+    const int d = threadIdx.x;
+    int recv_off = 0, send_off = 0;
+    for (int g = 0; g < me; ++g) recv_off += flows[g * G + d];
+    for (int d2 = 0; d2 < d; ++d2) send_off += flows[me * G + d2];
+    dst_delta[d] = recv_off - send_off;
+  }
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int g = 0; g < G; ++g) {
+      recv_split[g] = run;
+      run += flows[g * G + me];
+    }
+    recv_split[G] = run;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// dispatch push: permute_kernel's row placement (hm_permute.cu) with the store going to the
+// destination rank's receive buffer instead of a local send buffer
+// ------------------------------------------------------------------------------------------
+constexpr int kPushWarps = 8;
+
+template <int VEC>
+__global__ void __launch_bounds__(kPushWarps * 32)
+    dispatch_push_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ topk_idx,
+                         const int32_t* __restrict__ lrank, const int32_t* __restrict__ tile_off,
+                         const int32_t* __restrict__ S, const int32_t* __restrict__ slot_base,
+                         const int32_t* __restrict__ dst_delta, int64_t T, int me, int G, int E, int k, int n16,
+                         const unsigned long long* __restrict__ dst_rows, const unsigned long long* __restrict__ dst_tok,
+                         int32_t* __restrict__ pos) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kPushWarps + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const int tile = (int)(t / 128);
+  uint4 v[VEC];
+  const uint4* src = x + t * n16;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const int c = i * 32 + lane;
+    if (c < n16) v[i] = ld_global_nc_v4(src + c);
+  }
+  for (int j = 0; j < k; ++j) {
+    const int e = __ldg(topk_idx + t * k + j);
+    const int r = __ldg(tile_off + (int64_t)tile * E + e) + __ldg(lrank + t * k + j);
+    const int32_t* srow = S + ((int64_t)me * E + e) * G;
+    int c = 0, d = 0;
+    for (; d < G - 1; ++d) {
+      const int s = __ldg(srow + d);
+      if (c + s > r) break;
+      c += s;
+    }
+    const int64_t p = (int64_t)__ldg(slot_base + ((int64_t)me * E + e) * G + d) + (r - c);  // send layout
+    const int64_t q = p + __ldg(dst_delta + d);                                                // d's receive row
+    uint4* dst = reinterpret_cast<uint4*>(__ldg(dst_rows + d)) + q * n16;
+    if (lane == 0) {
+      if (pos != nullptr) pos[t * k + j] = (int32_t)p;
+      reinterpret_cast<int32_t*>(__ldg(dst_tok + d))[q] = (int32_t)(t * k + j);
+    }
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const int cc = i * 32 + lane;
+      if (cc < n16) dst[cc] = v[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// device-driven expert fetch (K6).  All CTAs copy fetch i's gate/up block, then its down
+// block, then move on (one logical channel in plan order, engine.py:253-265); the last CTA
+// to finish a block publishes its slot's ready flag with release semantics.
+// ------------------------------------------------------------------------------------------
+constexpr int kFetchThreads = 512;
+constexpr int kFetchUnroll = 4;
+
+__device__ __forceinline__ void copy_block(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + (kFetchUnroll - 1) * stride < n16; i += kFetchUnroll * stride) {
+    uint4 v[kFetchUnroll];
+#pragma unroll
+    for (int u = 0; u < kFetchUnroll; ++u) v[u] = ld_global_nc_v4(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kFetchUnroll; ++u) dst[i + u * stride] = v[u];
+  }
+  for (; i < n16; i += stride) dst[i] = ld_global_nc_v4(src + i);
+}
+
+__device__ __forceinline__ void block_done(int32_t* counter, int32_t* flag, int value) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int old = atomicAdd(counter, 1);
+    if (old == (int)gridDim.x - 1) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFetchThreads)
+    fetch_kernel(const int32_t* __restrict__ fetch, const int32_t* __restrict__ n_fetch_p,
+                 const unsigned long long* __restrict__ src_in, const unsigned long long* __restrict__ src_out,
+                 int64_t in16, int64_t out16, uint4* __restrict__ dst_in, uint4* __restrict__ dst_out, int first_slot,
+                 int n_slots, int32_t* __restrict__ ready_in, int32_t* __restrict__ ready_out,
+                 int32_t* __restrict__ counters, int value) {
+  const int n_fetch = min(*n_fetch_p, n_slots);
+  for (int i = 0; i < n_fetch; ++i) {
+    const int e = __ldg(fetch + i);
+    const int slot = first_slot + i;
+    copy_block(dst_in + (int64_t)slot * in16, reinterpret_cast<const uint4*>(__ldg(src_in + e)), in16);
+    block_done(counters + 2 * i, ready_in + slot, value);
+    copy_block(dst_out + (int64_t)slot * out16, reinterpret_cast<const uint4*>(__ldg(src_out + e)), out16);
+    block_done(counters + 2 * i + 1, ready_out + slot, value);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------------------------
+int launch_ep_offsets(const int32_t* S, int G, int E, int me, int32_t* dst_delta, int32_t* recv_split,
+                      cudaStream_t stream) {
+  if (G < 1 || G > 32 || E < 1 || me < 0 || me >= G) return set_error(HM_EINVAL, "ep_offsets: bad G/E/me");
+  ep_offsets_kernel<<<1, 1024, 0, stream>>>(S, G, E, me, dst_delta, recv_split);
+  return check_launch("ep_offsets");
+}
+
+int launch_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+                         const int32_t* S, const int32_t* slot_base, const int32_t* dst_delta, int tokens, int me,
+                         int G, int E, int k, int d, const unsigned long long* dst_rows,
+                         const unsigned long long* dst_tok, int32_t* pos, cudaStream_t stream) {
+  if (d % 8 != 0) return set_error(HM_EINVAL, "dispatch_push: d must be a multiple of 8");
+  if (G < 1 || G > 32 || me < 0 || me >= G || k < 1) return set_error(HM_EINVAL, "dispatch_push: bad G/me/k");
+  if (tokens <= 0) return HM_OK;
+  const int n16 = d / 8;
+  const int blocks = (tokens + kPushWarps - 1) / kPushWarps;
+  const auto* xs = reinterpret_cast<const uint4*>(x);
+#define HM_PUSH(V)                                                                                             \
+  dispatch_push_kernel<V><<<blocks, kPushWarps * 32, 0, stream>>>(xs, topk_idx, lrank, tile_off, S, slot_base, \
+                                                                  dst_delta, tokens, me, G, E, k, n16,          \
+                                                                  dst_rows, dst_tok, pos)
+  if (n16 <= 32) HM_PUSH(1);
+  else if (n16 <= 64) HM_PUSH(2);
+  else if (n16 <= 128) HM_PUSH(4);
+  else if (n16 <= 256) HM_PUSH(8);
+  else if (n16 <= 512) HM_PUSH(16);
+  else return set_error(HM_EINVAL, "dispatch_push: d > 4096 unsupported");
+#undef HM_PUSH
+  return check_launch("dispatch_push");
+}
+
+int launch_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const unsigned long long* src_in,
+                         const unsigned long long* src_out, size_t in_bytes, size_t out_bytes, void* dst_in,
+                         void* dst_out, int first_slot, int n_slots, int32_t* ready_in, int32_t* ready_out,
+                         int32_t* counters, int value, int ctas, cudaStream_t stream) {
+  if (in_bytes % 16 != 0 || out_bytes % 16 != 0) return set_error(HM_EINVAL, "fetch_experts: sizes must be 16-byte multiples");
+  if (n_slots <= 0) return HM_OK;
+  cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int32_t) * 2 * n_slots, stream);
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "fetch_experts memset: %s", cudaGetErrorString(e));
+  fetch_kernel<<<ctas > 0 ? ctas : 32, kFetchThreads, 0, stream>>>(
+      fetch, n_fetch, src_in, src_out, (int64_t)(in_bytes / 16), (int64_t)(out_bytes / 16),
+      reinterpret_cast<uint4*>(dst_in), reinterpret_cast<uint4*>(dst_out), first_slot, n_slots, ready_in, ready_out,
+      counters, value);
+  return check_launch("fetch_experts");
+}
+
+}  // namespace hm

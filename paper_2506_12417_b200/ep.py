@@ -152,6 +152,8 @@ class EPHarMoEnyBlock:
         self.S_host = torch.empty((self.G, E, self.G), dtype=torch.int32, pin_memory=True)
         self.fetch_host = torch.empty(E + 1, dtype=torch.int32, pin_memory=True)
         self.stats = BlockStats()
+        if cfg.transport == "p2p":
+            self._setup_p2p()
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s=None, std: float = 0.02, group=None):
@@ -186,6 +188,143 @@ class EPHarMoEnyBlock:
                 ptrs.append(p.value + off)  # the handle maps the allocation base
             self.peer_in.append(ptrs[0])
             self.peer_out.append(ptrs[1])
+
+    # ---------------------------------------------------------------------------------------
+    # transport "p2p": one-sided pushes into peer-mapped buffers (NVLink / NVSwitch)
+    # ---------------------------------------------------------------------------------------
+    def _ipc_export_open(self, t: torch.Tensor):
+        """Exchange one IPC handle per rank for tensor `t`; returns every rank's device address."""
+        L = _lib.load()
+        buf = ctypes.create_string_buffer(64)
+        off = ctypes.c_size_t(0)
+        _lib.check(L.hm_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)), "hm_ipc_get_handle")
+        allh = [None] * self.G
+        dist.all_gather_object(allh, (bytes(buf.raw), int(off.value)), group=self.group)
+        addrs = []
+        for g in range(self.G):
+            if g == self.me:
+                addrs.append(t.data_ptr())
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(L.hm_ipc_open(allh[g][0], ctypes.byref(p)), "hm_ipc_open")
+            self._ipc_bases.append(p.value)
+            addrs.append(p.value + allh[g][1])
+        return addrs
+
+    def _setup_p2p(self):
+        """Allocate this rank's peer-visible arena (flags, m_all rows, receive buffer + token
+        indices, token-major output) and map every rank's arena (one IPC handle each)."""
+        cfg, G, E, d = self.cfg, self.G, self.cfg.num_experts, self.cfg.d_model
+        k, Tmax = cfg.top_k, cfg.max_tokens_per_rank
+        if not hasattr(self, "_ipc_bases"):
+            self._ipc_bases = []
+        self.cap_send = Tmax * k
+        self.cap_recv = G * Tmax * k
+
+        def al(n):
+            return (n + 255) // 256 * 256
+
+        lay = {}
+        off = 0
+        for name, nbytes in (("flags", 3 * G * 4), ("m_all", G * E * 4), ("recv_tok", self.cap_recv * 4),
+                             ("x_recv", self.cap_recv * d * 2), ("y_ret", self.cap_send * d * 2)):
+            lay[name] = off
+            off += al(nbytes)
+        self.arena = torch.zeros(off, dtype=torch.uint8, device=self.device)
+        a = self.arena
+        self.flags = a[lay["flags"]: lay["flags"] + 3 * G * 4].view(torch.int32).view(3, G)
+        self.m_all_buf = a[lay["m_all"]: lay["m_all"] + G * E * 4].view(torch.int32).view(G, E)
+        self.recv_tok = a[lay["recv_tok"]: lay["recv_tok"] + self.cap_recv * 4].view(torch.int32)
+        self.x_recv = a[lay["x_recv"]: lay["x_recv"] + self.cap_recv * d * 2].view(torch.bfloat16).view(-1, d)
+        self.y_ret = a[lay["y_ret"]: lay["y_ret"] + self.cap_send * d * 2].view(torch.bfloat16).view(-1, d)
+        self.h_buf = torch.empty((self.cap_recv, cfg.d_ff), dtype=torch.bfloat16, device=self.device)
+        torch.cuda.synchronize(self.device)
+        bases = self._ipc_export_open(self.arena)
+        i64 = dict(dtype=torch.int64, device=self.device)
+        self.p2p_rows = torch.tensor([b + lay["x_recv"] for b in bases], **i64)
+        self.p2p_tok = torch.tensor([b + lay["recv_tok"] for b in bases], **i64)
+        self.p2p_out = torch.tensor([b + lay["y_ret"] for b in bases], **i64)
+        me = self.me
+        self.meta_addrs = [b + lay["flags"] + (0 * G + me) * 4 for b in bases]
+        self.tok_addrs = [b + lay["flags"] + (1 * G + me) * 4 for b in bases]
+        self.y_addrs = [b + lay["flags"] + (2 * G + me) * 4 for b in bases]
+        self.mall_row_addrs = [b + lay["m_all"] + me * E * 4 for b in bases]
+        base0 = self.arena.data_ptr() + lay["flags"]
+        self.local_flag_addrs = [[base0 + (c * G + g) * 4 for g in range(G)] for c in range(3)]
+        # device fetch sources: expert e at its home rank (NVLink) or in pinned host memory
+        in_bytes, out_bytes = self.n_in * d * 2, d * cfg.d_ff * 2
+        src_in, src_out = [], []
+        for e in range(E):
+            h, hs = int(self.home_np[e]), self._hslot[e]
+            if self.fetch_source == "host":
+                src_in.append(self.w_in_host[e].data_ptr())
+                src_out.append(self.w_out_host[e].data_ptr())
+            else:
+                src_in.append(self.peer_in[h] + hs * in_bytes)
+                src_out.append(self.peer_out[h] + hs * out_bytes)
+        self.fetch_src_in = torch.tensor(src_in, **i64)
+        self.fetch_src_out = torch.tensor(src_out, **i64)
+        self.fetch_counters = torch.zeros(2 * max(self.n_cache, 1), dtype=torch.int32, device=self.device)
+        self.dst_delta = torch.empty(G, dtype=torch.int32, device=self.device)
+        self.recv_split = torch.empty(G + 1, dtype=torch.int32, device=self.device)
+        dist.barrier(group=self.group)  # every arena zeroed and mapped before anyone signals
+
+    def _forward_p2p(self, x, s, mark):
+        cfg, G, E, me = self.cfg, self.G, self.cfg.num_experts, self.me
+        Tg, k, d = x.shape[0], cfg.top_k, cfg.d_model
+        if Tg > cfg.max_tokens_per_rank:
+            raise ValueError(f"{Tg} tokens exceed max_tokens_per_rank={cfg.max_tokens_per_rank}")
+        L = _lib.load()
+        idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, 1, Tg, k, cfg.renormalize, E=E, stream=s)
+        tiles = (Tg + ops.TILE_M - 1) // ops.TILE_M
+        hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)
+        mark("router")
+        # step 2: my histogram row into every rank's m_all (peer stores), then flags
+        for addr in self.mall_row_addrs:
+            _lib.check(L.hm_fetch_expert(addr, hist.data_ptr(), E * 4, None, 0, s.cuda_stream), "m_all push")
+        ops.stream_signal(self.meta_addrs, 1, s)
+        ops.stream_wait(self.flags[0], 1, s)
+        ops.stream_signal(self.local_flag_addrs[0], 0, s)
+        p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
+                     stream=s)
+        S, lay = p.S, p.layout
+        m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
+        ops.ep_offsets(S, me, self.dst_delta, self.recv_split, stream=s)
+        mark("schedule")
+        # K6 from the device-side fetch list, on the fetch stream, overlapping the dispatch + FFN
+        if self.n_cache > 0:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            fs = self.fetch_stream
+            fs.wait_event(ev)
+            ops.fetch_experts(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.n_in * d * 2,
+                              d * cfg.d_ff * 2, self.w_in, self.w_out, self.n_home, self.n_cache, self.ready_in,
+                              self.ready_out, self.fetch_counters, value=1, stream=fs)
+        pos = torch.empty((Tg, k), dtype=torch.int32, device=self.device)
+        ops.dispatch_push(x, idx, lrank, tile_off, S, lay.slot_base, self.dst_delta, me, self.p2p_rows, self.p2p_tok,
+                          pos=pos, stream=s)
+        ops.stream_signal(self.tok_addrs, 1, s)
+        ops.stream_wait(self.flags[1], 1, s)
+        ops.stream_signal(self.local_flag_addrs[1], 0, s)
+        mark("dispatch_push")
+        ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
+                         slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s)
+        mark("gemm1")
+        ops.grouped_gemm_remote(self.h_buf, self.w_out.view(-1, cfg.d_ff), d, lay, ops.HM_EPI_STORE, self.p2p_out,
+                                self.recv_split, self.recv_tok, slot_ready=self.ready_out,
+                                ready_from_slot=self.n_home, epoch=1, stream=s)
+        if self.n_cache > 0:
+            self.ready_in[self.n_home:].zero_()
+            self.ready_out[self.n_home:].zero_()
+        ops.stream_signal(self.y_addrs, 1, s)
+        ops.stream_wait(self.flags[2], 1, s)
+        ops.stream_signal(self.local_flag_addrs[2], 0, s)
+        mark("gemm2_push")
+        y = ops.combine(self.y_ret[: Tg * k], None, w, residual=x if cfg.residual else None, stream=s)
+        mark("combine")
+        self.stats = BlockStats(m_all=m_all, schedule=S, iters=p.iters, loads=p.loads,
+                                extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay))
+        return y
 
     def _fetch(self, experts):
         """K6: one transfer channel (the fetch stream), plan order, overwrite semantics:
@@ -234,6 +373,8 @@ class EPHarMoEnyBlock:
         with torch.cuda.stream(s):
             mark("start")
             x = x.contiguous()
+            if cfg.transport == "p2p":
+                return self._forward_p2p(x, s, mark)
             idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, 1, Tg, k, cfg.renormalize, E=E,
                                                        stream=s)
             hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)

@@ -236,3 +236,64 @@ def combine(Y, pos, topk_w, out=None, residual=None, stream=None):
         out = torch.empty((T, d), dtype=torch.bfloat16, device=Y.device)
     _lib.call("hm_combine", _ptr(Y), _ptr(pos), _ptr(topk_w), T, k, d, _ptr(residual), _ptr(out), _stream(stream))
     return out
+
+
+# ------------------------------------------------------------------------------------------
+# expert parallelism over peer memory (ep.py transport "p2p")
+# ------------------------------------------------------------------------------------------
+def ep_offsets(S, me: int, dst_delta=None, recv_split=None, stream=None):
+    """dst_delta [G] (send-layout row -> receive row of destination d), recv_split [G+1]."""
+    _require_cuda(S)
+    G, E, _ = S.shape
+    if dst_delta is None:
+        dst_delta = torch.empty(G, dtype=torch.int32, device=S.device)
+    if recv_split is None:
+        recv_split = torch.empty(G + 1, dtype=torch.int32, device=S.device)
+    _lib.call("hm_ep_offsets", _ptr(S), G, E, int(me), _ptr(dst_delta), _ptr(recv_split), _stream(stream))
+    return dst_delta, recv_split
+
+
+def dispatch_push(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, me: int, dst_rows, dst_tok, pos=None,
+                  stream=None):
+    """Fused scatter + dispatch: rows land in the destination ranks' receive buffers.
+    dst_rows / dst_tok: uint64 (int64) device tensors of G peer pointers."""
+    _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, dst_rows, dst_tok, pos)
+    T, d = x.shape
+    k = topk_idx.shape[1]
+    G, E, _ = S.shape
+    _lib.call("hm_dispatch_push", _ptr(x), _ptr(topk_idx), _ptr(lrank), _ptr(tile_off), _ptr(S), _ptr(slot_base),
+              _ptr(dst_delta), T, int(me), G, E, k, d, _ptr(dst_rows), _ptr(dst_tok), _ptr(pos), _stream(stream))
+
+
+def grouped_gemm_remote(A, W, N: int, layout: "Layout", epilogue: int, out_ptrs, out_split, row_map, slot_ready=None,
+                        ready_from_slot: int = 0, epoch: int = 0, a_rows: int | None = None, stream=None):
+    """K5 with the rows of each segment stored into the owning source rank's buffer (peer pointer)."""
+    _require_cuda(A, W, out_ptrs, out_split, row_map, slot_ready)
+    rows = A.shape[0] if a_rows is None else int(a_rows)
+    K = A.shape[1]
+    _lib.call("hm_grouped_gemm_remote", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(layout.segs),
+              _ptr(layout.n_seg), _ptr(layout.mtile_prefix), int(epilogue), _ptr(out_ptrs), _ptr(out_split),
+              out_ptrs.numel(), _ptr(row_map), _ptr(slot_ready), int(ready_from_slot), int(epoch), _stream(stream))
+
+
+def fetch_experts(fetch, n_fetch, src_in, src_out, in_bytes: int, out_bytes: int, dst_in, dst_out, first_slot: int,
+                  n_slots: int, ready_in, ready_out, counters, value: int = 1, ctas: int = 0, stream=None):
+    """Device-driven K6 over the layout's fetch list (no host round trip)."""
+    _require_cuda(fetch, n_fetch, src_in, src_out, dst_in, dst_out, ready_in, ready_out, counters)
+    _lib.call("hm_fetch_experts", _ptr(fetch), _ptr(n_fetch), _ptr(src_in), _ptr(src_out), int(in_bytes),
+              int(out_bytes), _ptr(dst_in), _ptr(dst_out), int(first_slot), int(n_slots), _ptr(ready_in),
+              _ptr(ready_out), _ptr(counters), int(value), int(ctas), _stream(stream))
+
+
+def stream_signal(addresses, value: int, stream=None):
+    """Write `value` to each device address (ints: peer flag words) after prior stream work."""
+    import ctypes
+
+    arr = (ctypes.c_void_p * len(addresses))(*[int(a) for a in addresses])
+    _lib.call("hm_stream_signal", arr, len(addresses), int(value) & 0xFFFFFFFF, _stream(stream))
+
+
+def stream_wait(flags, value: int, stream=None):
+    """Block the stream until every int32 of `flags` (device tensor) is >= value."""
+    _require_cuda(flags)
+    _lib.call("hm_stream_wait", _ptr(flags), flags.numel(), int(value) & 0xFFFFFFFF, _stream(stream))

@@ -31,7 +31,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, fetch_source, out_q):
+def _worker(rank, world, port, fetch_source, transport, out_q):
     import sys
 
     sys.path.insert(0, REPO)
@@ -42,50 +42,62 @@ def _worker(rank, world, port, fetch_source, out_q):
         from paper_2506_12417_b200.block import MoEConfig
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
-        cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, **KW)
+        cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, transport=transport,
+                        max_tokens_per_rank=T // world, **KW)
         blk = EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
         g = torch.Generator(device="cuda").manual_seed(99)
         x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
         Tg = T // world
         xl = x[rank * Tg:(rank + 1) * Tg].contiguous()
         outs = []
-        for _ in range(2):  # second forward re-uses the fetch slots (epoch flags)
+        for _ in range(3):  # later forwards re-use the fetch slots and the peer flags
             outs.append(blk(xl).cpu())
         torch.cuda.synchronize()
-        out_q.put((rank, outs[0].view(torch.int16).numpy(), outs[1].view(torch.int16).numpy(),
-                   blk.stats.schedule.cpu().numpy(), int(blk.stats.extras["n_fetch"])))
+        out_q.put((rank, outs[0].view(torch.int16).numpy(), outs[2].view(torch.int16).numpy(),
+                   blk.stats.schedule.cpu().numpy(), int(blk.stats.extras["layout"].n_fetch.item())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fetch_source", ["peer", "host"])
-def test_ep_two_ranks_one_gpu_bit_identical(fetch_source):
+@pytest.mark.parametrize("fetch_source,transport,world", [("peer", "nccl", 2), ("host", "nccl", 2),
+                                                           ("peer", "p2p", 2), ("host", "p2p", 2),
+                                                           ("peer", "p2p", 4)])
+def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
+    """transport "nccl": exchanges through the process group (gloo here, host-staged);
+    transport "p2p": one-sided pushes into the other ranks' IPC-mapped buffers + stream flags,
+    no collective and no host round trip inside the forward."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
 
-    world = 2
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, fetch_source, out_q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fetch_source, transport, out_q))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
-    for _ in range(world):
-        r, y0, y1, S, n_fetch = out_q.get(timeout=120)
-        res[r] = (y0, y1, S, n_fetch)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    try:
+        for _ in range(world):
+            r, y0, y1, S, n_fetch = out_q.get(timeout=120)
+            res[r] = (y0, y1, S, n_fetch)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:  # a rank stuck on a flag must not outlive the test
+            if p.is_alive():
+                p.kill()
     # single-process reference on the full batch (same weights / routing; G=1)
     ref = HarMoEnyBlock.random(MoEConfig(**KW), seed=7, device="cuda", zipf_s=1.3, std=0.05)
     g = torch.Generator(device="cuda").manual_seed(99)
     x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
     y_ref = ref(x).cpu().view(torch.int16).numpy()
     Tg = T // world
-    assert np.array_equal(res[0][2], res[1][2]), "replicated schedules differ"
-    assert res[0][3] + res[1][3] > 0, "the skewed schedule should make some rank fetch experts"
+    for r in range(1, world):
+        assert np.array_equal(res[0][2], res[r][2]), "replicated schedules differ"
+    assert sum(res[r][3] for r in range(world)) > 0, "the skewed schedule should make some rank fetch experts"
     for r in range(world):
         y0, y1, _, _ = res[r]
         assert np.array_equal(y0, y_ref[r * Tg:(r + 1) * Tg])
