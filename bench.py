@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs (launch every kernel from Python)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="EP (N>1) exchanges: one-sided NVLink pushes + stream flags (graph-captured), or NCCL "
+                         "all_to_all (host round trip per layer for the split sizes)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = test harness for the multi-rank path on fewer GPUs (not a measurement)")
     ap.add_argument("--e2e-chunks", type=int, default=2,
@@ -295,7 +298,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
-        cfg = MoEConfig(rank=rank, world_size=world, eq_tokens=args.q, placement=args.placement, **cfg_kw)
+        cfg = MoEConfig(rank=rank, world_size=world, eq_tokens=args.q, placement=args.placement,
+                        transport=args.transport, max_tokens_per_rank=T_total // world, **cfg_kw)
         blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
     else:
         cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, **cfg_kw)
@@ -320,10 +324,17 @@ def run_ours(args, rank, world, local_rank):
         kernel_table(blk, x)
         return
 
-    # LOCAL (single process) forward has no host sync -> CUDA graphs (one per stage group,
-    # so gemm1 keeps its own event bracket inside the timed region); EP runs eagerly
+    # LOCAL and EP-p2p forwards never synchronise the host -> CUDA graphs (one per stage
+    # group, so gemm1 keeps its own event bracket inside the timed region); EP over NCCL
+    # runs eagerly (the all_to_all split sizes are host arguments)
+    ep_graph = world > 1 and args.transport == "p2p" and args.layers == 1 and not args.eager
     graphed = world == 1 and not args.eager
-    if graphed:
+    if ep_graph:
+        cap = blk.capture(T_local)
+        cap.x.copy_(x)
+        step = lambda marks=None: cap.replay(marks)  # noqa: E731
+        fwd_host = cap.forward_host
+    elif graphed:
         cap = blk.capture(T_local)
         cap.x.copy_(x)
         step = lambda marks=None: cap.replay(marks)  # noqa: E731
@@ -444,6 +455,7 @@ def run_ours(args, rank, world, local_rank):
             "layers": args.layers,
             "d_model": d, "d_ff": f, "experts": E, "top_k": k, "activation": act, "tokens": T_total,
             "q": args.q, "placement": args.placement, "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+            "transport": (f"{args.transport}" + (" (CUDA graphs)" if ep_graph else " (eager)")) if world > 1 else None,
             "l2": "flushed between timed steps (256 MB write)",
             "stages_us": stage_us,
             "block_roofline_tokens_per_sec": roof_tokens,

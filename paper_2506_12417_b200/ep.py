@@ -154,6 +154,8 @@ class EPHarMoEnyBlock:
         self.stats = BlockStats()
         if cfg.transport == "p2p":
             self._setup_p2p()
+            # ours: router, hist_scan, plan, ep_offsets, dispatch_push, fetch, gemm1, gemm2, combine
+            self.KERNELS_PER_FORWARD = 9
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s=None, std: float = 0.02, group=None):
@@ -269,62 +271,106 @@ class EPHarMoEnyBlock:
         self.recv_split = torch.empty(G + 1, dtype=torch.int32, device=self.device)
         dist.barrier(group=self.group)  # every arena zeroed and mapped before anyone signals
 
-    def _forward_p2p(self, x, s, mark):
+    def _p2p_stages(self, st, s):
+        """The p2p forward as three stream-ordered stages over the state dict ``st`` (input
+        st["x"]): "dispatch" (router, metadata push, plan, fused scatter + dispatch push),
+        "gemm1" (device-driven fetch forked onto the fetch stream + FFN1, joined), "combine"
+        (FFN2 storing into the source ranks + combine).  Each stage is graph-capturable."""
         cfg, G, E, me = self.cfg, self.G, self.cfg.num_experts, self.me
-        Tg, k, d = x.shape[0], cfg.top_k, cfg.d_model
-        if Tg > cfg.max_tokens_per_rank:
-            raise ValueError(f"{Tg} tokens exceed max_tokens_per_rank={cfg.max_tokens_per_rank}")
+        k, d = cfg.top_k, cfg.d_model
         L = _lib.load()
-        idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, 1, Tg, k, cfg.renormalize, E=E, stream=s)
-        tiles = (Tg + ops.TILE_M - 1) // ops.TILE_M
-        hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)
-        mark("router")
-        # step 2: my histogram row into every rank's m_all (peer stores), then flags
-        for addr in self.mall_row_addrs:
-            _lib.check(L.hm_fetch_expert(addr, hist.data_ptr(), E * 4, None, 0, s.cuda_stream), "m_all push")
-        ops.stream_signal(self.meta_addrs, 1, s)
-        ops.stream_wait(self.flags[0], 1, s)
-        ops.stream_signal(self.local_flag_addrs[0], 0, s)
-        p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
-                     stream=s)
-        S, lay = p.S, p.layout
-        m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
-        ops.ep_offsets(S, me, self.dst_delta, self.recv_split, stream=s)
-        mark("schedule")
-        # K6 from the device-side fetch list, on the fetch stream, overlapping the dispatch + FFN
-        if self.n_cache > 0:
-            ev = torch.cuda.Event()
-            ev.record(s)
+
+        def dispatch():
+            x = st["x"]
+            Tg = x.shape[0]
+            if Tg > cfg.max_tokens_per_rank:
+                raise ValueError(f"{Tg} tokens exceed max_tokens_per_rank={cfg.max_tokens_per_rank}")
+            idx, w, tile_hist, lrank = ops.router_topk(x, self.wg, self.bias, 1, Tg, k, cfg.renormalize, E=E,
+                                                       stream=s)
+            hist, tile_off = ops.hist_scan(tile_hist, 1, (Tg + ops.TILE_M - 1) // ops.TILE_M, stream=s)
+            # step 2: my histogram row into every rank's m_all (peer stores), then flags
+            for addr in self.mall_row_addrs:
+                _lib.check(L.hm_fetch_expert(addr, hist.data_ptr(), E * 4, None, 0, s.cuda_stream), "m_all push")
+            ops.stream_signal(self.meta_addrs, 1, s)
+            ops.stream_wait(self.flags[0], 1, s)
+            ops.stream_signal(self.local_flag_addrs[0], 0, s)
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
+                         stream=s)
+            m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
+            ops.ep_offsets(p.S, me, self.dst_delta, self.recv_split, stream=s)
+            pos = torch.empty((Tg, k), dtype=torch.int32, device=self.device)
+            ops.dispatch_push(x, idx, lrank, tile_off, p.S, p.layout.slot_base, self.dst_delta, me, self.p2p_rows,
+                              self.p2p_tok, pos=pos, stream=s)
+            ops.stream_signal(self.tok_addrs, 1, s)
+            ops.stream_wait(self.flags[1], 1, s)
+            ops.stream_signal(self.local_flag_addrs[1], 0, s)
+            st.update(idx=idx, w=w, plan=p, m_all=m_all, pos=pos, Tg=Tg)
+            self.stats = BlockStats(m_all=m_all, schedule=p.S, iters=p.iters, loads=p.loads,
+                                    extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=p.layout))
+
+        def gemm1():
+            lay = st["plan"].layout
             fs = self.fetch_stream
-            fs.wait_event(ev)
-            ops.fetch_experts(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.n_in * d * 2,
-                              d * cfg.d_ff * 2, self.w_in, self.w_out, self.n_home, self.n_cache, self.ready_in,
-                              self.ready_out, self.fetch_counters, value=1, stream=fs)
-        pos = torch.empty((Tg, k), dtype=torch.int32, device=self.device)
-        ops.dispatch_push(x, idx, lrank, tile_off, S, lay.slot_base, self.dst_delta, me, self.p2p_rows, self.p2p_tok,
-                          pos=pos, stream=s)
-        ops.stream_signal(self.tok_addrs, 1, s)
-        ops.stream_wait(self.flags[1], 1, s)
-        ops.stream_signal(self.local_flag_addrs[1], 0, s)
-        mark("dispatch_push")
-        ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
-                         slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s)
-        mark("gemm1")
-        ops.grouped_gemm_remote(self.h_buf, self.w_out.view(-1, cfg.d_ff), d, lay, ops.HM_EPI_STORE, self.p2p_out,
-                                self.recv_split, self.recv_tok, slot_ready=self.ready_out,
-                                ready_from_slot=self.n_home, epoch=1, stream=s)
-        if self.n_cache > 0:
-            self.ready_in[self.n_home:].zero_()
-            self.ready_out[self.n_home:].zero_()
-        ops.stream_signal(self.y_addrs, 1, s)
-        ops.stream_wait(self.flags[2], 1, s)
-        ops.stream_signal(self.local_flag_addrs[2], 0, s)
-        mark("gemm2_push")
-        y = ops.combine(self.y_ret[: Tg * k], None, w, residual=x if cfg.residual else None, stream=s)
-        mark("combine")
-        self.stats = BlockStats(m_all=m_all, schedule=S, iters=p.iters, loads=p.loads,
-                                extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=lay))
-        return y
+            if self.n_cache > 0:  # K6 from the device-side fetch list, overlapping FFN1
+                fs.wait_stream(s)
+                ops.fetch_experts(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.n_in * d * 2,
+                                  d * cfg.d_ff * 2, self.w_in, self.w_out, self.n_home, self.n_cache, self.ready_in,
+                                  self.ready_out, self.fetch_counters, value=1, stream=fs)
+            ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
+                             slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s)
+            if self.n_cache > 0:
+                s.wait_stream(fs)
+
+        def combine():
+            lay = st["plan"].layout
+            ops.grouped_gemm_remote(self.h_buf, self.w_out.view(-1, cfg.d_ff), d, lay, ops.HM_EPI_STORE,
+                                    self.p2p_out, self.recv_split, self.recv_tok, slot_ready=self.ready_out,
+                                    ready_from_slot=self.n_home, epoch=1, stream=s)
+            if self.n_cache > 0:
+                self.ready_in[self.n_home:].zero_()
+                self.ready_out[self.n_home:].zero_()
+            ops.stream_signal(self.y_addrs, 1, s)
+            ops.stream_wait(self.flags[2], 1, s)
+            ops.stream_signal(self.local_flag_addrs[2], 0, s)
+            x = st["x"]
+            st["y"] = ops.combine(self.y_ret[: st["Tg"] * k], None, st["w"], residual=x if cfg.residual else None,
+                                  stream=s)
+
+        return [("dispatch", dispatch), ("gemm1", gemm1), ("combine", combine)]
+
+    def _forward_p2p(self, x, s, mark):
+        st = {"x": x}
+        for name, fn in self._p2p_stages(st, s):
+            fn()
+            mark(name)
+        return st["y"]
+
+    def capture(self, num_tokens: int, pool=None):
+        """CUDA-graph the p2p forward (every rank must call it, same token count): the
+        forward never synchronises the host and its cross-rank waits are stream flags, so
+        all of it is captured, one graph per stage."""
+        from .block import CapturedForward
+
+        if self.cfg.transport != "p2p":
+            raise ValueError("only the p2p transport is graph-capturable (NCCL split sizes are host arguments)")
+        x = torch.zeros((num_tokens, self.cfg.d_model), dtype=torch.bfloat16, device=self.device)
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.forward(x, stream=side)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        st = {"x": x}
+        pool = pool if pool is not None else torch.cuda.graph_pool_handle()
+        graphs = []
+        for name, fn in self._p2p_stages(st, side):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=pool, stream=side):
+                fn()
+            graphs.append((name, g))
+        torch.cuda.synchronize(self.device)
+        return CapturedForward(graphs, x, st["y"], self.stats)
 
     def _fetch(self, experts):
         """K6: one transfer channel (the fetch stream), plan order, overwrite semantics:

@@ -42,7 +42,7 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
         from paper_2506_12417_b200.block import MoEConfig
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
-        cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, transport=transport,
+        cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, transport=transport.split("-")[0],
                         max_tokens_per_rank=T // world, **KW)
         blk = EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
         g = torch.Generator(device="cuda").manual_seed(99)
@@ -50,8 +50,14 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
         Tg = T // world
         xl = x[rank * Tg:(rank + 1) * Tg].contiguous()
         outs = []
-        for _ in range(3):  # later forwards re-use the fetch slots and the peer flags
-            outs.append(blk(xl).cpu())
+        if transport == "p2p-graph":
+            cap = blk.capture(Tg)  # every rank captures; replays synchronise through the flags
+            cap.x.copy_(xl)
+            for _ in range(3):
+                outs.append(cap.replay().clone().cpu())
+        else:
+            for _ in range(3):  # later forwards re-use the fetch slots and the peer flags
+                outs.append(blk(xl).cpu())
         torch.cuda.synchronize()
         out_q.put((rank, outs[0].view(torch.int16).numpy(), outs[2].view(torch.int16).numpy(),
                    blk.stats.schedule.cpu().numpy(), int(blk.stats.extras["layout"].n_fetch.item())))
@@ -61,7 +67,8 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
 
 @pytest.mark.parametrize("fetch_source,transport,world", [("peer", "nccl", 2), ("host", "nccl", 2),
                                                            ("peer", "p2p", 2), ("host", "p2p", 2),
-                                                           ("peer", "p2p", 4)])
+                                                           ("peer", "p2p", 4), ("peer", "p2p-graph", 2),
+                                                           ("host", "p2p-graph", 4)])
 def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
     """transport "nccl": exchanges through the process group (gloo here, host-staged);
     transport "p2p": one-sided pushes into the other ranks' IPC-mapped buffers + stream flags,
