@@ -55,6 +55,11 @@ extern "C" {
 #define HM_EPI_SWIGLU 2 /* out = bf16(silu(gate) * up), W13 block-interleaved by 128 rows */
 
 /* dispatch layouts */
+/* scheduling policy (the `rebalance` argument of hm_schedule / hm_schedule_batched / hm_plan) */
+#define HM_POLICY_NONE 0       /* initial_assign only (policies.py:109-117; SimFlags rebalancing off) */
+#define HM_POLICY_REBALANCE 1  /* initial_assign + Alg. 2 rebalance (policies.py:120-141) */
+#define HM_POLICY_EVEN_SPLIT 2 /* even_split_assign baseline (policies.py:174-203); ignores home and q */
+
 #define HM_LAYOUT_LOCAL 0 /* all G ranks on this device: buffer [dest][expert][source][rank] */
 #define HM_LAYOUT_EP 1    /* this process is rank `me`: send buffer [dest][expert][rank], */
                           /* receive buffer [source][expert][rank] (NCCL all_to_all chunks) */
@@ -94,6 +99,8 @@ HM_API int hm_hist_scan(const int32_t* tile_hist, int n_ranks, int tiles_per_ran
  * Scheduler (K3): S[g,e,home[e]] = m_all[g,e] (policies.py:109-117), then, when `rebalance`,
  * HarMoEny's greedy token rebalancing (policies.py:120-141, Alg. 2) with threshold q, bit-exact
  * against the reference (lowest-index ties).  Replicated on every rank; no communication.
+ * `rebalance` is an HM_POLICY_* code (0/1 keep their boolean meaning); HM_POLICY_EVEN_SPLIT
+ * builds the even_split_assign baseline schedule (policies.py:174-203) instead, iters = 0.
  *   m_all [G,E] int32, home [E] int32 -> S [G,E,G] int32, iters [1] int32, loads [G] int32 (or NULL).
  * q < 1 -> HM_EINVAL ("token threshold q must be >= 1").  Requires G <= 32.
  */

@@ -56,6 +56,9 @@ def lib():
         L.orc_histogram.restype = None
         L.orc_dispatch_ranks.argtypes = [p32, ctypes.c_int64, p64, ctypes.c_int, ctypes.c_int, ctypes.c_int, p32, p32]
         L.orc_plan_order.argtypes = [p64, p32, ctypes.c_int, p32]
+        L.orc_even_split.argtypes = [p64, ctypes.c_int, ctypes.c_int, p64]
+        L.orc_even_split.restype = None
+        L.orc_affinity.argtypes = [p64, ctypes.c_int, ctypes.c_int, ctypes.c_int, p64]
         L.orc_round_robin.argtypes = [ctypes.c_int, ctypes.c_int, p64]
         L.orc_round_robin.restype = None
         L.orc_blocked.argtypes = [ctypes.c_int, ctypes.c_int, p64]
@@ -104,6 +107,24 @@ def rebalance_with_stats(S0, q: int):
     if lib().orc_rebalance(_p64(S), G, E, int(q), _p64(it)):
         raise ValueError("token threshold q must be >= 1")
     return S, int(it[0])
+
+
+def even_split(m_all) -> np.ndarray:
+    """even_split_assign (policies.py:174-203)."""
+    m = np.ascontiguousarray(m_all, dtype=np.int64)
+    G, E = m.shape
+    S = np.empty((G, E, G), np.int64)
+    lib().orc_even_split(_p64(m), G, E, _p64(S))
+    return S
+
+
+def affinity_home(counts, G: int, slots: int) -> np.ndarray:
+    """affinity_placement (policies.py:206-229) -> home[E]."""
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    h = np.empty(c.shape[0], np.int64)
+    if lib().orc_affinity(_p64(c), c.shape[0], int(G), int(slots), _p64(h)):
+        raise ValueError(f"infeasible placement: {c.shape[0]} experts > {G} GPUs x {slots} slots")
+    return h
 
 
 def schedule(m_all, home, q: int, rebalance: bool = True):

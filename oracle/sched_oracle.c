@@ -13,6 +13,8 @@
  *                            PAPER.md:702-745); argmax/argmin ties break to the
  *                            lowest index exactly like numpy (policies.py:15-16)
  *   orc_round_robin / orc_blocked <- policies.py:91-106
+ *   orc_even_split       <- moesim/policies.py:174-203   (even_split_assign baseline)
+ *   orc_affinity         <- moesim/policies.py:206-229   (affinity_placement, LPT)
  *   orc_histogram        <- core.py:89-96 (RoutingMatrix row = per-GPU histogram)
  *   orc_dispatch_ranks   <- the split-bucket contract of SURVEY.md §8(a) A13
  *                            (the reference drops token identity)
@@ -115,6 +117,64 @@ int orc_schedule(const int64_t* m, const int64_t* home, int G, int E, int64_t q,
     if (rc) return rc;
     if (rebalance) return orc_rebalance(S, G, E, q, iters);
     if (q < 1) return 1;
+    return 0;
+}
+
+/* policies.py:174-203: each expert's pooled total split as evenly as integers allow
+ * (remainder to the lowest-index GPUs); sources fill the targets in index order. */
+void orc_even_split(const int64_t* m, int G, int E, int64_t* S) {
+    memset(S, 0, sizeof(int64_t) * (size_t)G * E * G);
+    int64_t* remaining = (int64_t*)malloc(sizeof(int64_t) * (size_t)G);
+    for (int e = 0; e < E; ++e) {
+        int64_t total = 0;
+        for (int g = 0; g < G; ++g) total += m[(int64_t)g * E + e];
+        if (total == 0) continue;
+        int64_t base = total / G, rem = total % G;
+        for (int g = 0; g < G; ++g) remaining[g] = base + (g < rem ? 1 : 0);
+        int dest = 0;
+        for (int src = 0; src < G; ++src) {
+            int64_t left = m[(int64_t)src * E + e];
+            while (left > 0) {
+                while (remaining[dest] == 0) ++dest;
+                int64_t take = left < remaining[dest] ? left : remaining[dest];
+                S[IDX3(src, e, dest, E, G)] += take;
+                remaining[dest] -= take;
+                left -= take;
+            }
+        }
+    }
+    free(remaining);
+}
+
+/* policies.py:206-229: experts by descending popularity (ties: lower id) onto the GPU with
+ * the least accumulated mass that has a free slot (ties: lower GPU).  Returns 1 if
+ * E > G * slots (the reference's ValueError), else 0. */
+int orc_affinity(const int64_t* counts, int E, int G, int slots, int64_t* home) {
+    if ((int64_t)E > (int64_t)G * slots) return 1;
+    int* order = (int*)malloc(sizeof(int) * (size_t)(E > 0 ? E : 1));
+    int64_t* mass = (int64_t*)calloc((size_t)G, sizeof(int64_t));
+    int* used = (int*)calloc((size_t)G, sizeof(int));
+    for (int e = 0; e < E; ++e) order[e] = e;
+    /* insertion sort by (-count, id): stable and E is small */
+    for (int i = 1; i < E; ++i) {
+        int v = order[i], j = i - 1;
+        while (j >= 0 && counts[order[j]] < counts[v]) {
+            order[j + 1] = order[j];
+            --j;
+        }
+        order[j + 1] = v;
+    }
+    for (int i = 0; i < E; ++i) {
+        int e = order[i], best = -1;
+        for (int g = 0; g < G; ++g)
+            if (used[g] < slots && (best < 0 || mass[g] < mass[best])) best = g;
+        home[e] = best;
+        mass[best] += counts[e];
+        used[best] += 1;
+    }
+    free(order);
+    free(mass);
+    free(used);
     return 0;
 }
 

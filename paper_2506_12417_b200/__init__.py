@@ -19,10 +19,13 @@ from .core import (
 from .engine import SimFlags, build_schedule, static_placement
 from .policies import (
     PlacementKind,
+    PopularityProfile,
     SchedulerConfig,
     SchedulingPolicy,
+    affinity_placement,
     blocked_placement,
     estimate_token_threshold,
+    even_split_assign,
     initial_assign,
     rebalance,
     rebalance_with_stats,
@@ -55,5 +58,5 @@ __all__ = [
     "SchedulingPolicy", "blocked_placement", "estimate_token_threshold", "initial_assign", "rebalance",
     "rebalance_with_stats", "round_robin_placement", "threshold_bound", "skew_probabilities",
     "zipf_probabilities", "zipf_routing_matrix", "HarMoEnyBlock", "MoEConfig", "BlockStats", "replace_moe_layer",
-    "HarMoEnyLayer", "MeasuredCostModel", "Trace", "TraceBatch", "TraceParseError", "read_trace", "write_trace",
+    "HarMoEnyLayer", "MeasuredCostModel", "PopularityProfile", "affinity_placement", "even_split_assign", "Trace", "TraceBatch", "TraceParseError", "read_trace", "write_trace",
 ]

@@ -14,6 +14,7 @@ import os
 HM_OK, HM_EINVAL, HM_ECUDA, HM_ENCCL, HM_ENOSPC = 0, 1, 2, 3, 4
 HM_EPI_STORE, HM_EPI_RELU, HM_EPI_SWIGLU = 0, 1, 2
 HM_LAYOUT_LOCAL, HM_LAYOUT_EP = 0, 1
+HM_POLICY_NONE, HM_POLICY_REBALANCE, HM_POLICY_EVEN_SPLIT = 0, 1, 2
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libharmoe.so")
 

@@ -36,11 +36,20 @@ from . import ops
 from .policies import PlacementKind, SchedulingPolicy, blocked_placement, round_robin_placement
 
 
+_POLICY_CODES = {
+    "harmony": ops.HM_POLICY_REBALANCE, "harmoeny": ops.HM_POLICY_REBALANCE, "rebalance": ops.HM_POLICY_REBALANCE,
+    "round_robin": ops.HM_POLICY_NONE, "static": ops.HM_POLICY_NONE, "none": ops.HM_POLICY_NONE,
+    "even_split": ops.HM_POLICY_EVEN_SPLIT,
+}
+
+
 @dataclass
 class MoEConfig:
     rank: int = 0
     world_size: int = 1
-    scheduling_policy: str = "harmony"  # "harmony"/"rebalance" or "round_robin" (no rebalancing)
+    # "harmony"/"rebalance" (Alg. 2), "round_robin" (static placement, no rebalancing) or
+    # "even_split" (the paper's even-split baseline, policies.py:174-203)
+    scheduling_policy: str = "harmony"
     expert_cache_size: int = 0  # fetch slots per GPU (0 = one per fetched expert)
     eq_tokens: int = 32  # token threshold q (Eq. 4)
     d_model: int = 2048
@@ -61,6 +70,8 @@ class MoEConfig:
     def __post_init__(self):
         if self.eq_tokens < 1:
             raise ValueError("token_threshold_q must be >= 1")
+        if str(getattr(self.scheduling_policy, "value", self.scheduling_policy)).lower() not in _POLICY_CODES:
+            raise ValueError(f"unknown scheduling_policy {self.scheduling_policy!r}")
         if self.transport not in ("nccl", "p2p"):
             raise ValueError("transport must be 'nccl' or 'p2p'")
         if self.max_tokens_per_rank < 1:
@@ -73,8 +84,13 @@ class MoEConfig:
             raise ValueError("logical ranks are a single-process mode (world_size == 1)")
 
     @property
+    def policy_code(self) -> int:
+        """HM_POLICY_* code the planner kernel runs."""
+        return _POLICY_CODES[str(getattr(self.scheduling_policy, "value", self.scheduling_policy)).lower()]
+
+    @property
     def rebalance(self) -> bool:
-        return str(self.scheduling_policy).lower() in ("harmony", "harmoeny", "rebalance", SchedulingPolicy.REBALANCE)
+        return self.policy_code == ops.HM_POLICY_REBALANCE
 
     @property
     def num_ranks(self) -> int:
@@ -321,7 +337,7 @@ class HarMoEnyBlock:
 
         def plan():
             # steps 2+3 fused: per-rank histograms (m_all), schedule S, layout + GEMM work list
-            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_LOCAL,
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_LOCAL,
                          tile_hist=st["tile_hist"], tiles_per_rank=tiles_per_rank, stream=s)
             st["plan"] = p
             self.stats = BlockStats(m_all=p.m_all, schedule=p.S, iters=p.iters, loads=p.loads,

@@ -181,7 +181,7 @@ def measure_cost_model(cfg, token_points=DEFAULT_POINTS, probe_experts: int | No
     G = cfg.num_ranks
     home = torch.tensor([e % G for e in range(E)], dtype=torch.int32, device=dev)
     m_all = torch.randint(0, 64, (G, E), dtype=torch.int32, device=dev, generator=g)
-    meta = _time_ms(lambda: ops.plan(home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_LOCAL, m_all=m_all),
+    meta = _time_ms(lambda: ops.plan(home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_LOCAL, m_all=m_all),
                     reps) / 1e3
     try:
         import torch.distributed as dist

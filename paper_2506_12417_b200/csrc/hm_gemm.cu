@@ -322,7 +322,9 @@ struct PairCursor {
   int s = 0;
   int base = 0;  // pair-tile index (x NB) where segment s starts
   __device__ __forceinline__ int pair_tiles(int i) const { return (mp[i + 1] - mp[i] + 1) >> 1; }
-  __device__ __forceinline__ void seek(int t, int4& seg, int& m, int& nb) {
+  // hf: the segment's last pair tile holds <= 128 rows (odd 128-row tile count) and runs as
+  // an M=128 cta_group::2 MMA (64 rows per CTA) instead of a half-empty M=256 one
+  __device__ __forceinline__ void seek(int t, int4& seg, int& m, int& nb, bool& hf) {
     int span = pair_tiles(s) * NB;
     while (base + span <= t) {
       base += span;
@@ -334,7 +336,9 @@ struct PairCursor {
     const int local = t - base;
     nb = local / ms;
     m = local - nb * ms;
+    hf = half_tiles && m == ms - 1 && ((mp[s + 1] - mp[s]) & 1);
   }
+  bool half_tiles = true;
 };
 
 // kGather: the A tile is not TMA-loaded from a permuted buffer but gathered straight from
@@ -361,7 +365,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 template <int kEpi, bool kGather>
 __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kGemmThreads, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                             const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
+                             const __grid_constant__ CUtensorMap tmap_a64, const __grid_constant__ CUtensorMap tmap_b64,
+                             int half_tiles, const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
                              const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K,
                              int ldo, const int* __restrict__ row_map, const int* __restrict__ slot_ready,
                              int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
@@ -402,6 +407,10 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     fence_mbar_init();
     if (!kGather) tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
+    if (half_tiles) {
+      if (!kGather) tma_prefetch_desc(&tmap_a64);
+      if (kEpi == kEpiSwiGLU) tma_prefetch_desc(&tmap_b64);
+    }
   }
   if (warp == 1) tmem_alloc_2cta<kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -425,14 +434,21 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       const uint64_t pol_b = l2_policy_evict_last();
       const uint32_t full_leader = mapa_shared(full, 0);
       PairCursor cur{segs, mp, NB};
+      cur.half_tiles = half_tiles != 0;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total; t += npairs) {
         int4 seg;
         int m, nb;
-        cur.seek(t, seg, m, nb);
-        const int row0 = seg.x + m * 2 * kBM + (int)rank * kBM;
-        const int brow = seg.z * N + nb * kBN + (int)rank * (kBN / 2);
+        bool hf;
+        cur.seek(t, seg, m, nb, hf);
+        const int row0 = seg.x + m * 2 * kBM + (int)rank * (hf ? kBM / 2 : kBM);
+        const int brow0 = seg.z * N + nb * kBN;
+        const int brow = brow0 + (int)rank * (kBN / 2);
+        // half tile: A is 64 rows per CTA; SwiGLU B is re-paired so CTA r holds gate rows
+        // [64r, 64r+64) then the matching up rows -> every TMEM lane holds gate and up
+        const bool b_split = hf && kEpi == kEpiSwiGLU;
+        const uint32_t tx = (kGather ? 0u : (hf ? k2Half / 2 : k2Half)) + k2Half;
         if (slot_ready != nullptr && seg.z >= ready_from_slot) {
           // watchdog: a fetch that never lands is a bug upstream; fail the launch instead of
           // hanging the device (~10 s)
@@ -445,10 +461,18 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         }
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(&full[stage], (kGather ? 2 : 4) * k2Half);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * tx);
           uint8_t* sa = smem + stage * 2 * k2Half;
-          if (!kGather) tma_load_2d_2cta(sa, &tmap_a, full_leader + stage * 8, kb * kBK, row0, pol_a);
-          tma_load_2d_2cta(sa + k2Half, &tmap_b, full_leader + stage * 8, kb * kBK, brow, pol_b);
+          if (!kGather)
+            tma_load_2d_2cta(sa, hf ? &tmap_a64 : &tmap_a, full_leader + stage * 8, kb * kBK, row0, pol_a);
+          if (b_split) {
+            tma_load_2d_2cta(sa + k2Half, &tmap_b64, full_leader + stage * 8, kb * kBK, brow0 + (int)rank * 64,
+                             pol_b);
+            tma_load_2d_2cta(sa + k2Half + k2Half / 2, &tmap_b64, full_leader + stage * 8, kb * kBK,
+                             brow0 + kBN / 2 + (int)rank * 64, pol_b);
+          } else {
+            tma_load_2d_2cta(sa + k2Half, &tmap_b, full_leader + stage * 8, kb * kBK, brow, pol_b);
+          }
           if (++stage == k2Stages) {
             stage = 0;
             phase ^= 1;
@@ -459,11 +483,19 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ===== MMA issuer (leader CTA) =====
-      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, kBN);
+      constexpr uint32_t idesc_full = make_idesc_bf16(2 * kBM, kBN);
+      constexpr uint32_t idesc_half = make_idesc_bf16(kBM, kBN);  // 64 rows per CTA, "2x2" TMEM layout
+      PairCursor cur{segs, mp, NB};
+      cur.half_tiles = half_tiles != 0;
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
       for (int t = pair; t < total; t += npairs, ++i) {
+        int4 seg;
+        int m, nb;
+        bool hf;
+        cur.seek(t, seg, m, nb, hf);
+        const uint32_t idesc = hf ? idesc_half : idesc_full;
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -495,14 +527,17 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const int sub = lane >> 3;              // row within a group of 4
     const uint32_t full_leader = mapa_shared(full, 0);
     PairCursor cur{segs, mp, NB};
+    cur.half_tiles = half_tiles != 0;
     int stage = 0, sig_stage = 0, pending = 0;
     uint32_t phase = 0;
     for (int t = pair; t < total; t += npairs) {
       int4 seg;
       int m, nb;
-      cur.seek(t, seg, m, nb);
-      const int rows = max(0, min(kBM, seg.y - m * 2 * kBM - (int)rank * kBM));
-      const int rbase = seg.x + m * 2 * kBM + (int)rank * kBM;
+      bool hf;
+      cur.seek(t, seg, m, nb, hf);
+      const int cta_rows = hf ? kBM / 2 : kBM;
+      const int rows = max(0, min(cta_rows, seg.y - m * 2 * kBM - (int)rank * cta_rows));
+      const int rbase = seg.x + m * 2 * kBM + (int)rank * cta_rows;
       const char* src[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -517,7 +552,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = lw * 32 + i * 4 + sub;
-          cp_async16(dst + r * 128 + ((c ^ (r & 7)) << 4), src[i] + kb * 128);
+          if (r < cta_rows) cp_async16(dst + r * 128 + ((c ^ (r & 7)) << 4), src[i] + kb * 128);
         }
         cp_async_commit();
         if (++pending > kALookahead) {
@@ -552,18 +587,29 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const uint32_t my_srow = stg + lane * kStgPitch;
     const uint32_t tempty_leader = mapa_shared(tempty, 0);
     PairCursor cur{segs, mp, NB};
+    cur.half_tiles = half_tiles != 0;
     int i = 0;
     for (int t = pair; t < total; t += npairs, ++i) {
       int4 seg;
       int m, nb;
-      cur.seek(t, seg, m, nb);
-      const int rows = max(0, min(kBM, seg.y - m * 2 * kBM - (int)rank * kBM));  // this CTA's valid rows
-      const int r_in_tile = q * 32 + lane;
+      bool hf;
+      cur.seek(t, seg, m, nb, hf);
+      // Full tile: lane = row (128 per CTA), columns [0, 256).  Half tile (M=128 "2x2" layout):
+      // row r < 64 of this CTA sits in lanes r (columns [0,128) of the MMA's N) and 64 + r
+      // (columns [128,256)), both at TMEM columns [0,128).  SwiGLU half tiles were loaded
+      // with B re-paired, so each lane half holds 64 gate columns then the 64 matching up.
+      const int cta_rows = hf ? kBM / 2 : kBM;
+      const int rows = max(0, min(cta_rows, seg.y - m * 2 * kBM - (int)rank * cta_rows));  // valid rows
+      const int r_in_tile = (hf ? (q & 1) : q) * 32 + lane;
+      const int ncols = hf ? kHalfCols / 2 : kHalfCols;  // output columns of this warp
+      const int tcol0 = half * ncols;                    // its first TMEM column
+      const int ocol0 = (hf ? (q >> 1) * kHalfCols : 0) + half * ncols;
+      const int upoff = hf ? kBN / 4 : kBN / 2;  // SwiGLU: TMEM column distance gate -> up
       const bool valid = r_in_tile < rows;
-      int64_t row = (int64_t)seg.x + m * 2 * kBM + rank * kBM + r_in_tile;
+      int64_t row = (int64_t)seg.x + m * 2 * kBM + rank * cta_rows + r_in_tile;
       if (row_map != nullptr && valid) row = __ldg(row_map + row);
-      const int64_t obase = row * ldo + (int64_t)nb * kOutCols + half * kHalfCols;
-      const int nvalid = max(0, min(32, rows - q * 32));
+      const int64_t obase = row * ldo + (int64_t)nb * kOutCols + ocol0;
+      const int nvalid = max(0, min(32, rows - (r_in_tile - lane)));
       // remote output (EP over peer memory): the segment's rows belong to source rank g, the
       // one whose receive range [out_split[g], out_split[g+1]) holds the segment; its rows are
       // stored straight into that rank's token-major output over NVLink
@@ -578,11 +624,11 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < kHalfCols; c0 += kStgCols) {
+      for (int c0 = 0; c0 < ncols; c0 += kStgCols) {
         uint32_t a[32], u[32];
-        const int col = half * kHalfCols + c0;
+        const int col = tcol0 + c0;
         tmem_ld_32x32b_x32(taddr + col, a);
-        if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + 128 + col, u);
+        if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + upoff + col, u);
         tmem_ld_wait();
         stage_row<kEpi>(my_srow, a, u);
         __syncwarp();
@@ -611,6 +657,15 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     tc_fence_after();
     tmem_dealloc_2cta<kTmemCols>(tmem_base);
   }
+}
+
+static bool use_half_tiles() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HM_GEMM_NO_HALF");
+    v = (e != nullptr && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 static bool use_2cta() {
@@ -650,6 +705,17 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     CUtensorMap tb2;  // each CTA of the pair loads 128 of the tile's 256 weight rows
     rc = make_tmap_2d_bf16(&tb2, W, (uint64_t)w_rows, (uint64_t)K, kBN / 2, kBK);
     if (rc) return rc;
+    // half tiles: 64-row A boxes, and 64-row B boxes for the re-paired SwiGLU weight halves
+    const int half_tiles = use_half_tiles() ? 1 : 0;
+    CUtensorMap ta64 = ta, tb64 = tb2;
+    if (half_tiles && a_gather == nullptr) {
+      rc = make_tmap_2d_bf16(&ta64, A, (uint64_t)a_rows, (uint64_t)K, kBM / 2, kBK);
+      if (rc) return rc;
+    }
+    if (half_tiles && epilogue == kEpiSwiGLU) {
+      rc = make_tmap_2d_bf16(&tb64, W, (uint64_t)w_rows, (uint64_t)K, kBN / 4, kBK);
+      if (rc) return rc;
+    }
     const bool gather = a_gather != nullptr;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(grid & ~1));
@@ -669,7 +735,8 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
   do {                                                                                                            \
     cudaFuncSetAttribute(grouped_gemm_2cta_kernel<EPI, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
                          (int)kGemm2Smem);                                                                        \
-    e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, s4, mtile_prefix, n_seg, o, N, K,     \
+    e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, ta64, tb64, half_tiles, s4,          \
+                           mtile_prefix, n_seg, o, N, K,                                                          \
                            ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
                            (int)a_rows, out_ptrs, out_split, n_out);                                              \
   } while (0)

@@ -220,10 +220,38 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
   if (init_from_m) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) S[i] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < G * E; i += blockDim.x) {
-      const int g = i / E, e = i - (i / E) * E;
-      S[(g * E + e) * G + home[e]] = m_all[i];
+    if (rebalance == HM_POLICY_EVEN_SPLIT) {
+      // even_split_assign (policies.py:174-203): expert e's pooled total split as evenly as
+      // integers allow (remainder to the lowest-index GPUs), sources fill the per-GPU targets
+      // in index order.  One thread per expert; at most 2G-1 (source, dest) steps.
+      for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        int total = 0;
+        for (int g = 0; g < G; ++g) total += m_all[g * E + e];
+        if (total == 0) continue;
+        const int base = total / G, rem = total - base * G;
+        int dest = 0;
+        int room = base + (0 < rem ? 1 : 0);
+        for (int src = 0; src < G; ++src) {
+          int left = m_all[src * E + e];
+          while (left > 0) {
+            while (room == 0) {
+              ++dest;
+              room = base + (dest < rem ? 1 : 0);
+            }
+            const int take = min(left, room);
+            S[(src * E + e) * G + dest] += take;
+            room -= take;
+            left -= take;
+          }
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < G * E; i += blockDim.x) {
+        const int g = i / E, e = i - (i / E) * E;
+        S[(g * E + e) * G + home[e]] = m_all[i];
+      }
     }
+    if (rebalance != HM_POLICY_REBALANCE) rebalance = HM_POLICY_NONE;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < G * G; i += blockDim.x) {
@@ -677,6 +705,8 @@ int launch_schedule_batched(const int32_t* m_all, const int32_t* home, int B, in
                             int32_t* S, int32_t* iters, int32_t* loads, cudaStream_t stream) {
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
   if (G < 1 || G > 32 || E < 1) return set_error(HM_EINVAL, "schedule: need 1 <= G <= 32 and E >= 1");
+  if (rebalance < HM_POLICY_NONE || rebalance > HM_POLICY_EVEN_SPLIT)
+    return set_error(HM_EINVAL, "schedule: unknown policy code");
   if (B < 0) return set_error(HM_EINVAL, "schedule: batch count must be >= 0");
   if (B == 0) return HM_OK;
   const size_t sbytes = (size_t)2 * G * E * G * sizeof(int);  // S + transposed copy for the fast loop
@@ -734,6 +764,8 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
   int rc = check_layout_args(G, E, mode, me);
   if (rc) return rc;
+  if (rebalance < HM_POLICY_NONE || rebalance > HM_POLICY_EVEN_SPLIT)
+    return set_error(HM_EINVAL, "plan: unknown policy code");
   const bool hist = tile_hist != nullptr;
   if (hist && mode != HM_LAYOUT_LOCAL) return set_error(HM_EINVAL, "plan: tile histograms imply the LOCAL layout");
   if (!hist && m_in == nullptr) return set_error(HM_EINVAL, "plan: need tile_hist or m_all");

@@ -33,21 +33,25 @@ class SimFlags:
 
 def build_schedule(m_all: RoutingMatrix, placement: Placement, config: SchedulerConfig,
                    flags: SimFlags) -> ScheduleTensor:
-    """initial_assign (+ rebalance when policy is REBALANCE and enabled), one GPU kernel launch."""
+    """Policy dispatch of engine.py:287-299 in one GPU kernel launch: even_split_assign for
+    EVEN_SPLIT, else initial_assign (+ rebalance when policy is REBALANCE and enabled)."""
     import numpy as np
     import torch
 
     from . import ops
     from .policies import _to_i32
 
-    if config.policy is SchedulingPolicy.EVEN_SPLIT:
-        raise NotImplementedError("even_split is a baseline policy outside the HarMoEny hot path (SURVEY.md §2)")
-    if placement.num_experts != m_all.num_experts or placement.num_gpus != m_all.num_gpus:
-        raise ValueError("placement dimensions do not match routing matrix")
-    do_rebalance = config.policy is SchedulingPolicy.REBALANCE and flags.rebalancing_enabled
+    home = np.asarray(placement.home, np.int64)
+    if config.policy is SchedulingPolicy.EVEN_SPLIT:  # even_split_assign(m_all, m_all.num_gpus), engine.py:293
+        policy = ops.HM_POLICY_EVEN_SPLIT
+        home = np.zeros(m_all.num_experts, np.int64)  # the even split ignores the placement
+    else:
+        if placement.num_experts != m_all.num_experts or placement.num_gpus != m_all.num_gpus:
+            raise ValueError("placement dimensions do not match routing matrix")
+        do_rebalance = config.policy is SchedulingPolicy.REBALANCE and flags.rebalancing_enabled
+        policy = ops.HM_POLICY_REBALANCE if do_rebalance else ops.HM_POLICY_NONE
     S, _, _ = ops.schedule(_to_i32(m_all.counts, "build_schedule"),
-                           _to_i32(np.asarray(placement.home, np.int64), "home"),
-                           config.token_threshold_q, rebalance=do_rebalance)
+                           _to_i32(home, "home"), config.token_threshold_q, rebalance=policy)
     torch.cuda.current_stream().synchronize()
     return ScheduleTensor(S.cpu().numpy().astype(np.int64))
 

@@ -294,7 +294,7 @@ class EPHarMoEnyBlock:
             ops.stream_signal(self.meta_addrs, 1, s)
             ops.stream_wait(self.flags[0], 1, s)
             ops.stream_signal(self.local_flag_addrs[0], 0, s)
-            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
                          stream=s)
             m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
             ops.ep_offsets(p.S, me, self.dst_delta, self.recv_split, stream=s)
@@ -426,7 +426,7 @@ class EPHarMoEnyBlock:
             hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)
             mark("router")
             m_all = exchange_metadata(hist, self.group)
-            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.rebalance, ops.HM_LAYOUT_EP, me, m_all=m_all, stream=s)
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP, me, m_all=m_all, stream=s)
             S, iters, loads, lay = p.S, p.iters, p.loads, p.layout
             self.S_host.copy_(S, non_blocking=True)
             self.fetch_host[:E].copy_(lay.fetch, non_blocking=True)

@@ -123,27 +123,39 @@ def patch_moesim(moesim_module=None):
     ref_core = moesim_module.core
     from . import policies
 
-    orig = (eng.build_schedule, eng.rebalance)
+    orig = (eng.build_schedule, eng.rebalance, eng.even_split_assign, eng.affinity_placement)
 
     def rebalance(s_initial, q):
         s, _ = policies.rebalance_with_stats(s_initial, q)
         return ref_core.ScheduleTensor(np.asarray(s.counts))
 
+    def even_split_assign(m_all, num_gpus):
+        return ref_core.ScheduleTensor(np.asarray(policies.even_split_assign(m_all, num_gpus).counts))
+
+    def affinity_placement(profile, num_gpus, slots):
+        p = policies.affinity_placement(policies.PopularityProfile(counts=profile.counts,
+                                                                   window_batches=profile.window_batches),
+                                        num_gpus, slots)
+        return ref_core.Placement(home=p.home, num_gpus=p.num_gpus)
+
     def build_schedule(m_all, placement, config, flags):
-        if config.policy is moesim_module.SchedulingPolicy.EVEN_SPLIT:
-            return orig[0](m_all, placement, config, flags)  # baseline policy: left to the reference
         from . import ops
         from .policies import _to_i32
 
-        do_rb = config.policy is moesim_module.SchedulingPolicy.REBALANCE and flags.rebalancing_enabled
-        S, _, _ = ops.schedule(_to_i32(m_all.counts, "build_schedule"),
-                               _to_i32(np.asarray(placement.home, np.int64), "home"),
-                               config.token_threshold_q, rebalance=do_rb)
+        home = np.asarray(placement.home, np.int64)
+        if config.policy is moesim_module.SchedulingPolicy.EVEN_SPLIT:  # engine.py:292-293
+            policy, home = ops.HM_POLICY_EVEN_SPLIT, np.zeros(m_all.num_experts, np.int64)
+        else:
+            do_rb = config.policy is moesim_module.SchedulingPolicy.REBALANCE and flags.rebalancing_enabled
+            policy = ops.HM_POLICY_REBALANCE if do_rb else ops.HM_POLICY_NONE
+        S, _, _ = ops.schedule(_to_i32(m_all.counts, "build_schedule"), _to_i32(home, "home"),
+                               config.token_threshold_q, rebalance=policy)
         return ref_core.ScheduleTensor(S.cpu().numpy().astype(np.int64))
 
     eng.build_schedule, eng.rebalance = build_schedule, rebalance
+    eng.even_split_assign, eng.affinity_placement = even_split_assign, affinity_placement
 
     def restore():
-        eng.build_schedule, eng.rebalance = orig
+        eng.build_schedule, eng.rebalance, eng.even_split_assign, eng.affinity_placement = orig
 
     return restore

@@ -9,7 +9,16 @@ from __future__ import annotations
 import torch
 
 from . import _lib
-from ._lib import HM_EPI_RELU, HM_EPI_STORE, HM_EPI_SWIGLU, HM_LAYOUT_EP, HM_LAYOUT_LOCAL  # noqa: F401
+from ._lib import (  # noqa: F401
+    HM_EPI_RELU,
+    HM_EPI_STORE,
+    HM_EPI_SWIGLU,
+    HM_LAYOUT_EP,
+    HM_LAYOUT_LOCAL,
+    HM_POLICY_EVEN_SPLIT,
+    HM_POLICY_NONE,
+    HM_POLICY_REBALANCE,
+)
 
 TILE_M = 128
 
@@ -22,6 +31,16 @@ def _require_cuda(*tensors):
             raise ValueError("harmoe ops need CUDA tensors (no CPU fallback)")
         if not t.is_contiguous():
             raise ValueError("harmoe ops need contiguous tensors")
+
+
+def _policy(rebalance) -> int:
+    """bool (rebalance on/off) or an HM_POLICY_* code -> the C ABI's policy argument."""
+    if isinstance(rebalance, bool):
+        return HM_POLICY_REBALANCE if rebalance else HM_POLICY_NONE
+    code = int(rebalance)
+    if code not in (HM_POLICY_NONE, HM_POLICY_REBALANCE, HM_POLICY_EVEN_SPLIT):
+        raise ValueError(f"unknown scheduling policy code {code}")
+    return code
 
 
 def _ptr(t):
@@ -85,7 +104,7 @@ def schedule(m_all, home, q: int, rebalance: bool = True, stream=None):
     S = torch.empty((G, E, G), dtype=torch.int32, device=dev)
     iters = torch.empty(1, dtype=torch.int32, device=dev)
     loads = torch.empty(G, dtype=torch.int32, device=dev)
-    _lib.call("hm_schedule", _ptr(m_all), _ptr(home), G, E, int(q), int(bool(rebalance)), _ptr(S), _ptr(iters),
+    _lib.call("hm_schedule", _ptr(m_all), _ptr(home), G, E, int(q), _policy(rebalance), _ptr(S), _ptr(iters),
               _ptr(loads), _stream(stream))
     return S, iters, loads
 
@@ -100,7 +119,7 @@ def schedule_batched(m_all, home, q: int, rebalance: bool = True, stream=None):
     S = torch.empty((B, G, E, G), dtype=torch.int32, device=dev)
     iters = torch.empty(B, dtype=torch.int32, device=dev)
     loads = torch.empty((B, G), dtype=torch.int32, device=dev)
-    _lib.call("hm_schedule_batched", _ptr(m_all), _ptr(home), B, G, E, int(q), int(bool(rebalance)), _ptr(S),
+    _lib.call("hm_schedule_batched", _ptr(m_all), _ptr(home), B, G, E, int(q), _policy(rebalance), _ptr(S),
               _ptr(iters), _ptr(loads), _stream(stream))
     return S, iters, loads
 
@@ -168,7 +187,7 @@ def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, 
     lay = Layout(torch.empty((G, E, G), **i32), torch.empty((cap, 4), **i32), torch.empty(1, **i32),
                  torch.empty(cap + 1, **i32), torch.empty(E, **i32), torch.empty(1, **i32))
     _lib.call("hm_plan", _ptr(tile_hist), int(tiles_per_rank), _ptr(m_all), _ptr(home), G, E, int(q),
-              int(bool(rebalance)), int(mode), int(me), _ptr(m_out) if tile_hist is not None else None,
+              _policy(rebalance), int(mode), int(me), _ptr(m_out) if tile_hist is not None else None,
               _ptr(tile_off), _ptr(S), _ptr(iters), _ptr(loads), _ptr(lay.slot_base), _ptr(lay.segs),
               _ptr(lay.n_seg), _ptr(lay.mtile_prefix), _ptr(lay.fetch), _ptr(lay.n_fetch), _stream(stream))
     return Plan(m_out, tile_off, S, iters, loads, lay)

@@ -8,8 +8,10 @@ ScheduleTensor returned, ValueError on q < 1) but run ``hm_schedule`` /
 int32 conversion happens at this boundary.
 
 Placements and the Eq. 4 threshold are host-side closed forms, restated from
-policies.py:91-106 and 232-255.  The baseline policies even_split/affinity are
-out of scope for the hot path and raise NotImplementedError.
+policies.py:91-106 and 232-255.  The baseline policies of the paper's ablations
+ sit on the same seam: ``even_split_assign`` runs in the
+same GPU scheduler kernel (HM_POLICY_EVEN_SPLIT), ``affinity_placement`` is a
+host-side placement like round-robin/blocked (policies.py:206-229).
 """
 
 from __future__ import annotations
@@ -114,8 +116,65 @@ def rebalance(s_initial: ScheduleTensor, q: int) -> ScheduleTensor:
     return s
 
 
-def even_split_assign(m_all: RoutingMatrix, num_gpus: int) -> ScheduleTensor:  # pragma: no cover - out of scope
-    raise NotImplementedError("even_split is a baseline policy outside the HarMoEny hot path (SURVEY.md §2)")
+def even_split_assign(m_all: RoutingMatrix, num_gpus: int) -> ScheduleTensor:
+    """Each expert's pooled tokens split evenly over all GPUs (policies.py:174-203), on the GPU.
+
+    Remainder to the lowest-index GPUs; sources fill the per-GPU targets in index order."""
+    from . import ops
+
+    if num_gpus != m_all.num_gpus:
+        raise ValueError("num_gpus does not match routing matrix")
+    home = np.zeros(m_all.num_experts, np.int64)  # unused by the even split
+    S, _, _ = ops.schedule(_to_i32(m_all.counts, "even_split_assign"), _to_i32(home, "home"), 1,
+                           rebalance=ops.HM_POLICY_EVEN_SPLIT)
+    return ScheduleTensor(S.cpu().numpy().astype(np.int64))
+
+
+@dataclass(frozen=True)
+class PopularityProfile:
+    """Cumulative per-expert token counts over a profiling window (policies.py:68-88)."""
+
+    counts: np.ndarray
+    window_batches: int
+
+    def __post_init__(self):
+        arr = np.array(self.counts, dtype=np.int64, copy=True)
+        if arr.ndim != 1:
+            raise ValueError("profile counts must be one-dimensional")
+        if arr.size and arr.min() < 0:
+            raise ValueError("profile counts must be non-negative")
+        arr.setflags(write=False)
+        object.__setattr__(self, "counts", arr)
+        if self.window_batches < 0:
+            raise ValueError("window_batches must be >= 0")
+
+    @property
+    def num_experts(self) -> int:
+        return self.counts.shape[0]
+
+
+def affinity_placement(profile: PopularityProfile, num_gpus: int, slots: int) -> Placement:
+    """Greedy LPT packing by profiled popularity (policies.py:206-229).
+
+    Experts in descending popularity (ties: lower id first) go to the GPU with the least
+    accumulated mass that still has a free slot (ties: lower GPU index).  A stable sort plus a
+    running per-GPU (mass, index) minimum gives the reference's choice in O(E log E + E*G)."""
+    E = profile.num_experts
+    if E > num_gpus * slots:
+        raise ValueError(f"infeasible placement: {E} experts > {num_gpus} GPUs x {slots} slots")
+    counts = profile.counts
+    order = np.lexsort((np.arange(E), -counts))
+    mass = np.zeros(num_gpus, np.int64)
+    used = np.zeros(num_gpus, np.int64)
+    home = np.zeros(E, np.int64)
+    for e in order:
+        free = used < slots
+        masked = np.where(free, mass, np.iinfo(np.int64).max)
+        g = int(np.argmin(masked))  # first minimum = lowest index among equal masses
+        home[e] = g
+        mass[g] += int(counts[e])
+        used[g] += 1
+    return Placement(home=tuple(int(h) for h in home), num_gpus=num_gpus)
 
 
 def estimate_token_threshold(gpu_flops: float, dtype_bytes: float, pcie_bandwidth: float) -> int:

@@ -20,6 +20,9 @@ scheduler kernel are pinned to the reference, not to a restatement:
                         (workload.py:183-232), resampled alpha, 5 batches x 3 layers
 * trace_g4_e16_schedules.npz - the reference build_schedule (engine.py:287-299)
                         of every (batch, layer) of that trace, per placement and q
+* baseline_policies.npz - even_split_assign (policies.py:174-203) on the
+                        baseline-shape + acceptance matrices; affinity_placement
+                        (policies.py:206-229) on random popularity profiles
 
 The inputs are stored alongside the outputs, so the fixtures do not depend on
 numpy RNG stream stability.
@@ -195,10 +198,49 @@ def trace_files():
     return out
 
 
+def baseline_policies():
+    """The paper's ablation baselines on the same seam: the reference's
+    even_split_assign (policies.py:174-203) on every baseline-shape and acceptance routing
+    matrix, and affinity_placement (policies.py:206-229) on random popularity profiles."""
+    from moesim import PopularityProfile, affinity_placement, even_split_assign
+
+    out = []
+    for pack in (baseline_shapes(), acceptance_c2(400)):
+        off = 0
+        for G, E in zip(pack["G"], pack["E"]):
+            m = pack["m"][off:off + G * E].reshape(G, E)
+            off += G * E
+            S = even_split_assign(RoutingMatrix(m), int(G)).counts
+            out.append(dict(m=m, home=np.zeros(E, np.int64), q=1, S=S, iters=0))
+    d = _pack(out)
+    rng = np.random.default_rng(777)
+    E_l, G_l, slots_l, counts_l, home_l = [], [], [], [], []
+    for i in range(300):
+        E = int(rng.integers(1, 160))
+        G = int(rng.integers(1, 9))
+        slots = -(-E // G) + int(rng.integers(0, 4))
+        if i % 4 == 0:
+            counts = rng.integers(0, 5, size=E)  # many ties
+        else:
+            counts = (rng.zipf(1.3, size=E) * rng.integers(1, 100)).clip(max=10**9)
+        home = affinity_placement(PopularityProfile(counts=counts, window_batches=1), G, slots).home
+        E_l.append(E)
+        G_l.append(G)
+        slots_l.append(slots)
+        counts_l.append(np.asarray(counts, np.int64))
+        home_l.append(np.asarray(home, np.int64))
+    d.update(aff_E=np.array(E_l, np.int32), aff_G=np.array(G_l, np.int32), aff_slots=np.array(slots_l, np.int32),
+             aff_counts=np.concatenate(counts_l), aff_home=np.concatenate(home_l))
+    return d
+
+
 def main():
     print("moesim", moesim.__version__, "numpy", np.__version__)
     for name, fn in [("fig4", fig4), ("acceptance_c2", acceptance_c2), ("baseline_shapes", baseline_shapes),
-                     ("plan_order", plan_order), ("trace_g4_e16_schedules", trace_files)]:
+                     ("plan_order", plan_order), ("trace_g4_e16_schedules", trace_files),
+                     ("baseline_policies", baseline_policies)]:
+        if len(sys.argv) > 1 and name not in sys.argv[1:]:  # regenerate only the named fixtures
+            continue
         d = fn()
         path = os.path.join(HERE, name + ".npz")
         np.savez_compressed(path, **d)

@@ -67,6 +67,34 @@ def test_patch_moesim_simulate_run_identical():
         restore()
 
 
+@pytest.mark.parametrize("policy", ["EVEN_SPLIT", "AFFINITY"])
+def test_patch_moesim_baseline_policies_identical(policy):
+    """The ablation baselines through the patched seam (GPU even split, affinity placement)
+    reproduce the reference simulator's loads and latencies exactly (engine.py:292-293,435-440)."""
+    _cuda()
+    moesim = _moesim()
+    from paper_2506_12417_b200.integration import patch_moesim
+
+    model = moesim.model_preset("switch128")
+    cluster = moesim.ClusterSpec(num_gpus=4, expert_slots_per_gpu=40, link_bandwidth=2e11, link_latency=1e-6,
+                                 pcie_bandwidth=8e9, gpu_flops=1e12)
+    wl = moesim.WorkloadSpec(num_batches=4, tokens_per_gpu_per_batch=4096,
+                             skew=moesim.SkewSpec(alpha=0.8, skewed_experts=tuple(range(6))), seed=11)
+    trace = moesim.generate_trace(wl, model, cluster.num_gpus)
+    cfg = moesim.SchedulerConfig(token_threshold_q=32, policy=getattr(moesim.SchedulingPolicy, policy),
+                                 placement=moesim.PlacementKind.ROUND_ROBIN,
+                                 affinity_refresh_batches=2 if policy == "AFFINITY" else None)
+    ref = moesim.simulate_run(trace, model, cluster, cfg, moesim.SimFlags())
+    restore = patch_moesim(moesim)
+    try:
+        got = moesim.simulate_run(trace, model, cluster, cfg, moesim.SimFlags())
+    finally:
+        restore()
+    for a, b in zip(ref.per_gpu_token_loads, got.per_gpu_token_loads):
+        assert np.array_equal(a, b)
+    assert ref.per_batch_latency == got.per_batch_latency
+
+
 class _Expert(nn.Module):
     def __init__(self, d, f):
         super().__init__()

@@ -60,6 +60,29 @@ def test_schedule_kernel_bit_exact(golden, pack):
             break
 
 
+def test_even_split_kernel_bit_exact(golden):
+    """HM_POLICY_EVEN_SPLIT == the reference's even_split_assign (policies.py:174-203)."""
+    from paper_2506_12417_b200 import RoutingMatrix, even_split_assign, ops
+
+    dev = _cuda()
+    n = 0
+    for inst in iter_packed(golden("baseline_policies")):
+        m = torch.from_numpy(inst["m"].astype(np.int32)).to(dev)
+        home = torch.zeros(inst["m"].shape[1], dtype=torch.int32, device=dev)
+        S, iters, loads = ops.schedule(m, home, 1, rebalance=ops.HM_POLICY_EVEN_SPLIT)
+        assert np.array_equal(S.cpu().numpy(), inst["S"]), f"instance {inst['i']}"
+        assert int(iters.item()) == 0
+        assert np.array_equal(loads.cpu().numpy(), inst["S"].sum(axis=(0, 1)))
+        n += 1
+    assert n > 500
+    inst = next(iter_packed(golden("baseline_policies")))
+    assert np.array_equal(even_split_assign(RoutingMatrix(inst["m"]), inst["m"].shape[0]).counts, inst["S"])
+    with pytest.raises(ValueError):
+        even_split_assign(RoutingMatrix(inst["m"]), inst["m"].shape[0] + 1)
+    with pytest.raises(ValueError):
+        ops.schedule(m, home, 1, rebalance=7)
+
+
 def test_rebalance_dropin_api(golden):
     """The moesim-signature wrappers (policies.rebalance_with_stats) reproduce the reference."""
     _cuda()
@@ -184,14 +207,19 @@ def _segs_from_counts(counts, wslots, device):
 
 
 @pytest.mark.parametrize("epi", ["store", "relu", "swiglu"])
-@pytest.mark.parametrize("N,K", [(256, 64), (512, 768), (1536, 2048)])
-def test_grouped_gemm(epi, N, K):
+@pytest.mark.parametrize("N,K,counts", [
+    (256, 64, (1, 0, 300, 129, 64)),
+    (512, 768, (1, 0, 300, 129, 64)),
+    (1536, 2048, (1, 0, 300, 129, 64)),
+    # odd 128-row tile counts end in an M=128 half tile: exactly 128 / 64 / 65 / 63 rows in it
+    (512, 256, (128, 384, 65, 63, 640)),
+])
+def test_grouped_gemm(epi, N, K, counts):
     from paper_2506_12417_b200 import ops
 
     dev = _cuda()
     g = torch.Generator(device=dev).manual_seed(N + K)
     E = 5
-    counts = [1, 0, 300, 129, 64, 17][:E]
     wslots = [3, 1, 0, 4, 2][:E]
     lay, rows = _segs_from_counts(counts, wslots, dev)
     A = torch.randn((rows, K), device=dev, generator=g).to(torch.bfloat16)
@@ -307,14 +335,18 @@ def test_block_output_independent_of_schedule():
     shapes = dict(d_model=256, num_experts=32, d_ff=256, top_k=4, activation="swiglu")
     x = torch.randn((1024, 256), device=dev, generator=torch.Generator(device=dev).manual_seed(3)).to(torch.bfloat16)
     ys = []
-    for policy in ("harmony", "round_robin"):
+    for policy in ("harmony", "round_robin", "even_split"):
         cfg = MoEConfig(logical_ranks=4, eq_tokens=1, placement="blocked", scheduling_policy=policy, **shapes)
         blk = _block(cfg, seed=11, dev=dev, zipf_s=1.5)
         ys.append(bits(blk(x)))
         if policy == "harmony":
             assert blk.stats.load_imbalance() <= 1.1
             assert int(blk.stats.iters.item()) > 0
-    assert np.array_equal(ys[0], ys[1])
+        if policy == "even_split":  # every expert split over all 4 GPUs (policies.py:174-203)
+            S = blk.stats.schedule.cpu().numpy()
+            assert np.array_equal(S, orc.even_split(blk.stats.m_all.cpu().numpy()))
+            assert blk.stats.load_imbalance() <= 1.05  # +-1 token per expert and GPU
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
 
 
 def test_graph_capture_matches_eager():

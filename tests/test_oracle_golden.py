@@ -94,3 +94,42 @@ def test_bf16_roundtrip():
     assert orc.bf16_to_f32(b)[1] == 1.0  # tie to even
     assert orc.bf16_to_f32(b)[2] == 1.0078125
     assert orc.bf16_to_f32(b)[3] == -3.5
+
+
+def test_even_split_oracle_matches_reference(golden):
+    """even_split_assign (policies.py:174-203) restated in C == the reference's own output."""
+    n = 0
+    for inst in iter_packed(golden("baseline_policies")):
+        S = orc.even_split(inst["m"])
+        assert np.array_equal(S, inst["S"]), f"instance {inst['i']}"
+        assert np.array_equal(S.sum(axis=2), inst["m"])  # conservation per (source, expert)
+        n += 1
+    assert n > 500
+
+
+def _affinity_cases(d):
+    oc = 0
+    for E, G, slots in zip(d["aff_E"], d["aff_G"], d["aff_slots"]):
+        E = int(E)
+        yield d["aff_counts"][oc:oc + E], int(G), int(slots), d["aff_home"][oc:oc + E]
+        oc += E
+
+
+def test_affinity_matches_reference(golden):
+    """affinity_placement (policies.py:206-229): C oracle and the package's host placement."""
+    from paper_2506_12417_b200 import PopularityProfile, affinity_placement
+
+    d = golden("baseline_policies")
+    n = 0
+    for counts, G, slots, home in _affinity_cases(d):
+        assert np.array_equal(orc.affinity_home(counts, G, slots), home)
+        p = affinity_placement(PopularityProfile(counts=counts, window_batches=1), G, slots)
+        assert list(p.home) == home.tolist()
+        n += 1
+    assert n == 300
+    with pytest.raises(ValueError, match="infeasible placement"):
+        affinity_placement(PopularityProfile(counts=np.ones(5, np.int64), window_batches=1), 2, 2)
+    with pytest.raises(ValueError):
+        orc.affinity_home(np.ones(5, np.int64), 2, 2)
+    with pytest.raises(ValueError, match="non-negative"):
+        PopularityProfile(counts=np.array([1, -1]), window_batches=1)

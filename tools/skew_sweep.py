@@ -42,13 +42,13 @@ def main():
     x = torch.randn((T, d), device="cuda", generator=g).to(torch.bfloat16)
     for s in (0.0, 0.5, 1.0, 1.5):
         for G in (1, 2, 4, 8):
-            for policy in ("round_robin", "harmony"):
+            for policy in ("round_robin", "harmony", "even_split"):
                 cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q,
                                 logical_ranks=G, placement="blocked", scheduling_policy=policy)
                 blk = HarMoEnyBlock.random(cfg, seed=0, zipf_s=s)
                 ms = timed(lambda: blk(x))
                 loads = blk.stats.loads.double().cpu()
-                rec = dict(workload=name, zipf_s=s, G=G, rebalance=policy == "harmony", q=q,
+                rec = dict(workload=name, zipf_s=s, G=G, rebalance=policy == "harmony", policy=policy, q=q,
                            load_max_over_mean=round(float(loads.max() / loads.mean()), 4),
                            moves=int(blk.stats.iters.item()), block_ms_one_gpu=round(ms, 4),
                            tokens_per_s_one_gpu=round(T / ms * 1e3))
