@@ -334,11 +334,17 @@ struct PairCursor {
     seg = segs[s];
     const int ms = pair_tiles(s);
     const int local = t - base;
-    nb = local / ms;
-    m = local - nb * ms;
+    if (m_major) {  // the NB pairs that share an A tile run side by side; W stays L2-resident
+      m = local / NB;
+      nb = local - m * NB;
+    } else {  // consecutive pairs share a weight n-block
+      nb = local / ms;
+      m = local - nb * ms;
+    }
     hf = half_tiles && m == ms - 1 && ((mp[s + 1] - mp[s]) & 1);
   }
   bool half_tiles = true;
+  bool m_major = true;
 };
 
 // kGather: the A tile is not TMA-loaded from a permuted buffer but gathered straight from
@@ -366,7 +372,8 @@ template <int kEpi, bool kGather>
 __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kGemmThreads, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                              const __grid_constant__ CUtensorMap tmap_a64, const __grid_constant__ CUtensorMap tmap_b64,
-                             int half_tiles, const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
+                             int half_tiles /* bit0 half tiles, bit1 m-major walk */,
+                             const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
                              const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K,
                              int ldo, const int* __restrict__ row_map, const int* __restrict__ slot_ready,
                              int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     fence_mbar_init();
     if (!kGather) tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
-    if (half_tiles) {
+    if (half_tiles & 1) {
       if (!kGather) tma_prefetch_desc(&tmap_a64);
       if (kEpi == kEpiSwiGLU) tma_prefetch_desc(&tmap_b64);
     }
@@ -434,7 +441,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       const uint64_t pol_b = l2_policy_evict_last();
       const uint32_t full_leader = mapa_shared(full, 0);
       PairCursor cur{segs, mp, NB};
-      cur.half_tiles = half_tiles != 0;
+      cur.half_tiles = (half_tiles & 1) != 0;
+      cur.m_major = (half_tiles & 2) != 0;
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total; t += npairs) {
@@ -486,7 +494,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       constexpr uint32_t idesc_full = make_idesc_bf16(2 * kBM, kBN);
       constexpr uint32_t idesc_half = make_idesc_bf16(kBM, kBN);  // 64 rows per CTA, "2x2" TMEM layout
       PairCursor cur{segs, mp, NB};
-      cur.half_tiles = half_tiles != 0;
+      cur.half_tiles = (half_tiles & 1) != 0;
+      cur.m_major = (half_tiles & 2) != 0;
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
@@ -527,7 +536,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const int sub = lane >> 3;              // row within a group of 4
     const uint32_t full_leader = mapa_shared(full, 0);
     PairCursor cur{segs, mp, NB};
-    cur.half_tiles = half_tiles != 0;
+    cur.half_tiles = (half_tiles & 1) != 0;
+      cur.m_major = (half_tiles & 2) != 0;
     int stage = 0, sig_stage = 0, pending = 0;
     uint32_t phase = 0;
     for (int t = pair; t < total; t += npairs) {
@@ -587,7 +597,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const uint32_t my_srow = stg + lane * kStgPitch;
     const uint32_t tempty_leader = mapa_shared(tempty, 0);
     PairCursor cur{segs, mp, NB};
-    cur.half_tiles = half_tiles != 0;
+    cur.half_tiles = (half_tiles & 1) != 0;
+      cur.m_major = (half_tiles & 2) != 0;
     int i = 0;
     for (int t = pair; t < total; t += npairs, ++i) {
       int4 seg;
@@ -668,6 +679,15 @@ static bool use_half_tiles() {
   return v == 1;
 }
 
+static bool use_m_major() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HM_GEMM_NB_MAJOR");
+    v = (e != nullptr && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool use_2cta() {
   static int v = -1;
   if (v < 0) {
@@ -706,13 +726,13 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     rc = make_tmap_2d_bf16(&tb2, W, (uint64_t)w_rows, (uint64_t)K, kBN / 2, kBK);
     if (rc) return rc;
     // half tiles: 64-row A boxes, and 64-row B boxes for the re-paired SwiGLU weight halves
-    const int half_tiles = use_half_tiles() ? 1 : 0;
+    const int half_tiles = (use_half_tiles() ? 1 : 0) | (use_m_major() ? 2 : 0);  // tile-walk flags
     CUtensorMap ta64 = ta, tb64 = tb2;
-    if (half_tiles && a_gather == nullptr) {
+    if ((half_tiles & 1) && a_gather == nullptr) {
       rc = make_tmap_2d_bf16(&ta64, A, (uint64_t)a_rows, (uint64_t)K, kBM / 2, kBK);
       if (rc) return rc;
     }
-    if (half_tiles && epilogue == kEpiSwiGLU) {
+    if ((half_tiles & 1) && epilogue == kEpiSwiGLU) {
       rc = make_tmap_2d_bf16(&tb64, W, (uint64_t)w_rows, (uint64_t)K, kBN / 4, kBK);
       if (rc) return rc;
     }
