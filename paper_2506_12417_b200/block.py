@@ -281,11 +281,14 @@ class HarMoEnyBlock:
         self.home = torch.from_numpy(self.home_np).to(device)
         self.device = device
         self.stats = BlockStats()
-        # fused scatter (HM_FUSED_SCATTER=1): FFN1 gathers token rows itself with cp.async
-        # loader warps instead of a permuted copy.  Measured on B200 (Qwen-128, 16k tokens):
-        # +2.5% in short runs, -2% once the 1 kW power cap engages (the gather burns more
-        # power per FLOP), so the copy-permute stays the default.
-        self.fused_scatter = os.environ.get("HM_FUSED_SCATTER", "0") == "1"
+        # fused scatter: FFN1 gathers token rows itself with cp.async loader warps, so the
+        # k-fold replicated token buffer (T*k*d*2 bytes written, then read) never exists.  With
+        # the m-major pair-tile walk the NB pairs sharing an A tile gather the same rows side by
+        # side (L2 hits).  Measured on B200: Qwen-128 (top-8) +4.5% short / +3.7% power-capped;
+        # Switch-128 (top-1, HBM-bound FFN1) -31%, Mixtral (top-2) -2% -> on for top_k >= 4.
+        # HM_FUSED_SCATTER=0/1 overrides.
+        env = os.environ.get("HM_FUSED_SCATTER", "")
+        self.fused_scatter = (env == "1") if env in ("0", "1") else cfg.top_k >= 4
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s: float | None = None, std: float = 0.02):
