@@ -334,17 +334,19 @@ struct PairCursor {
     seg = segs[s];
     const int ms = pair_tiles(s);
     const int local = t - base;
-    if (m_major) {  // the NB pairs that share an A tile run side by side; W stays L2-resident
-      m = local / NB;
-      nb = local - m * NB;
-    } else {  // consecutive pairs share a weight n-block
-      nb = local / ms;
-      m = local - nb * ms;
-    }
+    // grouped rasterisation: groups of `gm` m-tiles; inside a group n-block-major, so the
+    // pairs running side by side cover a gm x (pairs/gm) rectangle of the segment's tiles.
+    // gm = 1: the NB pairs sharing an A tile run together and W stays L2-resident (small
+    // experts); gm ~ sqrt(pairs): fewest DRAM bytes per wave when W does not fit L2.
+    const int g = local / (gm * NB);
+    const int gsz = min(gm, ms - g * gm);
+    const int r = local - g * gm * NB;
+    nb = r / gsz;
+    m = g * gm + (r - nb * gsz);
     hf = half_tiles && m == ms - 1 && ((mp[s + 1] - mp[s]) & 1);
   }
   bool half_tiles = true;
-  bool m_major = true;
+  int gm = 1;
 };
 
 // kGather: the A tile is not TMA-loaded from a permuted buffer but gathered straight from
@@ -372,7 +374,7 @@ template <int kEpi, bool kGather>
 __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kGemmThreads, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                              const __grid_constant__ CUtensorMap tmap_a64, const __grid_constant__ CUtensorMap tmap_b64,
-                             int half_tiles /* bit0 half tiles, bit1 m-major walk */,
+                             int half_tiles /* bit0 half tiles, bits 1+: m-tile group of the walk */,
                              const int4* __restrict__ segs_g, const int* __restrict__ mprefix_g,
                              const int* __restrict__ n_seg_ptr, __nv_bfloat16* __restrict__ out, int N, int K,
                              int ldo, const int* __restrict__ row_map, const int* __restrict__ slot_ready,
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       const uint32_t full_leader = mapa_shared(full, 0);
       PairCursor cur{segs, mp, NB};
       cur.half_tiles = (half_tiles & 1) != 0;
-      cur.m_major = (half_tiles & 2) != 0;
+      cur.gm = max(1, half_tiles >> 1);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < total; t += npairs) {
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       constexpr uint32_t idesc_half = make_idesc_bf16(kBM, kBN);  // 64 rows per CTA, "2x2" TMEM layout
       PairCursor cur{segs, mp, NB};
       cur.half_tiles = (half_tiles & 1) != 0;
-      cur.m_major = (half_tiles & 2) != 0;
+      cur.gm = max(1, half_tiles >> 1);
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const uint32_t full_leader = mapa_shared(full, 0);
     PairCursor cur{segs, mp, NB};
     cur.half_tiles = (half_tiles & 1) != 0;
-      cur.m_major = (half_tiles & 2) != 0;
+      cur.gm = max(1, half_tiles >> 1);
     int stage = 0, sig_stage = 0, pending = 0;
     uint32_t phase = 0;
     for (int t = pair; t < total; t += npairs) {
@@ -598,7 +600,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const uint32_t tempty_leader = mapa_shared(tempty, 0);
     PairCursor cur{segs, mp, NB};
     cur.half_tiles = (half_tiles & 1) != 0;
-      cur.m_major = (half_tiles & 2) != 0;
+      cur.gm = max(1, half_tiles >> 1);
     int i = 0;
     for (int t = pair; t < total; t += npairs, ++i) {
       int4 seg;
@@ -679,13 +681,15 @@ static bool use_half_tiles() {
   return v == 1;
 }
 
-static bool use_m_major() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HM_GEMM_NB_MAJOR");
-    v = (e != nullptr && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
+// m-tile group of the pair-tile walk: 1 when a segment's weights (N x K bf16) fit easily
+// in L2 (they stay resident while the A tiles stream once: Qwen-128 / Switch-128, +2% FFN1
+// over the n-block-major walk), else 16 m-tiles per group (Mixtral 8x7B, 235 MB of W1 per
+// expert: 1.54 -> 1.72-1.80 Mtok/s vs gm = 1, best of the 1/4/8/16/24/32/64 sweep within
+// the power-cap noise).  HM_GEMM_GM overrides.
+static int walk_group(int N, int K) {
+  const char* e = getenv("HM_GEMM_GM");
+  if (e != nullptr && atoi(e) > 0) return atoi(e);
+  return ((size_t)N * K * 2 <= (size_t)24 << 20) ? 1 : 16;
 }
 
 static bool use_2cta() {
@@ -726,7 +730,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     rc = make_tmap_2d_bf16(&tb2, W, (uint64_t)w_rows, (uint64_t)K, kBN / 2, kBK);
     if (rc) return rc;
     // half tiles: 64-row A boxes, and 64-row B boxes for the re-paired SwiGLU weight halves
-    const int half_tiles = (use_half_tiles() ? 1 : 0) | (use_m_major() ? 2 : 0);  // tile-walk flags
+    const int half_tiles = (use_half_tiles() ? 1 : 0) | (walk_group(N, K) << 1);  // tile-walk flags
     CUtensorMap ta64 = ta, tb64 = tb2;
     if ((half_tiles & 1) && a_gather == nullptr) {
       rc = make_tmap_2d_bf16(&ta64, A, (uint64_t)a_rows, (uint64_t)K, kBM / 2, kBK);
