@@ -323,7 +323,7 @@ def expert_ffn(xe_f32, w1_bits, w2_bits, act: str, w3_bits=None):
     return round_bf16(y.astype(np.float32))
 
 
-def moe_block(x_bits, wg_bits, bias, w1_bits, w2_bits, k, act, renormalize, w3_bits=None):
+def moe_block(x_bits, wg_bits, bias, w1_bits, w2_bits, k, act, renormalize, w3_bits=None, return_scale=False):
     """Full single-rank block: router -> per-expert FFN -> weighted combine.
     The schedule never changes the math (each token row is computed by its
     expert's weights wherever it runs), so the oracle output is G-independent."""
@@ -343,4 +343,9 @@ def moe_block(x_bits, wg_bits, bias, w1_bits, w2_bits, k, act, renormalize, w3_b
     acc = np.zeros((T, d), np.float32)
     for j in range(k):
         acc = (acc + w[:, j : j + 1] * yk[:, j, :]).astype(np.float32)
+    if return_scale:
+        # sum_j w_j |Y_j|: the magnitude of the combined terms, the reference for an elementwise
+        # tolerance where the weighted sum cancels (each Y_j carries its own bf16 rounding)
+        scale = np.einsum("tk,tkd->td", np.abs(w), np.abs(yk)).astype(np.float32)
+        return f32_to_bf16(acc), idx, w, logits, scale
     return f32_to_bf16(acc), idx, w, logits
