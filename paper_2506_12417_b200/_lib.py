@@ -16,7 +16,8 @@ HM_EPI_STORE, HM_EPI_RELU, HM_EPI_SWIGLU = 0, 1, 2
 HM_LAYOUT_LOCAL, HM_LAYOUT_EP = 0, 1
 HM_POLICY_NONE, HM_POLICY_REBALANCE, HM_POLICY_EVEN_SPLIT = 0, 1, 2
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libharmoe.so")
+# HM_LIB_PATH: load a variant build of the same C ABI (kernel A/B experiments, tools/build_variant.sh)
+LIB_PATH = os.environ.get("HM_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libharmoe.so")
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int

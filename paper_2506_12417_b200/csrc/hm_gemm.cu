@@ -355,8 +355,16 @@ struct PairCursor {
 // scatter (K4) is never written.  Loader warps fence the generic-proxy writes for the
 // tensor core (fence.proxy.async) and arrive on the leader's full barrier, which then
 // counts 1 (B expect_tx) + 8 (4 loader warps x 2 CTAs) arrivals.
-constexpr int kALoadWarps = 4;
-constexpr int kALookahead = 2;  // cp.async groups in flight per loader thread (4 measured slower)
+#ifndef HM_ALOAD_WARPS
+#define HM_ALOAD_WARPS 4
+#endif
+#ifndef HM_ALOOKAHEAD
+#define HM_ALOOKAHEAD 2
+#endif
+constexpr int kALoadWarps = HM_ALOAD_WARPS;  // 4 or 8
+constexpr int kALookahead = HM_ALOOKAHEAD;   // cp.async groups in flight per loader thread
+constexpr int kARowsPerWarp = 128 / kALoadWarps;
+constexpr int kARowsPerLane = kARowsPerWarp / 4;
 
 __device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(src) : "memory");
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     // ===== A-loaders (gather mode): loader warp lw fills tile rows [32lw, 32lw+32); 8 lanes
     // copy one row's 128-byte k-block segment (16 B each), so every cp.async instruction
     // moves 4 whole rows = 4 full cache lines =====
-    const int lw = warp - (2 + kEpiWarps);  // 0..3
+    const int lw = warp - (2 + kEpiWarps);  // 0..kALoadWarps-1
     const int c = lane & 7;                 // 16-byte chunk of the row segment
     const int sub = lane >> 3;              // row within a group of 4
     const uint32_t full_leader = mapa_shared(full, 0);
@@ -550,10 +558,10 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       const int cta_rows = hf ? kBM / 2 : kBM;
       const int rows = max(0, min(cta_rows, seg.y - m * 2 * kBM - (int)rank * cta_rows));
       const int rbase = seg.x + m * 2 * kBM + (int)rank * cta_rows;
-      const char* src[8];
+      const char* src[kARowsPerLane];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = lw * 32 + i * 4 + sub;
+      for (int i = 0; i < kARowsPerLane; ++i) {
+        const int r = lw * kARowsPerWarp + i * 4 + sub;
         int src_row = 0;  // rows past the segment read any valid row (results never stored)
         if (r < rows) src_row = min(__ldg(a_gather + rbase + r) / a_gather_div, a_src_rows - 1);
         src[i] = reinterpret_cast<const char*>(a_src + (int64_t)src_row * K) + c * 16;
@@ -562,8 +570,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t dst = smem_u32(smem + stage * 2 * k2Half);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = lw * 32 + i * 4 + sub;
+        for (int i = 0; i < kARowsPerLane; ++i) {
+          const int r = lw * kARowsPerWarp + i * 4 + sub;
           if (r < cta_rows) cp_async16(dst + r * 128 + ((c ^ (r & 7)) << 4), src[i] + kb * 128);
         }
         cp_async_commit();
