@@ -228,15 +228,29 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def use_all_cores():
+    """Give the CPU arm every host core this process may run on: torchrun sets
+    OMP_NUM_THREADS=1 per rank, which would leave OpenBLAS single-threaded.  Returns the
+    BLAS thread count actually in effect (the `cores` the CPU numbers are quoted on)."""
+    n = cpu_cores()
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+
+        threadpool_limits(limits=n)
+        return max([int(i.get("num_threads", 1)) for i in threadpool_info()] or [1])
+    except Exception:  # noqa: BLE001 - no threadpoolctl: report what the env allows
+        return int(os.environ.get("OMP_NUM_THREADS", n))
+
+
 def run_reference(args, rank, world):
     wl = WORKLOADS[args.workload]
     if rank != 0:
         return
     sample = 256
+    cores = use_all_cores()
     times = cpu_measure(wl, sample, steps=args.steps, warmup=args.warmup, zipf_s=args.zipf, q=args.q)
     per_step = float(np.mean(times))
     value = sample / per_step
-    cores = cpu_cores()
     line = {
         "impl": "reference", "metric": "moe_block_tokens_per_sec", "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
@@ -438,8 +452,9 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     if not args.no_cpu_baseline:
         sample = 256
+        cores = use_all_cores()
         times = cpu_measure(wl, sample, seconds=args.cpu_seconds, zipf_s=args.zipf, q=args.q)
-        cpu = {"value": sample / float(np.mean(times)), "unit": "tokens/s", "cores": cpu_cores(), "kind": "port",
+        cpu = {"value": sample / float(np.mean(times)), "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": f"{sample}-token slices of the {args.workload} batch, {len(times)} reps "
                          f"(~{args.cpu_seconds:.0f}s; numpy/OpenBLAS restatement + C scheduler oracle)"}
     line = {
