@@ -34,7 +34,15 @@ from .policies import (
 )
 from .costmodel import MeasuredCostModel
 from .trace import Trace, TraceBatch, TraceParseError, read_trace, write_trace
-from .workload import skew_probabilities, zipf_probabilities, zipf_routing_matrix
+from .workload import (
+    SkewSpec,
+    WorkloadSpec,
+    generate_trace,
+    sample_routing,
+    skew_probabilities,
+    zipf_probabilities,
+    zipf_routing_matrix,
+)
 
 __version__ = "0.1.0"
 
@@ -58,5 +66,6 @@ __all__ = [
     "SchedulingPolicy", "blocked_placement", "estimate_token_threshold", "initial_assign", "rebalance",
     "rebalance_with_stats", "round_robin_placement", "threshold_bound", "skew_probabilities",
     "zipf_probabilities", "zipf_routing_matrix", "HarMoEnyBlock", "MoEConfig", "BlockStats", "replace_moe_layer",
-    "HarMoEnyLayer", "MeasuredCostModel", "PopularityProfile", "affinity_placement", "even_split_assign", "Trace", "TraceBatch", "TraceParseError", "read_trace", "write_trace",
+    "HarMoEnyLayer", "MeasuredCostModel", "PopularityProfile", "affinity_placement", "even_split_assign",
+    "SkewSpec", "WorkloadSpec", "generate_trace", "sample_routing", "Trace", "TraceBatch", "TraceParseError", "read_trace", "write_trace",
 ]

@@ -126,3 +126,92 @@ def calibrated_router_bias(num_experts: int, s: float, k: int, noise_std: float 
         b += step * (lt - np.log(np.maximum(f, 1e-6)))
         b -= b.max()
     return best.astype(np.float32)
+
+
+# ------------------------------------------------------------------------------------------
+# The reference's workload API (moesim/workload.py:40-210): skew specs, the per-source
+# multinomial sampler and trace generation.  Same validation, same RNG call sequence
+# (PCG64, one uniform per batch when resampling, one multinomial per layer), so for one
+# numpy build the traces are identical to the reference's (pinned in tests/test_trace.py
+# against tests/golden/trace_g4_e16.jsonl, which the reference itself wrote).  These
+# produce count matrices for scheduler-only runs and trace replay; the MoE block's own
+# routing comes from the router kernel.
+# ------------------------------------------------------------------------------------------
+MODE_FIXED = "fixed"
+MODE_RESAMPLE_UNIFORM = "resample_uniform"
+
+
+from dataclasses import dataclass  # noqa: E402
+
+
+@dataclass(frozen=True)
+class SkewSpec:
+    """Expert-popularity skew (workload.py:40-67): mass ``alpha`` on ``skewed_experts``,
+    constant or redrawn per batch from U[resample_lo, resample_hi]."""
+
+    alpha: float
+    skewed_experts: tuple = (0,)
+    mode: str = MODE_FIXED
+    resample_lo: float = 0.0
+    resample_hi: float = 0.0
+
+    def __post_init__(self):
+        object.__setattr__(self, "skewed_experts", tuple(int(e) for e in self.skewed_experts))
+        if not 0.0 <= self.alpha <= 1.0:
+            raise ValueError(f"alpha must be in [0, 1], got {self.alpha}")
+        if self.mode not in (MODE_FIXED, MODE_RESAMPLE_UNIFORM):
+            raise ValueError(f"unknown per-batch mode {self.mode!r}")
+        if not 0.0 <= self.resample_lo <= self.resample_hi <= 1.0:
+            raise ValueError("resample bounds must satisfy 0 <= lo <= hi <= 1")
+        if len(set(self.skewed_experts)) != len(self.skewed_experts):
+            raise ValueError("skewed expert indices must be distinct")
+        if any(e < 0 for e in self.skewed_experts):
+            raise ValueError("skewed expert indices must be non-negative")
+        max_alpha = self.resample_hi if self.mode == MODE_RESAMPLE_UNIFORM else self.alpha
+        if max_alpha > 0 and not self.skewed_experts:
+            raise ValueError("skewed_experts must be non-empty when alpha can exceed 0")
+
+
+@dataclass(frozen=True)
+class WorkloadSpec:
+    """One synthetic experiment (workload.py:70-82)."""
+
+    num_batches: int
+    tokens_per_gpu_per_batch: int
+    skew: SkewSpec
+    seed: int
+
+    def __post_init__(self):
+        if self.num_batches < 1:
+            raise ValueError("num_batches must be >= 1")
+        if self.tokens_per_gpu_per_batch < 1:
+            raise ValueError("tokens_per_gpu_per_batch must be >= 1")
+
+
+def sample_routing(probs, tokens_per_gpu: int, num_gpus: int, rng: np.random.Generator):
+    """One routing matrix, each source row an independent multinomial (workload.py:167-180)."""
+    from .core import RoutingMatrix
+
+    probs = np.asarray(probs, dtype=np.float64)
+    total = probs.sum()
+    if abs(total - 1.0) > 1e-9:
+        raise ValueError(f"probabilities must sum to 1, got {total}")
+    return RoutingMatrix(rng.multinomial(tokens_per_gpu, probs / total, size=num_gpus))
+
+
+def generate_trace(spec: WorkloadSpec, model, num_gpus: int):
+    """num_batches x num_layers routing matrices (workload.py:183-210), layers independent."""
+    from .trace import Trace, TraceBatch
+
+    rng = np.random.Generator(np.random.PCG64(spec.seed))
+    batches = []
+    for b in range(spec.num_batches):
+        if spec.skew.mode == MODE_RESAMPLE_UNIFORM:
+            alpha = float(rng.uniform(spec.skew.resample_lo, spec.skew.resample_hi))
+        else:
+            alpha = spec.skew.alpha
+        probs = skew_probabilities(alpha, spec.skew.skewed_experts, model.num_experts)
+        layers = [sample_routing(probs, spec.tokens_per_gpu_per_batch, num_gpus, rng) for _ in range(model.num_layers)]
+        batches.append(TraceBatch(batch_id=b, alpha=alpha, layers=layers))
+    return Trace(num_gpus=num_gpus, num_experts=model.num_experts, num_layers=model.num_layers, seed=spec.seed,
+                 batches=batches)

@@ -140,3 +140,43 @@ def test_oracle_schedules_trace_like_reference(golden):
             for i in range(m.shape[0]):
                 S, _ = orc.schedule(m[i], ref[f"home_{pl}"], q, rebalance=True)
                 assert np.array_equal(S, want[i]), (pl, q, i)
+
+
+def test_generate_trace_reproduces_reference_file(tmp_path):
+    """generate_trace / sample_routing / SkewSpec / WorkloadSpec (workload.py:40-210): the spec
+    make_golden.py handed the reference reproduces the reference-written file byte for byte
+    (same numpy build; cross-version RNG stability is not promised)."""
+    from paper_2506_12417_b200 import ModelSpec, SkewSpec, WorkloadSpec, generate_trace
+
+    model = ModelSpec(num_layers=3, num_experts=16, d_model=64, d_ff=128, dtype_bytes=2)
+    spec = WorkloadSpec(num_batches=5, tokens_per_gpu_per_batch=700,
+                        skew=SkewSpec(alpha=0.0, skewed_experts=(0, 5), mode="resample_uniform",
+                                      resample_lo=0.3, resample_hi=0.95), seed=7)
+    t = generate_trace(spec, model, num_gpus=4)
+    ref = read_trace(REF_TRACE)
+    if t != ref:
+        pytest.skip(f"numpy {np.__version__} draws a different PCG64 multinomial stream than the fixture's build")
+    out = tmp_path / "g.jsonl"
+    write_trace(t, out)
+    assert out.read_bytes() == open(REF_TRACE, "rb").read()
+
+
+def test_workload_spec_validation():
+    from paper_2506_12417_b200 import RoutingMatrix, SkewSpec, WorkloadSpec, sample_routing
+
+    with pytest.raises(ValueError, match="alpha"):
+        SkewSpec(alpha=1.5)
+    with pytest.raises(ValueError, match="unknown per-batch mode"):
+        SkewSpec(alpha=0.5, mode="nope")
+    with pytest.raises(ValueError, match="resample bounds"):
+        SkewSpec(alpha=0.0, mode="resample_uniform", resample_lo=0.9, resample_hi=0.1)
+    with pytest.raises(ValueError, match="distinct"):
+        SkewSpec(alpha=0.5, skewed_experts=(1, 1))
+    with pytest.raises(ValueError, match="non-empty"):
+        SkewSpec(alpha=0.5, skewed_experts=())
+    with pytest.raises(ValueError, match="num_batches"):
+        WorkloadSpec(num_batches=0, tokens_per_gpu_per_batch=1, skew=SkewSpec(alpha=0.0), seed=0)
+    with pytest.raises(ValueError, match="sum to 1"):
+        sample_routing(np.array([0.5, 0.6]), 10, 2, np.random.default_rng(0))
+    m = sample_routing(np.array([0.25, 0.75]), 10, 3, np.random.default_rng(0))
+    assert isinstance(m, RoutingMatrix) and m.counts.shape == (3, 2) and (m.counts.sum(axis=1) == 10).all()
