@@ -547,25 +547,36 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     const uint32_t full_leader = mapa_shared(full, 0);
     PairCursor cur{segs, mp, NB};
     cur.half_tiles = (half_tiles & 1) != 0;
-      cur.gm = max(1, half_tiles >> 1);
-    int stage = 0, sig_stage = 0, pending = 0;
-    uint32_t phase = 0;
-    for (int t = pair; t < total; t += npairs) {
-      int4 seg;
-      int m, nb;
-      bool hf;
-      cur.seek(t, seg, m, nb, hf);
-      const int cta_rows = hf ? kBM / 2 : kBM;
-      const int rows = max(0, min(cta_rows, seg.y - m * 2 * kBM - (int)rank * cta_rows));
-      const int rbase = seg.x + m * 2 * kBM + (int)rank * cta_rows;
-      const char* src[kARowsPerLane];
+    cur.gm = max(1, half_tiles >> 1);
+    // the gather indices of a tile are loaded one tile ahead (software pipelined), so the
+    // dependent index -> row address chain never stalls the first k-block of a tile
+    auto tile_rows = [&](int tt, int& cta_rows, int (&gidx)[kARowsPerLane]) {
+      int4 sg;
+      int mm, nbb;
+      bool hff;
+      cur.seek(tt, sg, mm, nbb, hff);
+      cta_rows = hff ? kBM / 2 : kBM;
+      const int rows = max(0, min(cta_rows, sg.y - mm * 2 * kBM - (int)rank * cta_rows));
+      const int rbase = sg.x + mm * 2 * kBM + (int)rank * cta_rows;
 #pragma unroll
       for (int i = 0; i < kARowsPerLane; ++i) {
         const int r = lw * kARowsPerWarp + i * 4 + sub;
-        int src_row = 0;  // rows past the segment read any valid row (results never stored)
-        if (r < rows) src_row = min(__ldg(a_gather + rbase + r) / a_gather_div, a_src_rows - 1);
+        gidx[i] = r < rows ? __ldg(a_gather + rbase + r) : 0;  // rows past the segment: any valid row
+      }
+    };
+    int stage = 0, sig_stage = 0, pending = 0;
+    uint32_t phase = 0;
+    int cta_rows_nx = 0, gidx_nx[kARowsPerLane];
+    if (pair < total) tile_rows(pair, cta_rows_nx, gidx_nx);
+    for (int t = pair; t < total; t += npairs) {
+      const int cta_rows = cta_rows_nx;
+      const char* src[kARowsPerLane];
+#pragma unroll
+      for (int i = 0; i < kARowsPerLane; ++i) {
+        const int src_row = min(gidx_nx[i] / a_gather_div, a_src_rows - 1);
         src[i] = reinterpret_cast<const char*>(a_src + (int64_t)src_row * K) + c * 16;
       }
+      if (t + npairs < total) tile_rows(t + npairs, cta_rows_nx, gidx_nx);
       for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t dst = smem_u32(smem + stage * 2 * k2Half);
