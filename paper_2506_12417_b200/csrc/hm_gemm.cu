@@ -655,15 +655,28 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16);
+      // the TMEM load of chunk c+1 is in flight while chunk c is stored, and the accumulator
+      // is handed back to the MMA issuer as soon as its last columns are in registers (before
+      // the last chunk's global stores)
+      uint32_t a[32], u[32];
+      tmem_ld_32x32b_x32(taddr + tcol0, a);
+      if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + upoff + tcol0, u);
 #pragma unroll 1
       for (int c0 = 0; c0 < ncols; c0 += kStgCols) {
-        uint32_t a[32], u[32];
-        const int col = tcol0 + c0;
-        tmem_ld_32x32b_x32(taddr + col, a);
-        if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + upoff + col, u);
         tmem_ld_wait();
+        const bool last = c0 + kStgCols >= ncols;
+        if (last) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+        }
         stage_row<kEpi>(my_srow, a, u);
         __syncwarp();
+        if (!last) {
+          const int col = tcol0 + c0 + kStgCols;
+          tmem_ld_32x32b_x32(taddr + col, a);
+          if constexpr (kEpi == kEpiSwiGLU) tmem_ld_32x32b_x32(taddr + upoff + col, u);
+        }
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + (lane >> 2);
@@ -676,9 +689,6 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         }
         __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
     }
   }
 
