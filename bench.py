@@ -49,8 +49,12 @@ def parse():
     ap.add_argument("--workload", default="qwen128", choices=sorted(WORKLOADS))
     ap.add_argument("--layers", type=int, default=1, help="MoE decoder layers per step (BASELINE config 4)")
     ap.add_argument("--zipf", type=float, default=1.0)
-    ap.add_argument("--q", type=int, default=32)
+    ap.add_argument("--q", type=int, default=None,
+                    help="token threshold q; default 32, 4 for switch128 (buckets of a few dozen tokens)")
     ap.add_argument("--placement", default="round_robin")
+    ap.add_argument("--logical-ranks", type=int, default=None,
+                    help="N=1: simulate G GPUs in one process (HarMoEny schedule over G logical ranks); "
+                         "default 4 for switch128 (BASELINE configs[0]: 'simulated 4 GPUs'), else 1")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -64,7 +68,10 @@ def parse():
                     help="token chunks of the pinned-host pipeline (H2D / compute / D2H overlap) for e2e")
     ap.add_argument("--kernel-table", action="store_true",
                     help="print per-kernel CUDA times from torch.profiler (CUPTI) for a few steps and exit")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.q is None:
+        args.q = 4 if args.workload == "switch128" else 32
+    return args
 
 
 def kernel_table(blk, x, steps=5):
@@ -285,6 +292,12 @@ def algorithmic_work(wl, tokens, active_experts=None):
     return f1, f2, w_bytes, act_bytes, g1_bytes
 
 
+def logical_ranks(args) -> int:
+    if args.logical_ranks is not None:
+        return max(1, args.logical_ranks)
+    return 4 if args.workload == "switch128" else 1
+
+
 def load_ratio_logical(block_cls, cfg_kw, x, G, q, placement, zipf_s, seed, dev):
     """max/mean load of HarMoEny's schedule when the same batch is split over G ranks."""
     from paper_2506_12417_b200.block import MoEConfig
@@ -316,7 +329,7 @@ def run_ours(args, rank, world, local_rank):
                         transport=args.transport, max_tokens_per_rank=T_total // world, **cfg_kw)
         blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
     else:
-        cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, **cfg_kw)
+        cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, logical_ranks=logical_ranks(args), **cfg_kw)
         blk = HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
     if args.layers > 1:  # BASELINE config 4: decoder stack, one step = all layers
         from paper_2506_12417_b200.stack import MoEStack
@@ -472,7 +485,9 @@ def run_ours(args, rank, world, local_rank):
                          f", {T_total} tokens, calibrated Zipf s={args.zipf} routing, random-init weights"),
             "layers": args.layers,
             "d_model": d, "d_ff": f, "experts": E, "top_k": k, "activation": act, "tokens": T_total,
-            "q": args.q, "placement": args.placement, "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+            "q": args.q, "placement": args.placement, "parallelism": f"ep{world}" if world > 1 else (
+                "single-gpu" if logical_ranks(args) == 1 else f"single-gpu, {logical_ranks(args)} simulated GPUs"),
+            "logical_ranks": logical_ranks(args) if world == 1 else None,
             "transport": (f"{args.transport}" + (" (CUDA graphs)" if ep_graph else " (eager)")) if world > 1 else None,
             "l2": "flushed between timed steps (256 MB write)",
             "stages_us": stage_us,
