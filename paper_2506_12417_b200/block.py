@@ -78,6 +78,14 @@ class MoEConfig:
             raise ValueError("max_tokens_per_rank must be >= 1")
         if self.activation not in ("swiglu", "relu"):
             raise ValueError("activation must be 'swiglu' or 'relu'")
+        # grouped-GEMM tiling (256-wide n-blocks, 64-deep k-blocks): FFN1 N = d_ff (ReLU) or
+        # 2*d_ff (SwiGLU), FFN2 N = d_model; K = d_model / d_ff.  Every BASELINE shape fits.
+        n_in = self.d_ff if self.activation == "relu" else 2 * self.d_ff
+        if self.d_model % 256 or n_in % 256 or self.d_ff % 64:
+            raise ValueError("d_model must be a multiple of 256 and d_ff a multiple of "
+                             f"{256 if self.activation == 'relu' else 128} (grouped-GEMM tiles)")
+        if not 1 <= self.top_k <= self.num_experts:
+            raise ValueError("top_k must be in [1, num_experts]")
         if self.renormalize is None:
             self.renormalize = self.top_k > 1
         if self.world_size > 1 and self.logical_ranks not in (1, self.world_size):
@@ -311,6 +319,13 @@ class HarMoEnyBlock:
         T = x.shape[0]
         if T % G != 0:
             raise ValueError("token count must divide evenly over the logical ranks")
+        if T == 0:  # empty batch: empty output, all-zero routing matrix / schedule (no kernels)
+            i32 = dict(dtype=torch.int32, device=x.device)
+            E = cfg.num_experts
+            self.stats = BlockStats(m_all=torch.zeros((G, E), **i32), schedule=torch.zeros((G, E, G), **i32),
+                                    iters=torch.zeros(1, **i32), loads=torch.zeros(G, **i32),
+                                    extras=dict(topk_idx=torch.zeros((0, cfg.top_k), **i32)))
+            return torch.empty((0, cfg.d_model), dtype=torch.bfloat16, device=x.device)
         s = stream if stream is not None else torch.cuda.current_stream()
         st = {"x": x.contiguous()}
 

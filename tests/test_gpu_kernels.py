@@ -445,3 +445,48 @@ def test_dispatch_positions_follow_contract():
         dest, rank = orc.dispatch_ranks(idx[g * Tg:(g + 1) * Tg], S, g)
         p = pos[g * Tg:(g + 1) * Tg].reshape(-1)
         assert np.all(p >= base[dest]) and np.all(p < base[dest + 1])
+
+
+@pytest.mark.parametrize("T,G,E,k,act", [(1, 1, 16, 2, "swiglu"), (3, 1, 16, 4, "swiglu"), (130, 2, 16, 2, "swiglu"),
+                                         (8, 4, 8, 8, "swiglu"), (257, 1, 60, 4, "relu"), (0, 1, 16, 2, "swiglu")])
+def test_block_ragged_and_tiny_batches(T, G, E, k, act):
+    """Edge cases the reference's count model allows (zero tokens, fewer tokens than a tile,
+    ragged last tiles, k = E, E not a multiple of 16): output matches the oracle, S conserves."""
+    from paper_2506_12417_b200.block import MoEConfig
+
+    dev = _cuda()
+    cfg = MoEConfig(logical_ranks=G, eq_tokens=1, placement="blocked", d_model=256, num_experts=E, d_ff=256,
+                    top_k=k, activation=act)
+    blk = _block(cfg, seed=T + 1, dev=dev)
+    x = torch.randn((T, 256), device=dev, generator=torch.Generator(device=dev).manual_seed(T)).to(torch.bfloat16)
+    y = blk(x)
+    torch.cuda.synchronize()
+    assert tuple(y.shape) == (T, 256)
+    m_all = blk.stats.m_all.cpu().numpy()
+    assert m_all.sum() == T * k
+    assert np.array_equal(blk.stats.schedule.cpu().numpy().sum(axis=2), m_all)
+    if T == 0:
+        return
+    wg = bits(blk.wg[:E])
+    f = 256
+    if act == "swiglu":
+        w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, 256)
+        w1, w3 = w13[:, :, 0].reshape(E, f, 256), w13[:, :, 1].reshape(E, f, 256)
+    else:
+        w1, w3 = bits(blk.w_in).reshape(E, f, 256), None
+    w2 = bits(blk.w_out).reshape(E, 256, f)
+    y_ref, idx_ref, _, _ = orc.moe_block(bits(x), wg, blk.bias.cpu().numpy(), w1, w2, k, act, cfg.renormalize, w3)
+    ok = np.all(blk.stats.extras["topk_idx"].cpu().numpy() == idx_ref, axis=1)
+    assert ok.mean() >= 0.9
+    assert_close(orc.bf16_to_f32(bits(y))[ok], orc.bf16_to_f32(y_ref)[ok], f"T={T} G={G} E={E} k={k}")
+
+
+def test_config_rejects_untileable_shapes():
+    from paper_2506_12417_b200.block import MoEConfig
+
+    with pytest.raises(ValueError, match="multiple of 256"):
+        MoEConfig(d_model=128, d_ff=256, num_experts=8, top_k=2)
+    with pytest.raises(ValueError, match="multiple of 256"):
+        MoEConfig(d_model=256, d_ff=128, num_experts=8, top_k=1, activation="relu")
+    with pytest.raises(ValueError, match="top_k"):
+        MoEConfig(d_model=256, d_ff=256, num_experts=4, top_k=5)
