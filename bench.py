@@ -64,13 +64,17 @@ def parse():
                          "all_to_all (host round trip per layer for the split sizes)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = test harness for the multi-rank path on fewer GPUs (not a measurement)")
-    ap.add_argument("--e2e-chunks", type=int, default=2,
-                    help="token chunks of the pinned-host pipeline (H2D / compute / D2H overlap) for e2e")
+    ap.add_argument("--e2e-chunks", type=int, default=None,
+                    help="token chunks of the pinned-host pipeline (H2D / compute / D2H overlap) for e2e; "
+                         "default 2 for qwen128 (64 MB each way per step), 1 for the weight-bound "
+                         "switch128 / mixtral8 (a chunk re-reads every expert's weights)")
     ap.add_argument("--kernel-table", action="store_true",
                     help="print per-kernel CUDA times from torch.profiler (CUPTI) for a few steps and exit")
     args = ap.parse_args()
     if args.q is None:
         args.q = 4 if args.workload == "switch128" else 32
+    if args.e2e_chunks is None:
+        args.e2e_chunks = 2 if args.workload == "qwen128" else 1
     return args
 
 
@@ -292,6 +296,12 @@ def algorithmic_work(wl, tokens, active_experts=None):
     return f1, f2, w_bytes, act_bytes, g1_bytes
 
 
+def uses_gather(blk) -> bool:
+    """Does FFN1 gather its rows from x (fused scatter) in this block / the stack's layers?"""
+    first = blk.layers[0] if hasattr(blk, "layers") else blk
+    return bool(getattr(first, "fused_scatter", False))
+
+
 def logical_ranks(args) -> int:
     if args.logical_ranks is not None:
         return max(1, args.logical_ranks)
@@ -499,14 +509,17 @@ def run_ours(args, rank, world, local_rank):
         },
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"grouped_gemm_2cta_kernel<{'SwiGLU' if act == 'swiglu' else 'ReLU'}> (expert FFN1)",
+                     "kernel": (f"grouped_gemm_2cta_kernel<{'SwiGLU' if act == 'swiglu' else 'ReLU'}, "
+                                f"{'cp.async gather of x rows' if uses_gather(blk) else 'TMA'}> "
+                                f"(expert FFN1)"),
                      "work_per_launch": work_desc,
                      "peak_source": f"MEASURED_PEAKS.json ({peak_kind}; bf16 {peak_src}; burst {tc}, "
                                     f"sustained {tc_sus} TFLOP/s; HBM {hbm} GB/s)"},
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                "path": (f"HarMoEnyBlock.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, block, "
-                         f"HBM -> pinned y; copies overlapped with compute by token chunks")
-                if graphed and args.e2e_chunks > 1 else "forward_host (pinned H2D -> block -> D2H)"},
+                "path": (f"{type(blk).__name__}.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, "
+                         f"block, HBM -> pinned y; copies overlapped with compute across token chunks and "
+                         f"successive steps (ping-pong buffers)")
+                if graphed and args.e2e_chunks >= 1 else "forward_host (pinned H2D -> block -> D2H)"},
         "gpu_launches": blk.KERNELS_PER_FORWARD * args.steps,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
