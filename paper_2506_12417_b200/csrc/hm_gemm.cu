@@ -2,27 +2,28 @@
 //
 // Replaces the expert-compute phase the reference only models
 // (moesim/engine.py:128-132 CostModel.expert_flops, engine.py:354-359 per-GPU
-// execution; Alg.1 step 5).  One persistent CTA per SM walks a
-// device-resident tile list built by hm_dispatch_layout (no host sync):
+// execution; Alg.1 step 5).  Persistent CTAs walk a device-resident
+// tile list built by hm_dispatch_layout (no host sync):
 //
 //   segment s = {row_start, nrows, wslot, expert}: rows [row_start, row_start+nrows)
 //   of the token buffer A are multiplied by weight slot `wslot` (W[wslot] is
-//   [N, K] K-major, i.e. nn.Linear layout).  Tiles are 128 rows x 256 columns;
-//   within a segment the order is n-block-major so consecutive CTAs share the
-//   A rows in L2; segments come in HarMoEny plan order (engine.py:233-234:
-//   residents first, then fetched experts) so async weight fetches (K6) get the
-//   longest possible compute shadow.
+//   [N, K] K-major, i.e. nn.Linear layout).  Segments come in HarMoEny plan order
+//   (engine.py:233-234: residents first, then fetched experts) so async weight fetches
+//   (K6) get the longest possible compute shadow.
 //
-// Warp roles (320 threads): warp0 = TMA producer, warp1 = MMA issuer (one
-// elected thread) + TMEM owner, warps2-9 = epilogue.  4-stage smem ring
-// (48 KB/stage); 2 TMEM accumulators of 256 fp32 columns so the epilogue of
-// tile i overlaps the MMAs of tile i+1.
+// Two kernels share the epilogue design:
+// * grouped_gemm_2cta_kernel (default): CTA pairs (cluster of 2, tcgen05.mma.cta_group::2)
+//   on 256 x 256 pair tiles; a segment's odd 128-row tail runs as an M=128 "half" tile;
+//   the tile walk is m-major (or grouped by 16 m-tiles for experts whose weights do not fit
+//   L2); A comes by TMA or, for the fused scatter, from cp.async loader warps that gather
+//   token rows of x directly.  Described in detail above the kernel.
+// * grouped_gemm_kernel (HM_GEMM_1CTA=1): one CTA per SM, 128 x 256 tiles, 4-stage ring.
 //
-// Epilogue: epilogue warp w owns TMEM lane quarter w%4 (32 rows) and one half
-// of the tile's columns.  Each thread converts its row (TMEM -> regs -> bf16)
-// into a padded per-warp smem staging tile, then the warp writes whole 128-byte
-// row segments (4 rows per instruction), optionally scattered through row_map
-// (the FFN2 output goes token-major so the combine streams contiguously).
+// Epilogue: epilogue warp w owns TMEM lane quarter w%4 (32 rows) and one half of the
+// tile's columns.  Each thread converts its row (TMEM -> regs -> bf16) into a padded
+// per-warp smem staging tile, then the warp writes whole 64-byte row segments (8 rows per
+// instruction), optionally scattered through row_map (the FFN2 output goes token-major
+// so the combine streams contiguously).
 //   kEpiStore (bf16 out), kEpiRelu (Switch FFN1), kEpiSwiGLU (W13 is block-
 //   interleaved: within each 256-row block, rows [0,128) are gate rows and
 //   [128,256) the matching up rows -> 128 bf16 outputs per tile).
@@ -309,7 +310,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 //   tfull[a]  per CTA: multicast commit after the last k-block of a tile
 //   tempty[a] leader only: 8 epilogue warps of each CTA arrive (peer remotely)
 // Tiles are 256-row pair tiles of each segment; the cursor derives them from the
-// 128-row prefix on the fly (pair tiles of a segment = ceil(m128 / 2)).
+// 128-row prefix on the fly (pair tiles of a segment = ceil(m128 / 2)).  A segment whose
+// 128-row tile count is odd ends in a half tile: M=128 cta_group::2 (64 rows per CTA, the
+// "2x2" TMEM layout: row r in lanes r and 64 + r for the two column halves).
+// Gather mode: 4 loader warps per CTA fill the A stage with 16-byte cp.async copies of
+// x rows (manual 128B swizzle), the next tile's gather indices already in registers.
 // ==========================================================================================
 constexpr int k2Stages = 6;
 constexpr uint32_t k2Half = 128 * kBK * 2;  // 16 KB: one CTA's half of A or of B per stage
