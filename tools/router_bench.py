@@ -33,7 +33,8 @@ def t_us(fn, it=20):
 
 def main():
     for (T, d, E, k) in [(16384, 2048, 128, 8), (8192, 2048, 128, 8), (4096, 2048, 128, 8), (2048, 2048, 128, 8),
-                         (16384, 2048, 128, 1), (4096, 768, 128, 1), (16384, 4096, 8, 2)]:
+                         (16384, 2048, 128, 1), (16384, 2048, 16, 1), (16384, 2048, 16, 8), (16384, 512, 128, 8),
+                         (4096, 768, 128, 1), (16384, 4096, 8, 2)]:
         x = torch.randn((T, d), device="cuda").to(torch.bfloat16)
         wg = (torch.randn((ops.e_pad(E), d), device="cuda") * 0.02).to(torch.bfloat16)
         us = t_us(lambda: ops.router_topk(x, wg, None, 1, T, k, k > 1, E=E))
