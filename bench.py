@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--logical-ranks", type=int, default=None,
                     help="N=1: simulate G GPUs in one process (HarMoEny schedule over G logical ranks); "
                          "default 4 for switch128 (BASELINE configs[0]: 'simulated 4 GPUs'), else 1")
+    ap.add_argument("--sync-fetch", action="store_true",
+                    help="EP (N>1): synchronous expert loading ablation (SimFlags.async_loading_enabled=False)")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -336,7 +338,8 @@ def run_ours(args, rank, world, local_rank):
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
         cfg = MoEConfig(rank=rank, world_size=world, eq_tokens=args.q, placement=args.placement,
-                        transport=args.transport, max_tokens_per_rank=T_total // world, **cfg_kw)
+                        transport=args.transport, max_tokens_per_rank=T_total // world,
+                        async_fetch=not args.sync_fetch, **cfg_kw)
         blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
     else:
         cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, logical_ranks=logical_ranks(args), **cfg_kw)

@@ -61,6 +61,10 @@ class MoEConfig:
     placement: str = "round_robin"
     logical_ranks: int = 1  # LOCAL mode: number of simulated GPUs (world_size must be 1)
     fetch_source: str = "peer"  # EP mode: "peer" (NVLink) or "host" (pinned host memory)
+    # EP mode: fetch rebalanced experts' weights on a side stream overlapped with FFN1 of the
+    # resident experts (True, SimFlags.async_loading_enabled) or on the compute stream ahead
+    # of it (False: the synchronous-loading ablation, engine.py:266-269)
+    async_fetch: bool = True
     residual: bool = False  # decoder-layer residual y = x + MoE(x), fused into the combine kernel
     # EP mode: "nccl" (all_to_all_single; split sizes need S on the host once per layer) or "p2p"
     # (one-sided pushes into peers' buffers over NVLink/NVSwitch, no host round trip)

@@ -310,15 +310,18 @@ class EPHarMoEnyBlock:
 
         def gemm1():
             lay = st["plan"].layout
-            fs = self.fetch_stream
-            if self.n_cache > 0:  # K6 from the device-side fetch list, overlapping FFN1
-                fs.wait_stream(s)
+            # K6 from the device-side fetch list on the fetch stream, overlapping FFN1 (async), or
+            # in stream order ahead of it (sync ablation: the GEMM's ready-flag waits pass at once)
+            fs = self.fetch_stream if cfg.async_fetch else s
+            if self.n_cache > 0:
+                if fs is not s:
+                    fs.wait_stream(s)
                 ops.fetch_experts(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.n_in * d * 2,
                                   d * cfg.d_ff * 2, self.w_in, self.w_out, self.n_home, self.n_cache, self.ready_in,
                                   self.ready_out, self.fetch_counters, value=1, stream=fs)
             ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
                              slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s)
-            if self.n_cache > 0:
+            if self.n_cache > 0 and fs is not s:
                 s.wait_stream(fs)
 
         def combine():
@@ -378,8 +381,10 @@ class EPHarMoEnyBlock:
         if len(experts) > self.n_cache:
             raise RuntimeError(f"{len(experts)} experts to fetch exceed the {self.n_cache} cache slots")
         d, f = self.cfg.d_model, self.cfg.d_ff
-        s = self.fetch_stream
-        if self._last_gemm is not None:
+        # async: one transfer channel beside the compute stream; sync ablation: the compute
+        # stream itself (FFN1 starts only after every fetch landed)
+        s = self.fetch_stream if self.cfg.async_fetch else torch.cuda.current_stream()
+        if self._last_gemm is not None and s is self.fetch_stream:
             s.wait_event(self._last_gemm)  # previous layer's GEMMs are done with the slots
         in_bytes = self.n_in * d * 2
         out_bytes = d * f * 2

@@ -43,7 +43,7 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
         cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, transport=transport.split("-")[0],
-                        max_tokens_per_rank=T // world, **KW)
+                        max_tokens_per_rank=T // world, async_fetch="sync" not in transport, **KW)
         blk = EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
         g = torch.Generator(device="cuda").manual_seed(99)
         x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
@@ -68,11 +68,13 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
 @pytest.mark.parametrize("fetch_source,transport,world", [("peer", "nccl", 2), ("host", "nccl", 2),
                                                            ("peer", "p2p", 2), ("host", "p2p", 2),
                                                            ("peer", "p2p", 4), ("peer", "p2p-graph", 2),
-                                                           ("host", "p2p-graph", 4)])
+                                                           ("host", "p2p-graph", 4), ("peer", "nccl-sync", 2),
+                                                           ("peer", "p2p-sync", 2)])
 def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
     """transport "nccl": exchanges through the process group (gloo here, host-staged);
     transport "p2p": one-sided pushes into the other ranks' IPC-mapped buffers + stream flags,
-    no collective and no host round trip inside the forward."""
+    no collective and no host round trip inside the forward.  "-sync": the synchronous-loading
+    ablation (expert fetches in stream order ahead of FFN1, SimFlags.async_loading_enabled=False)."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
