@@ -22,6 +22,46 @@
 namespace hm {
 
 namespace {
+// descending compare-exchange on packed keys
+__device__ __forceinline__ void ce_desc(unsigned long long& x, unsigned long long& y) {
+  const unsigned long long hi = x > y ? x : y;
+  const unsigned long long lo = x > y ? y : x;
+  x = hi;
+  y = lo;
+}
+
+// key[0..8) <- the 8 largest of key[0..32), descending
+__device__ __forceinline__ void router_top8_of_32(unsigned long long (&key)[32]) {
+  // optimal 19-comparator network for 8 elements, applied to the four groups of 8
+#pragma unroll
+  for (int g = 0; g < 32; g += 8) {
+    unsigned long long* k = key + g;
+    ce_desc(k[0], k[2]); ce_desc(k[1], k[3]); ce_desc(k[4], k[6]); ce_desc(k[5], k[7]);
+    ce_desc(k[0], k[4]); ce_desc(k[1], k[5]); ce_desc(k[2], k[6]); ce_desc(k[3], k[7]);
+    ce_desc(k[0], k[1]); ce_desc(k[2], k[3]); ce_desc(k[4], k[5]); ce_desc(k[6], k[7]);
+    ce_desc(k[2], k[4]); ce_desc(k[3], k[5]);
+    ce_desc(k[1], k[4]); ce_desc(k[3], k[6]);
+    ce_desc(k[1], k[2]); ce_desc(k[3], k[4]); ce_desc(k[5], k[6]);
+  }
+  // top-8 of two sorted runs: elementwise max against the reversed run is bitonic and holds
+  // the 8 largest; three half-cleaner stages sort it
+#pragma unroll
+  for (int step = 8; step < 32; step *= 2) {
+#pragma unroll
+    for (int g = 0; g < 32; g += 2 * step) {
+      unsigned long long* A = key + g;
+      const unsigned long long* B = key + g + step;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) A[i] = A[i] > B[7 - i] ? A[i] : B[7 - i];
+#pragma unroll
+      for (int s2 = 4; s2 > 0; s2 >>= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if ((i & s2) == 0) ce_desc(A[i], A[i + s2]);
+    }
+  }
+}
+
 constexpr int kRBM = 128;
 constexpr int kRBK = 64;
 constexpr int kRMaxStages = 8;
@@ -40,7 +80,7 @@ inline int router_stages(int E_pad) {
 }  // namespace
 
 template <int KMAX>
-__global__ void __launch_bounds__(kRThreads, 1)
+__global__ void __maxnreg__(104)
     router_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                   const float* __restrict__ bias, int tokens_per_rank, int tiles_per_rank, int d, int E, int E_pad,
                   int k, int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
@@ -156,7 +196,55 @@ __global__ void __launch_bounds__(kRThreads, 1)
     float vals[32];
     float lsum = 0.0f;
     // single pass per chunk: logits stay in registers for the partial sum-exp
-    if (part < nchunk) {
+    if (KMAX == 8 && part < nchunk) {
+      // top-8 of this part's 32 logits as a sorting network over packed 64-bit keys
+      // (order-preserving value bits << 32 | ~expert, so equal logits keep the lowest expert
+      // first, as the insertion below does): four 19-comparator sorts of 8 and three
+      // bitonic top-8 merges - 136 independent compare-exchanges instead of 256 dependent
+      // insertion steps
+      const int c = part;
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(taddr + c * 32, a);
+      tmem_ld_wait();
+      // logits (bias added) in place, then max and partial sum-exp first so only the keys stay
+      // live through the network
+      float mx = -INFINITY;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int e = c * 32 + jj;
+        float v = -INFINITY;
+        if (e < E) {
+          v = __uint_as_float(a[jj]);
+          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
+        }
+        a[jj] = __float_as_uint(v);
+        mx = fmaxf(mx, v);
+      }
+      float cs = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj)
+        if (c * 32 + jj < E) cs = __fadd_rn(cs, expf(__fsub_rn(__uint_as_float(a[jj]), mx)));
+      lsum = cs;
+      unsigned long long key[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int e = c * 32 + jj;
+        unsigned long long kv = (static_cast<unsigned long long>(0x007FFFFFu) << 32) | 0x80000000u;  // -inf, id INT_MAX
+        if (e < E) {
+          uint32_t u = __float_as_uint(__fadd_rn(__uint_as_float(a[jj]), 0.0f));  // -0 == +0 like the float compare
+          u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+          kv = (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(e));
+        }
+        key[jj] = kv;
+      }
+      router_top8_of_32(key);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t u = static_cast<uint32_t>(key[j] >> 32);
+        tv[j] = __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+        ti[j] = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(key[j]));
+      }
+    } else if (part < nchunk) {
       const int c = part;
       uint32_t a[32];
       tmem_ld_32x32b_x32(taddr + c * 32, a);
