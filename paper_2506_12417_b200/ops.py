@@ -33,6 +33,12 @@ def _require_cuda(*tensors):
             raise ValueError("harmoe ops need contiguous tensors")
 
 
+def _require_dtype(dtype, *tensors, what: str = "tensor"):
+    for t in tensors:
+        if t is not None and t.dtype != dtype:
+            raise ValueError(f"{what} must be {dtype}, got {t.dtype}")
+
+
 def _policy(rebalance) -> int:
     """bool (rebalance on/off) or an HM_POLICY_* code -> the C ABI's policy argument."""
     if isinstance(rebalance, bool):
@@ -198,6 +204,8 @@ def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per
     """K4.  Returns (out [out_rows, d] bf16 | None, pos [T,k] i32, inv [out_rows] i32 | None).
     index_only: no row copies (the FFN1 GEMM gathers rows through inv)."""
     _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base)
+    _require_dtype(torch.bfloat16, x, out, what="permute rows")
+    _require_dtype(torch.int32, topk_idx, lrank, tile_off, S, slot_base, what="permute index tensors")
     T, d = x.shape
     k = topk_idx.shape[1]
     G, E, _ = S.shape
@@ -218,12 +226,15 @@ def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=
                  stream=None):
     """K5.  A [rows, K] bf16, W [slots*N, K] bf16 -> out [rows, N or N/2] bf16
     (row r written to row_map[r] when a row map is given).  With a_gather, buffer row r
-    reads A[a_gather[r] // a_gather_div] (TMA gather4) and out has ``out_rows`` rows."""
+    reads A[a_gather[r] // a_gather_div] (cp.async loader warps in the 2-CTA kernel, TMA
+    gather4 in the 1-CTA one) and out has ``out_rows`` rows."""
     if isinstance(layout_or_segs, Layout):
         segs, n_seg, mprefix = layout_or_segs.segs, layout_or_segs.n_seg, layout_or_segs.mtile_prefix
     else:
         segs, n_seg, mprefix = layout_or_segs
     _require_cuda(A, W, segs, n_seg, mprefix, slot_ready, row_map, a_gather)
+    _require_dtype(torch.bfloat16, A, W, out, what="grouped_gemm operands")
+    _require_dtype(torch.int32, segs, n_seg, mprefix, row_map, a_gather, slot_ready, what="grouped_gemm index tensors")
     rows, K = A.shape
     if a_gather is not None:
         rows_out = out_rows if out_rows is not None else a_gather.numel()
@@ -249,6 +260,9 @@ def fetch_expert(dst, src, ready_flag=None, epoch: int = 0, stream=None):
 def combine(Y, pos, topk_w, out=None, residual=None, stream=None):
     """K7.  y [T, d] bf16 = (residual +) sum_j w[t,j] * Y[pos[t,j]]; pos=None: Y is token-major [T*k, d]."""
     _require_cuda(Y, pos, topk_w, residual)
+    _require_dtype(torch.bfloat16, Y, residual, out, what="combine rows")
+    _require_dtype(torch.float32, topk_w, what="combine weights")
+    _require_dtype(torch.int32, pos, what="combine positions")
     T, k = topk_w.shape
     d = Y.shape[1]
     if out is None:
