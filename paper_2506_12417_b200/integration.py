@@ -42,18 +42,29 @@ def _linear_weight(expert: nn.Module, names) -> torch.Tensor | None:
     return None
 
 
-def extract_expert_weights(experts, activation: str):
-    """Stack per-expert nn.Linear weights (nn.Linear layout [out, in]).
+def extract_expert_weights(experts, activation: str, d_model: int | None = None):
+    """Stack per-expert weights as [E, out, in] (nn.Linear layout).
     Accepts an nn.ModuleList of expert MLPs with HF names (gate_proj/up_proj/down_proj,
-    w1/w3/w2, wi/wo) or a module holding fused 3-D parameters ``gate_up_proj``
-    [E, d, 2f] / ``down_proj`` [E, f, d] (HF fused-expert layout)."""
+    w1/w3/w2, wi/wo) or a module holding fused 3-D parameters ``gate_up_proj`` /
+    ``down_proj``, either in the per-expert nn.Linear layout ([E, 2f, d] / [E, d, f]:
+    transformers 5 ``Qwen3MoeExperts``, ``MixtralExperts``, ``OlmoeExperts``; gate rows first)
+    or transposed ([E, d, 2f] / [E, f, d]).  ``d_model`` (the router's input width, or the
+    module's ``hidden_dim``) tells the two apart when 2f == d would make the shapes ambiguous."""
     if hasattr(experts, "gate_up_proj") and hasattr(experts, "down_proj") and not isinstance(experts, nn.ModuleList):
-        gu = experts.gate_up_proj.detach()  # [E, d, 2f]
-        f = gu.shape[-1] // 2
-        w1 = gu[..., :f].transpose(1, 2).contiguous()
-        w3 = gu[..., f:].transpose(1, 2).contiguous()
-        w2 = experts.down_proj.detach().transpose(1, 2).contiguous()  # [E, d, f]
-        return w1, w2, w3
+        gu = experts.gate_up_proj.detach()
+        dn = experts.down_proj.detach()
+        d = getattr(experts, "hidden_dim", None) or d_model
+        if d is None:
+            raise ValueError("fused expert weights: pass d_model to tell [E, 2f, d] from [E, d, 2f]")
+        if gu.shape[-1] == d and dn.shape[-2] == d:  # [E, 2f, d] and [E, d, f]: nn.Linear layout
+            f = gu.shape[-2] // 2
+            return gu[:, :f].contiguous(), dn.contiguous(), gu[:, f:].contiguous()
+        if gu.shape[-2] == d and dn.shape[-1] == d:  # [E, d, 2f] and [E, f, d]: transposed
+            f = gu.shape[-1] // 2
+            w1 = gu[..., :f].transpose(1, 2).contiguous()
+            w3 = gu[..., f:].transpose(1, 2).contiguous()
+            return w1, dn.transpose(1, 2).contiguous(), w3
+        raise ValueError(f"fused expert weights {tuple(gu.shape)} / {tuple(dn.shape)} do not match d_model={d}")
     w1 = torch.stack([_linear_weight(e, _GATE_NAMES).detach() for e in experts])
     w2 = torch.stack([_linear_weight(e, _DOWN_NAMES).detach() for e in experts])
     w3 = None
@@ -85,7 +96,7 @@ def build_block(moe_module: nn.Module, path_to_experts: str, path_to_router_line
     experts = _get_path(moe_module, path_to_experts)
     router = _get_path(moe_module, path_to_router_linear_layer)
     wg = router.weight.detach() if isinstance(router, nn.Module) else router.detach()
-    w1, w2, w3 = extract_expert_weights(experts, config.activation)
+    w1, w2, w3 = extract_expert_weights(experts, config.activation, d_model=wg.shape[-1])
     if config.world_size > 1:
         from .ep import EPHarMoEnyBlock
 

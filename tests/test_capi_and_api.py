@@ -133,5 +133,21 @@ def test_extract_expert_weights_hf_layouts():
             self.down_proj = nn.Parameter(torch.randn(3, 16, 8))
 
     fz = Fused()
-    w1, w2, w3 = extract_expert_weights(fz, "swiglu")
+    w1, w2, w3 = extract_expert_weights(fz, "swiglu", d_model=8)
     assert torch.equal(w1[2], fz.gate_up_proj[2, :, :16].T) and torch.equal(w2[0], fz.down_proj[0].T)
+    assert torch.equal(w3[1], fz.gate_up_proj[1, :, 16:].T)
+
+    # transformers 5 fused experts (Qwen3MoeExperts / MixtralExperts): [E, 2f, d] gate rows first,
+    # down [E, d, f]; hidden_dim disambiguates 2f == d
+    from transformers.models.qwen3_moe.configuration_qwen3_moe import Qwen3MoeConfig
+    from transformers.models.qwen3_moe.modeling_qwen3_moe import Qwen3MoeExperts
+
+    hf = Qwen3MoeExperts(Qwen3MoeConfig(hidden_size=16, moe_intermediate_size=8, num_experts=3))
+    nn.init.normal_(hf.gate_up_proj)
+    nn.init.normal_(hf.down_proj)
+    w1, w2, w3 = extract_expert_weights(hf, "swiglu")
+    assert w1.shape == (3, 8, 16) and w3.shape == (3, 8, 16) and w2.shape == (3, 16, 8)
+    assert torch.equal(w1[1], hf.gate_up_proj[1, :8]) and torch.equal(w3[1], hf.gate_up_proj[1, 8:])
+    assert torch.equal(w2[2], hf.down_proj[2])
+    with pytest.raises(ValueError):
+        extract_expert_weights(Fused(), "swiglu", d_model=5)

@@ -156,3 +156,87 @@ def test_replace_moe_layer_matches_torch_reference():
     err = (got - ref).abs()
     tol = 2e-2 + 3e-2 * ref.abs()
     assert (err <= tol).float().mean() > 0.98  # near-tie routing flips aside
+
+
+def _hf_reference_block(block_cls, config, dev):
+    torch.manual_seed(3)
+    blk = block_cls(config).to(dev)
+    for p in blk.parameters():
+        nn.init.normal_(p, std=0.05)
+        p.data = p.data.to(torch.bfloat16).float()  # bf16-representable weights, fp32 HF math
+    return blk
+
+
+@pytest.mark.parametrize("arch", ["qwen3_moe", "mixtral"])
+def test_replace_moe_layer_on_transformers_blocks(arch):
+    """The paper's drop-in API on the real transformers 5 MoE blocks (fused [E, 2f, d] experts,
+    TopK routers): the B200 block reproduces the HF block's own forward within the bf16 bar."""
+    dev = _cuda()
+    from paper_2506_12417_b200 import MoEConfig, replace_moe_layer
+
+    d, f, E, k = 256, 256, 16, 4 if arch == "qwen3_moe" else 2
+    if arch == "qwen3_moe":
+        from transformers.models.qwen3_moe.configuration_qwen3_moe import Qwen3MoeConfig as C
+        from transformers.models.qwen3_moe.modeling_qwen3_moe import Qwen3MoeSparseMoeBlock as B
+
+        conf = C(hidden_size=d, moe_intermediate_size=f, num_experts=E, num_experts_per_tok=k, norm_topk_prob=True)
+    else:
+        from transformers.models.mixtral.configuration_mixtral import MixtralConfig as C
+        from transformers.models.mixtral.modeling_mixtral import MixtralSparseMoeBlock as B
+
+        conf = C(hidden_size=d, intermediate_size=f, num_local_experts=E, num_experts_per_tok=k)
+
+    class Parent(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.mlp = _hf_reference_block(B, conf, dev)
+
+        def forward(self, x):
+            return self.mlp(x)
+
+    model = Parent()
+    x = torch.randn((2, 96, d), device=dev).to(torch.bfloat16).float()
+    with torch.no_grad():
+        ref = model(x)
+    cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=k, activation="swiglu", eq_tokens=4, renormalize=True)
+    assert replace_moe_layer(model, Parent, B, "experts", "gate", cfg, device=dev) == 1
+    with torch.no_grad():
+        got = model(x)
+    assert got.shape == ref.shape
+    err = (got - ref).abs()
+    tol = 2e-2 + 3e-2 * ref.abs()
+    assert (err <= tol).float().mean() > 0.98, f"{arch}: {(err > tol).float().mean():.3%} out of tolerance"
+    frob = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
+    assert frob < 3e-2, f"{arch}: relative Frobenius error {frob}"
+
+
+def test_replace_moe_layer_in_a_transformers_model():
+    """replace_moe_layer(model, Qwen3MoeDecoderLayer, Qwen3MoeSparseMoeBlock, "experts", "gate", cfg)
+    on a randomly initialised 2-layer Qwen3-MoE causal LM: every MoE layer is
+    swapped and the logits stay within the bf16 bar of the original model's."""
+    dev = _cuda()
+    from transformers.models.qwen3_moe.configuration_qwen3_moe import Qwen3MoeConfig
+    from transformers.models.qwen3_moe.modeling_qwen3_moe import (Qwen3MoeDecoderLayer, Qwen3MoeForCausalLM,
+                                                                  Qwen3MoeSparseMoeBlock)
+
+    from paper_2506_12417_b200 import MoEConfig, replace_moe_layer
+
+    torch.manual_seed(0)
+    conf = Qwen3MoeConfig(vocab_size=512, hidden_size=256, intermediate_size=512, moe_intermediate_size=256,
+                          num_hidden_layers=2, num_attention_heads=4, num_key_value_heads=2, head_dim=64,
+                          num_experts=16, num_experts_per_tok=4, norm_topk_prob=True, max_position_embeddings=256)
+    conf._attn_implementation = "eager"
+    model = Qwen3MoeForCausalLM(conf).to(dev).eval()
+    for p in model.parameters():
+        p.data = p.data.to(torch.bfloat16).float()
+    ids = torch.randint(0, 512, (2, 64), device=dev)
+    with torch.no_grad():
+        ref = model(ids).logits
+    cfg = MoEConfig(d_model=256, num_experts=16, d_ff=256, top_k=4, activation="swiglu", eq_tokens=4, renormalize=True)
+    assert replace_moe_layer(model, Qwen3MoeDecoderLayer, Qwen3MoeSparseMoeBlock, "experts", "gate", cfg,
+                             device=dev) == 2
+    with torch.no_grad():
+        got = model(ids).logits
+    frob = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
+    assert frob < 2e-2, f"relative Frobenius error of the logits {frob}"
+    assert (got.argmax(-1) == ref.argmax(-1)).float().mean() > 0.95
