@@ -65,11 +65,12 @@ def extract_expert_weights(experts, activation: str, d_model: int | None = None)
             w3 = gu[..., f:].transpose(1, 2).contiguous()
             return w1, dn.transpose(1, 2).contiguous(), w3
         raise ValueError(f"fused expert weights {tuple(gu.shape)} / {tuple(dn.shape)} do not match d_model={d}")
-    w1 = torch.stack([_linear_weight(e, _GATE_NAMES).detach() for e in experts])
-    w2 = torch.stack([_linear_weight(e, _DOWN_NAMES).detach() for e in experts])
+    mods = list(experts.values()) if isinstance(experts, nn.ModuleDict) else list(experts)  # expert_0, expert_1, ...
+    w1 = torch.stack([_linear_weight(e, _GATE_NAMES).detach() for e in mods])
+    w2 = torch.stack([_linear_weight(e, _DOWN_NAMES).detach() for e in mods])
     w3 = None
     if activation == "swiglu":
-        w3 = torch.stack([_linear_weight(e, _UP_NAMES).detach() for e in experts])
+        w3 = torch.stack([_linear_weight(e, _UP_NAMES).detach() for e in mods])
     return w1, w2, w3
 
 

@@ -240,3 +240,39 @@ def test_replace_moe_layer_in_a_transformers_model():
     frob = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
     assert frob < 2e-2, f"relative Frobenius error of the logits {frob}"
     assert (got.argmax(-1) == ref.argmax(-1)).float().mean() > 0.95
+
+
+def test_replace_moe_layer_on_switch_transformers():
+    """Switch-128's own module family (SwitchTransformersSparseMLP: top-1 router classifier,
+    ModuleDict of ReLU wi/wo experts, weight = the top-1 softmax probability) with the expert
+    capacity above the token count (HarMoEny never drops tokens)."""
+    dev = _cuda()
+    from transformers.models.switch_transformers.configuration_switch_transformers import SwitchTransformersConfig
+    from transformers.models.switch_transformers.modeling_switch_transformers import SwitchTransformersSparseMLP
+
+    from paper_2506_12417_b200 import MoEConfig, replace_moe_layer
+
+    d, f, E, T = 256, 512, 16, 192
+    conf = SwitchTransformersConfig(d_model=d, d_ff=f, num_experts=E, expert_capacity=T, dropout_rate=0.0)
+
+    class Parent(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.mlp = _hf_reference_block(SwitchTransformersSparseMLP, conf, dev).eval()
+
+        def forward(self, x):
+            return self.mlp(x)
+
+    model = Parent()
+    x = torch.randn((1, T, d), device=dev).to(torch.bfloat16).float()
+    with torch.no_grad():
+        ref = model(x)
+    cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=1, activation="relu", eq_tokens=4)
+    assert replace_moe_layer(model, Parent, SwitchTransformersSparseMLP, "experts", "router.classifier", cfg,
+                             device=dev) == 1
+    with torch.no_grad():
+        got = model(x)
+    err = (got - ref).abs()
+    tol = 2e-2 + 3e-2 * ref.abs()
+    assert (err <= tol).float().mean() > 0.98
+    assert float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref)) < 3e-2
