@@ -75,18 +75,30 @@ def extract_expert_weights(experts, activation: str, d_model: int | None = None)
 
 
 class HarMoEnyLayer(nn.Module):
-    """nn.Module wrapper: hidden [..., d] -> MoE(hidden) through the B200 block."""
+    """nn.Module wrapper: hidden [..., d] -> MoE(hidden) through the B200 block.
 
-    def __init__(self, block, returns_router_logits: bool = False):
+    ``shared_expert`` / ``shared_expert_gate`` (the always-on dense expert of Qwen1.5/2-MoE,
+    the paper's Qwen model): y += sigmoid(gate(x)) * shared(x), a plain dense MLP outside the
+    routed path, run by the original module (cuBLAS) beside the routed experts."""
+
+    def __init__(self, block, returns_router_logits: bool = False, shared_expert: nn.Module | None = None,
+                 shared_expert_gate: nn.Module | None = None):
         super().__init__()
         self.block = block
         self.returns_router_logits = returns_router_logits
+        self.shared_expert = shared_expert
+        self.shared_expert_gate = shared_expert_gate
 
     @torch.no_grad()
     def forward(self, hidden_states: torch.Tensor, *args, **kwargs):
         shape = hidden_states.shape
         x = hidden_states.reshape(-1, shape[-1]).to(torch.bfloat16).contiguous()
         y = self.block(x).reshape(shape).to(hidden_states.dtype)
+        if self.shared_expert is not None:
+            s = self.shared_expert(hidden_states)
+            if self.shared_expert_gate is not None:
+                s = torch.sigmoid(self.shared_expert_gate(hidden_states)) * s
+            y = y + s
         if self.returns_router_logits:
             return y, None
         return y
@@ -116,7 +128,9 @@ def replace_moe_layer(model: nn.Module, moe_parent_type, moe_type, path_to_exper
         for name, child in list(parent.named_children()):
             if isinstance(child, moe_type):
                 blk = build_block(child, path_to_experts, path_to_router_linear_layer, config, device=device)
-                setattr(parent, name, HarMoEnyLayer(blk, returns_router_logits))
+                setattr(parent, name, HarMoEnyLayer(blk, returns_router_logits,
+                                                    shared_expert=getattr(child, "shared_expert", None),
+                                                    shared_expert_gate=getattr(child, "shared_expert_gate", None)))
                 replaced += 1
     return replaced
 

@@ -167,15 +167,21 @@ def _hf_reference_block(block_cls, config, dev):
     return blk
 
 
-@pytest.mark.parametrize("arch", ["qwen3_moe", "mixtral"])
+@pytest.mark.parametrize("arch", ["qwen3_moe", "mixtral", "qwen2_moe"])
 def test_replace_moe_layer_on_transformers_blocks(arch):
     """The paper's drop-in API on the real transformers 5 MoE blocks (fused [E, 2f, d] experts,
     TopK routers): the B200 block reproduces the HF block's own forward within the bf16 bar."""
     dev = _cuda()
     from paper_2506_12417_b200 import MoEConfig, replace_moe_layer
 
-    d, f, E, k = 256, 256, 16, 4 if arch == "qwen3_moe" else 2
-    if arch == "qwen3_moe":
+    d, f, E, k = 256, 256, 16, 2 if arch == "mixtral" else 4
+    if arch == "qwen2_moe":  # the paper's Qwen family: routed experts + a gated shared expert
+        from transformers.models.qwen2_moe.configuration_qwen2_moe import Qwen2MoeConfig as C
+        from transformers.models.qwen2_moe.modeling_qwen2_moe import Qwen2MoeSparseMoeBlock as B
+
+        conf = C(hidden_size=d, moe_intermediate_size=f, shared_expert_intermediate_size=512, num_experts=E,
+                 num_experts_per_tok=k, norm_topk_prob=True)
+    elif arch == "qwen3_moe":
         from transformers.models.qwen3_moe.configuration_qwen3_moe import Qwen3MoeConfig as C
         from transformers.models.qwen3_moe.modeling_qwen3_moe import Qwen3MoeSparseMoeBlock as B
 
