@@ -66,6 +66,22 @@ def main():
     except Exception as e:  # noqa: BLE001
         print(f"vLLM fused_experts unavailable: {type(e).__name__}: {e}"[:300], flush=True)
 
+    try:  # FlashInfer's ahead-of-time built CUTLASS fused MoE for SM100 (the TensorRT-LLM kernels)
+        from flashinfer.fused_moe import cutlass_fused_moe
+
+        def fi_fwd():
+            logits = torch.matmul(x, wg.t()).float() + bias
+            p = torch.softmax(logits, dim=-1)
+            w, ids = torch.topk(p, k, dim=-1)
+            w = w / w.sum(-1, keepdim=True)
+            # timing only: the gate/up half order follows TensorRT-LLM's convention, not checked here
+            return cutlass_fused_moe(x, ids.to(torch.int32), w, gate_up, down, torch.bfloat16, quant_scales=[])
+
+        t = timed(fi_fwd)
+        print(f"FlashInfer cutlass_fused_moe (SM100 AOT): {t:8.3f} ms  {T / t / 1e3:8.2f} M tok/s", flush=True)
+    except Exception as e:  # noqa: BLE001
+        print(f"FlashInfer cutlass_fused_moe unavailable: {type(e).__name__}: {e}"[:300], flush=True)
+
     if shape != "qwen128":
         return
     try:
