@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="qwen128", choices=sorted(WORKLOADS))
     ap.add_argument("--layers", type=int, default=1, help="MoE decoder layers per step (BASELINE config 4)")
+    ap.add_argument("--tokens", type=int, default=0, help="override the workload's token count (diagnostics)")
     ap.add_argument("--zipf", type=float, default=1.0)
     ap.add_argument("--q", type=int, default=None,
                     help="token threshold q; default 32, 4 for switch128 (buckets of a few dozen tokens)")
@@ -298,10 +299,10 @@ def algorithmic_work(wl, tokens, active_experts=None):
     return f1, f2, w_bytes, act_bytes, g1_bytes
 
 
-def uses_gather(blk) -> bool:
+def uses_gather(blk, tokens: int) -> bool:
     """Does FFN1 gather its rows from x (fused scatter) in this block / the stack's layers?"""
     first = blk.layers[0] if hasattr(blk, "layers") else blk
-    return bool(getattr(first, "fused_scatter", False))
+    return bool(first.uses_fused_scatter(tokens)) if hasattr(first, "uses_fused_scatter") else False
 
 
 def logical_ranks(args) -> int:
@@ -331,6 +332,9 @@ def run_ours(args, rank, world, local_rank):
 
     wl = WORKLOADS[args.workload]
     d, f, E, k, act, T_total = wl
+    if args.tokens:  # diagnostics: another batch size of the same layer
+        T_total = args.tokens
+        wl = (d, f, E, k, act, T_total)
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     cfg_kw = dict(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act)
@@ -513,7 +517,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": (f"grouped_gemm_2cta_kernel<{'SwiGLU' if act == 'swiglu' else 'ReLU'}, "
-                                f"{'cp.async gather of x rows' if uses_gather(blk) else 'TMA'}> "
+                                f"{'cp.async gather of x rows' if uses_gather(blk, T_total // world) else 'TMA'}> "
                                 f"(expert FFN1)"),
                      "work_per_launch": work_desc,
                      "peak_source": f"MEASURED_PEAKS.json ({peak_kind}; bf16 {peak_src}; burst {tc}, "

@@ -296,11 +296,20 @@ class HarMoEnyBlock:
         # fused scatter: FFN1 gathers token rows itself with cp.async loader warps, so the
         # k-fold replicated token buffer (T*k*d*2 bytes written, then read) never exists.  With
         # the m-major pair-tile walk the NB pairs sharing an A tile gather the same rows side by
-        # side (L2 hits).  Measured on B200: Qwen-128 (top-8) +4.5% short / +3.7% power-capped;
-        # Switch-128 (top-1, HBM-bound FFN1) -31%, Mixtral (top-2) -2% -> on for top_k >= 4.
-        # HM_FUSED_SCATTER=0/1 overrides.
+        # side (L2 hits).  Measured on B200: Qwen-128 16k tokens (top-8, ~1000 rows per expert)
+        # +4.5% short / +3.7% power-capped, 4k tokens even; but where FFN1 streams weights for
+        # small segments the gather latency throttles the weight pipeline: Qwen-128 at 256 /
+        # 1024 tokens -17% / -13%, Switch-128 (top-1) -31%, Mixtral (top-2) -2%.  Auto (None):
+        # on for top_k >= 4 with >= 256 rows per expert on average.  HM_FUSED_SCATTER=0/1 or
+        # assigning True/False overrides.
         env = os.environ.get("HM_FUSED_SCATTER", "")
-        self.fused_scatter = (env == "1") if env in ("0", "1") else cfg.top_k >= 4
+        self.fused_scatter = (env == "1") if env in ("0", "1") else None
+
+    def uses_fused_scatter(self, num_tokens: int) -> bool:
+        if self.fused_scatter is not None:
+            return bool(self.fused_scatter)
+        cfg = self.cfg
+        return cfg.top_k >= 4 and num_tokens * cfg.top_k >= 256 * cfg.num_experts
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s: float | None = None, std: float = 0.02):
@@ -366,7 +375,7 @@ class HarMoEnyBlock:
                                     extras=dict(topk_idx=st["idx"], topk_w=st["w"], layout=p.layout,
                                                 lrank=st["lrank"], tile_off=p.tile_off))
 
-        fused = self.fused_scatter
+        fused = self.uses_fused_scatter(G * Tg)
 
         def permute():
             # fused: index-only scatter (buffer positions + inverse map); the FFN1 GEMM then

@@ -3,7 +3,7 @@ experts, top-8, 16,384 tokens, bf16) through (a) this repo's block, (b) transfor
 Qwen3MoeSparseMoeBlock (eager per-expert loop) and (c) vLLM's Triton fused_experts with a torch
 router.  Diagnostics only (not a bench value); CUDA-event device time per forward.
 
-    python tools/compare_libs.py [qwen128|mixtral8]
+    python tools/compare_libs.py [qwen128|mixtral8] [tokens]
 """
 
 import os
@@ -31,12 +31,14 @@ def timed(fn, it=10, warm=3):
 def main():
     shape = sys.argv[1] if len(sys.argv) > 1 else "qwen128"
     d, f, E, k, T = {"qwen128": (2048, 768, 128, 8, 16384), "mixtral8": (4096, 14336, 8, 2, 16384)}[shape]
+    if len(sys.argv) > 2:  # token count override (e.g. small decode-like batches)
+        T = int(sys.argv[2])
     dev = torch.device("cuda")
     cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, eq_tokens=32, renormalize=True)
     print(f"{shape}: d {d}, d_ff {f}, {E} experts, top-{k}, {T} tokens")
     blk = HarMoEnyBlock.random(cfg, seed=0, zipf_s=1.0)
     x = torch.randn((T, d), device=dev).to(torch.bfloat16)
-    cap = blk.capture(T)
+    cap = blk.capture(T, groups=(("router", "schedule", "permute", "gemm1", "gemm2", "combine"),))  # one graph
     cap.x.copy_(x)
     ours = timed(lambda: cap.replay())
     print(f"this repo (graph replay)         : {ours:8.3f} ms  {T / ours / 1e3:8.2f} M tok/s", flush=True)
@@ -82,7 +84,7 @@ def main():
     except Exception as e:  # noqa: BLE001
         print(f"FlashInfer cutlass_fused_moe unavailable: {type(e).__name__}: {e}"[:300], flush=True)
 
-    if shape != "qwen128":
+    if shape != "qwen128" or T != 16384:
         return
     try:
         from transformers.models.qwen3_moe.configuration_qwen3_moe import Qwen3MoeConfig
