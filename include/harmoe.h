@@ -16,15 +16,22 @@
  *   hm_hist_scan        per-GPU token->expert histogram = RoutingMatrix row
  *                       (core.py:89-96) = metadata m_expert
  *   hm_schedule /       initial_assign + rebalance (policies.py:109-171) as
- *   hm_rebalance        dispatched by engine.build_schedule (engine.py:287-299)
+ *   hm_rebalance        dispatched by engine.build_schedule (engine.py:287-299);
+ *                       even_split_assign (policies.py:174-203) by policy code
+ *   hm_schedule_batched build_schedule over every (batch, layer) of a trace
+ *                       (engine.py:430-447; trace format workload.py:213-232)
  *   hm_dispatch_layout  byte flows of the scatter (engine._exchange_byte_vectors,
  *                       engine.py:278-284) + per-GPU execution order of
  *                       plan_gpu_execution (engine.py:233-234)
+ *   hm_plan             steps 2-3 fused: histogram reduce + hm_schedule + layout
  *   hm_permute          Alg.1 step 4 scatter
  *   hm_grouped_gemm     Alg.1 step 5 expert compute (cost
  *                       model engine.py:128-132)
- *   hm_fetch_expert     async expert fetch (engine.py:253-265)
+ *   hm_fetch_expert(s)  async expert fetch (engine.py:253-265)
  *   hm_combine          Alg.1 step 6 gather + reconstruct
+ *   hm_ep_offsets, hm_dispatch_push, hm_grouped_gemm_remote, hm_stream_signal/wait,
+ *   hm_ipc_*            expert parallelism over NVSwitch peer memory: the metadata exchange
+ *                       and the scatter / gather all-to-alls of engine.py:328-375
  */
 #ifndef HARMOE_H_
 #define HARMOE_H_
