@@ -658,6 +658,58 @@ __global__ void __launch_bounds__(kPlanThreads)
   dev_layout(S, home, G, E, mode, me, o, s_lay);
 }
 
+// Single-GPU planner (G = 1, LOCAL): nothing can move, so the schedule is S = m and the layout
+// reduces to one scan and one sort of the experts - done with one thread per expert instead of
+// the general (dest, expert) machinery.  Outputs are identical to plan_kernel<true> at G = 1:
+// rows expert-major, segments in plan order (all experts resident: more tokens first, then
+// lower id, engine.py:233-234), no fetches.
+__global__ void __launch_bounds__(kPlanThreads)
+    plan_g1_kernel(const int32_t* __restrict__ tile_hist, int tpr, int E, int32_t* __restrict__ m_out,
+                   int32_t* __restrict__ tile_off, int32_t* __restrict__ S_out, int32_t* __restrict__ iters_out,
+                   int32_t* __restrict__ loads_out, LayoutOut o) {
+  extern __shared__ int s_dyn[];
+  __shared__ int s_part[8 * 128];
+  __shared__ int s_tmp[32];
+  int* s_m = s_dyn;                 // [E]
+  int* s_base = s_m + E;            // [E + 1] expert-major row starts
+  int* s_cnt = s_base + E + 1;      // [E + 1] 128-row tiles per segment, plan order
+  unsigned long long* s_key =       // [E] plan-order keys (8-byte aligned)
+      reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_cnt + E + 1) + 7) & ~uintptr_t(7));
+  const int tid = threadIdx.x;
+  if (tid == 0) g_phase_ns[0] = globaltimer_ns();
+  dev_hist_reduce(tile_hist, 1, tpr, E, s_m, m_out, tile_off, s_part);
+  if (tid == 0) g_phase_ns[1] = globaltimer_ns();
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int n = s_m[e];
+    S_out[e] = n;  // S[0, e, 0]
+    s_key[e] = plan_key(true, n, e);
+  }
+  block_scan_to(s_m, E, s_base, s_tmp);  // s_base[E] = total (ends with __syncthreads)
+  if (tid == 0) {
+    g_phase_ns[2] = globaltimer_ns();
+    *iters_out = 0;
+    if (loads_out != nullptr) loads_out[0] = s_base[E];
+    *o.n_fetch = 0;
+  }
+  int nseg = 0;
+  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+    const int e = e0 + tid;
+    const unsigned long long key = e < E ? s_key[e] : ~0ull;
+    if (key != ~0ull) {
+      int rank = 0;  // keys are distinct (the expert id is part of the key)
+      for (int j = 0; j < E; ++j) rank += s_key[j] < key;
+      const int n = s_m[e];
+      o.segs[rank] = make_int4(s_base[e], n, e, e);
+      s_cnt[rank] = (n + 127) / 128;
+    }
+    if (e < E) o.slot_base[e] = s_base[e];
+    nseg += __syncthreads_count(key != ~0ull);
+  }
+  if (tid == 0) *o.n_seg = nseg;
+  block_scan_to(s_cnt, nseg, o.mprefix, s_tmp);
+  if (tid == 0) g_phase_ns[3] = globaltimer_ns();
+}
+
 // Whole planning stage in one launch.  kHist: m_all comes from the router's tile
 // histograms (LOCAL, n_ranks = G); otherwise from m_in (EP: the all-gathered m_all).
 template <bool kHist>
@@ -757,6 +809,15 @@ int launch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode,
   return check_launch("dispatch_layout");
 }
 
+static bool use_plan_g1() {  // HM_PLAN_G1=0: the general planner at G = 1 too (A/B, tests)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HM_PLAN_G1");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_in, const int32_t* home, int G, int E,
                 int q, int rebalance, int mode, int me, int32_t* m_out, int32_t* tile_off, int32_t* S, int32_t* iters,
                 int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix,
@@ -772,7 +833,12 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   const size_t smem = (size_t)(E + G * E + 2 * G * E * G + layout_scratch_ints(G, E)) * sizeof(int);
   if (smem > 200 * 1024) return set_error(HM_EINVAL, "plan: G*E*G too large for the fused planner; use hm_schedule");
   LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
-  if (hist) {
+  if (hist && G == 1 && use_plan_g1()) {
+    const size_t smem1 = (size_t)(3 * E + 2) * sizeof(int) + 8 + (size_t)E * 8;
+    cudaFuncSetAttribute(plan_g1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    plan_g1_kernel<<<1, kPlanThreads, smem1, stream>>>(tile_hist, tiles_per_rank, E, m_out, tile_off, S, iters, loads,
+                                                       o);
+  } else if (hist) {
     cudaFuncSetAttribute(plan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     plan_kernel<true><<<1, kPlanThreads, smem, stream>>>(tile_hist, tiles_per_rank, nullptr, home, G, E, q, rebalance,
                                                          mode, me, m_out, tile_off, S, iters, loads, o);

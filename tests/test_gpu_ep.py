@@ -170,3 +170,31 @@ def test_ep_block_single_rank_matches_local_block():
         assert torch.equal(loc.stats.schedule, ep.stats.schedule)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("E,tiles,zero_frac", [(128, 128, 0.0), (16, 3, 0.3), (60, 17, 0.5), (1024, 9, 0.9),
+                                               (8, 1, 0.0)])
+def test_plan_single_gpu_matches_general_kernels(E, tiles, zero_frac):
+    """The G=1 planner (one thread per expert) produces exactly what the general kernels do:
+    hist_scan (m, tile offsets), schedule (S = m) and dispatch_layout (rows, plan-order segments,
+    tile prefix, no fetches)."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    rng = np.random.default_rng(E + tiles)
+    th = rng.integers(0, 40, size=(tiles, E)) * (rng.random((tiles, E)) >= zero_frac)
+    th[:, rng.integers(0, E)] += 7  # ties in n and a hot expert
+    tile_hist = torch.from_numpy(th.astype(np.int32)).to(dev)
+    home = torch.zeros(E, dtype=torch.int32, device=dev)
+    p = ops.plan(home, 1, E, 32, True, ops.HM_LAYOUT_LOCAL, tile_hist=tile_hist, tiles_per_rank=tiles)
+    hist, tile_off = ops.hist_scan(tile_hist, 1, tiles)
+    S, iters, loads = ops.schedule(hist, home, 32, True)
+    lay = ops.dispatch_layout(S, home, ops.HM_LAYOUT_LOCAL)
+    torch.cuda.synchronize()
+    assert torch.equal(p.m_all, hist) and torch.equal(p.tile_off, tile_off)
+    assert torch.equal(p.S, S) and int(p.iters.item()) == 0 and torch.equal(p.loads, loads)
+    n = int(lay.n_seg.item())
+    assert int(p.layout.n_seg.item()) == n and int(p.layout.n_fetch.item()) == 0
+    assert torch.equal(p.layout.segs[:n], lay.segs[:n])
+    assert torch.equal(p.layout.mtile_prefix[: n + 1], lay.mtile_prefix[: n + 1])
+    assert torch.equal(p.layout.slot_base, lay.slot_base)

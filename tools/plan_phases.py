@@ -23,9 +23,10 @@ def main():
         buf = (ctypes.c_longlong * 8)()
         _lib.check(_lib.load().hm_debug_plan_phases(buf), "phases")
         t = list(buf)
+        sub = (f" [head {(t[4] - t[2]) / 1e3:.1f}, slots+segs {(t[5] - t[4]) / 1e3:.1f}, "
+               f"scan {(t[6] - t[5]) / 1e3:.1f}]") if G > 1 else " (single-GPU planner)"
         print(f"G={G}: hist {(t[1] - t[0]) / 1e3:.1f} us, schedule {(t[2] - t[1]) / 1e3:.1f} us, "
-              f"layout {(t[3] - t[2]) / 1e3:.1f} us [head {(t[4] - t[2]) / 1e3:.1f}, slots+segs "
-              f"{(t[5] - t[4]) / 1e3:.1f}, scan {(t[6] - t[5]) / 1e3:.1f}], iters {int(blk.stats.iters.item())}")
+              f"layout {(t[3] - t[2]) / 1e3:.1f} us{sub}, iters {int(blk.stats.iters.item())}")
 
 
 if __name__ == "__main__":
