@@ -154,9 +154,13 @@ __global__ void __launch_bounds__(kPermWarps * 32)
 template <int KT>
 __global__ void __launch_bounds__(kPermWarps * 32)
     combine_dense_kernel(const uint4* __restrict__ Y, const float* __restrict__ w, int64_t T, int k, int n16,
-                         const uint4* __restrict__ residual, uint4* __restrict__ y) {
+                         const uint4* __restrict__ residual, uint4* __restrict__ y, int parts) {
+  // warp (t, part): token t's 16-byte column chunks [part*32, ...) step 32*parts.  parts > 1 for
+  // small batches, so enough warps are in flight to cover DRAM latency
   const int lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
+  const int64_t wg = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
+  const int64_t t = wg / parts;
+  const int part = (int)(wg - t * parts);
   if (t >= T) return;
   const int kk = KT > 0 ? KT : k;
   float wj[KT > 0 ? KT : 16];
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(kPermWarps * 32)
   for (int j = 0; j < (KT > 0 ? KT : 16); ++j) wj[j] = (j < kk) ? __ldg(w + t * kk + j) : 0.0f;
   const uint4* base = Y + t * kk * n16;
   uint4* dst = y + t * n16;
-  for (int c = lane; c < n16; c += 32) {
+  for (int c = part * 32 + lane; c < n16; c += 32 * parts) {
     uint4 u[KT > 0 ? KT : 16];
 #pragma unroll
     for (int j = 0; j < (KT > 0 ? KT : 16); ++j)
@@ -242,13 +246,17 @@ int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T
   const int n16 = d / 8;
   const int vec = (n16 + 31) / 32;
   const unsigned grid = (unsigned)((T + kPermWarps - 1) / kPermWarps);
+  // dense layout: split each token's columns over up to n16/32 warps until ~16K warps are in flight
+  int parts = 1;
+  while (parts * 2 <= (n16 + 31) / 32 && (int64_t)T * parts * 2 <= 16384) parts *= 2;
+  const unsigned grid_d = (unsigned)(((int64_t)T * parts + kPermWarps - 1) / kPermWarps);
   auto* Ys = reinterpret_cast<const uint4*>(Y);
   auto* o = reinterpret_cast<uint4*>(y);
   auto* res = reinterpret_cast<const uint4*>(residual);
   if (pos == nullptr) {
     if (k > 16) return set_error(HM_EINVAL, "combine: dense layout needs k <= 16");
 #define HM_DENSE(KT) \
-  combine_dense_kernel<KT><<<grid, kPermWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, res, o)
+  combine_dense_kernel<KT><<<grid_d, kPermWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, res, o, parts)
     if (k == 1) HM_DENSE(1);
     else if (k == 2) HM_DENSE(2);
     else if (k == 4) HM_DENSE(4);
