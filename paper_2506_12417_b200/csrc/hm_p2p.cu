@@ -86,7 +86,11 @@ __global__ void __launch_bounds__(kPushWarps * 32)
     const int c = i * 32 + lane;
     if (c < n16) v[i] = ld_global_nc_v4(src + c);
   }
-  for (int j = 0; j < k; ++j) {
+  // lane j < k resolves slot j's destination rank and receive row (the k dependent load
+  // chains side by side); the row stores below then only need two shuffles per slot
+  int qj = 0, dj = 0;
+  if (lane < k) {
+    const int j = lane;
     const int e = __ldg(topk_idx + t * k + j);
     const int r = __ldg(tile_off + (int64_t)tile * E + e) + __ldg(lrank + t * k + j);
     const int32_t* srow = S + ((int64_t)me * E + e) * G;
@@ -96,13 +100,16 @@ __global__ void __launch_bounds__(kPushWarps * 32)
       if (c + s > r) break;
       c += s;
     }
-    const int64_t p = (int64_t)__ldg(slot_base + ((int64_t)me * E + e) * G + d) + (r - c);  // send layout
-    const int64_t q = p + __ldg(dst_delta + d);                                                // d's receive row
+    const int p = __ldg(slot_base + ((int64_t)me * E + e) * G + d) + (r - c);  // send layout
+    qj = p + __ldg(dst_delta + d);                                              // d's receive row
+    dj = d;
+    if (pos != nullptr) pos[t * k + j] = p;
+    reinterpret_cast<int32_t*>(__ldg(dst_tok + d))[qj] = (int32_t)(t * k + j);
+  }
+  for (int j = 0; j < k; ++j) {
+    const int64_t q = __shfl_sync(0xffffffffu, qj, j);
+    const int d = __shfl_sync(0xffffffffu, dj, j);
     uint4* dst = reinterpret_cast<uint4*>(__ldg(dst_rows + d)) + q * n16;
-    if (lane == 0) {
-      if (pos != nullptr) pos[t * k + j] = (int32_t)p;
-      reinterpret_cast<int32_t*>(__ldg(dst_tok + d))[q] = (int32_t)(t * k + j);
-    }
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
       const int cc = i * 32 + lane;
@@ -176,7 +183,8 @@ int launch_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* 
                          int G, int E, int k, int d, const unsigned long long* dst_rows,
                          const unsigned long long* dst_tok, int32_t* pos, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(HM_EINVAL, "dispatch_push: d must be a multiple of 8");
-  if (G < 1 || G > 32 || me < 0 || me >= G || k < 1) return set_error(HM_EINVAL, "dispatch_push: bad G/me/k");
+  if (G < 1 || G > 32 || me < 0 || me >= G || k < 1 || k > 32)
+    return set_error(HM_EINVAL, "dispatch_push: bad G/me/k");
   if (tokens <= 0) return HM_OK;
   const int n16 = d / 8;
   const int blocks = (tokens + kPushWarps - 1) / kPushWarps;

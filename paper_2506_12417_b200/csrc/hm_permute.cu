@@ -41,7 +41,11 @@ __global__ void __launch_bounds__(kPermWarps * 32)
     const int c = i * 32 + lane;
     if (c < n16) v[i] = ld_global_nc_v4(src + c);
   }
-  for (int j = 0; j < k; ++j) {
+  // lane j < k resolves slot j's buffer row (expert -> rank -> split-bucket destination ->
+  // row): the k dependent load chains run side by side instead of one after another
+  int pj = 0;
+  if (lane < k) {
+    const int j = lane;
     const int e = __ldg(topk_idx + t * k + j);
     const int r = __ldg(tile_off + (int64_t)tile * E + e) + __ldg(lrank + t * k + j);
     const int32_t* srow = S + ((int64_t)g * E + e) * G;
@@ -51,11 +55,12 @@ __global__ void __launch_bounds__(kPermWarps * 32)
       if (c + s > r) break;
       c += s;
     }
-    const int64_t p = (int64_t)__ldg(slot_base + ((int64_t)g * E + e) * G + d) + (r - c);
-    if (lane == 0) {
-      pos[t * k + j] = (int32_t)p;
-      if (inv != nullptr) inv[p] = (int32_t)(t * k + j);
-    }
+    pj = __ldg(slot_base + ((int64_t)g * E + e) * G + d) + (r - c);
+    pos[t * k + j] = pj;
+    if (inv != nullptr) inv[pj] = (int32_t)(t * k + j);
+  }
+  for (int j = 0; j < k; ++j) {
+    const int64_t p = __shfl_sync(0xffffffffu, pj, j);
     uint4* dst = out + p * n16;
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
@@ -207,8 +212,8 @@ int launch_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank,
                    const int32_t* S, const int32_t* slot_base, int n_ranks, int tokens_per_rank, int src_rank_base,
                    int G, int E, int k, int d, void* out, int32_t* pos, int32_t* inv, cudaStream_t stream) {
   if (d <= 0 || d % 8 != 0 || d > 8192) return set_error(HM_EINVAL, "permute: need d %% 8 == 0 and d <= 8192");
-  if (n_ranks < 1 || tokens_per_rank < 0 || G < 1 || E < 1 || k < 1)
-    return set_error(HM_EINVAL, "permute: bad sizes");
+  if (n_ranks < 1 || tokens_per_rank < 0 || G < 1 || E < 1 || k < 1 || k > 32)
+    return set_error(HM_EINVAL, "permute: bad sizes (1 <= k <= 32)");
   const int64_t T = (int64_t)n_ranks * tokens_per_rank;
   if (T == 0) return HM_OK;
   const int n16 = d / 8;
