@@ -332,6 +332,7 @@ def run_ours(args, rank, world, local_rank):
 
     wl = WORKLOADS[args.workload]
     d, f, E, k, act, T_total = wl
+    peer_fallback = None
     if args.tokens:  # diagnostics: another batch size of the same layer
         T_total = args.tokens
         wl = (d, f, E, k, act, T_total)
@@ -341,10 +342,20 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
+        from paper_2506_12417_b200.ep import PeerAccessError
+
         cfg = MoEConfig(rank=rank, world_size=world, eq_tokens=args.q, placement=args.placement,
                         transport=args.transport, max_tokens_per_rank=T_total // world,
                         async_fetch=not args.sync_fetch, **cfg_kw)
-        blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
+        try:
+            blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
+        except PeerAccessError as e:  # raised on every rank together: rebuild without peer mappings
+            peer_fallback = f"peer access unavailable ({str(e)[:120]}): NCCL transport, host expert fetch"
+            args.transport = "nccl"
+            cfg = MoEConfig(rank=rank, world_size=world, eq_tokens=args.q, placement=args.placement,
+                            transport="nccl", fetch_source="host", max_tokens_per_rank=T_total // world,
+                            async_fetch=not args.sync_fetch, **cfg_kw)
+            blk = EPHarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
     else:
         cfg = MoEConfig(eq_tokens=args.q, placement=args.placement, logical_ranks=logical_ranks(args), **cfg_kw)
         blk = HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=args.zipf)
@@ -505,7 +516,8 @@ def run_ours(args, rank, world, local_rank):
             "q": args.q, "placement": args.placement, "parallelism": f"ep{world}" if world > 1 else (
                 "single-gpu" if logical_ranks(args) == 1 else f"single-gpu, {logical_ranks(args)} simulated GPUs"),
             "logical_ranks": logical_ranks(args) if world == 1 else None,
-            "transport": (f"{args.transport}" + (" (CUDA graphs)" if ep_graph else " (eager)")) if world > 1 else None,
+            "transport": ((f"{args.transport}" + (" (CUDA graphs)" if ep_graph else " (eager)")) if world > 1
+                          else None) if peer_fallback is None else peer_fallback,
             "l2": "flushed between timed steps (256 MB write)",
             "stages_us": stage_us,
             "block_roofline_tokens_per_sec": roof_tokens,

@@ -87,6 +87,20 @@ def return_tokens(y_recv: torch.Tensor, send_counts, recv_counts, group=None, ou
 # ------------------------------------------------------------------------------------------
 # the block
 # ------------------------------------------------------------------------------------------
+class PeerAccessError(RuntimeError):
+    """CUDA IPC / peer mapping failed on at least one rank.  Raised on EVERY rank at the same
+    point (after a collective agreement), so the caller can rebuild the block with the NCCL
+    transport and host-memory expert fetches without desynchronising the process group."""
+
+
+def _agree_all_ok(ok: bool, group, device) -> bool:
+    """True iff every rank's `ok` is True (one small all_reduce)."""
+    dev = device if dist.get_backend(group) == "nccl" else "cpu"
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    return bool(flag.item())
+
+
 class EPHarMoEnyBlock:
     """One MoE layer sharded by expert over the ranks of `group` (NCCL)."""
 
@@ -177,19 +191,26 @@ class EPHarMoEnyBlock:
         dist.all_gather_object(allh, hs, group=self.group)
         self.peer_in, self.peer_out = [], []
         self._ipc_bases = []
-        for g in range(self.G):
-            if g == self.me:
-                self.peer_in.append(self.w_in.data_ptr())
-                self.peer_out.append(self.w_out.data_ptr())
-                continue
-            ptrs = []
-            for h, off in allh[g]:
-                p = ctypes.c_void_p()
-                _lib.check(L.hm_ipc_open(h, ctypes.byref(p)), "hm_ipc_open")
-                self._ipc_bases.append(p.value)
-                ptrs.append(p.value + off)  # the handle maps the allocation base
-            self.peer_in.append(ptrs[0])
-            self.peer_out.append(ptrs[1])
+        err = None
+        try:
+            for g in range(self.G):
+                if g == self.me:
+                    self.peer_in.append(self.w_in.data_ptr())
+                    self.peer_out.append(self.w_out.data_ptr())
+                    continue
+                ptrs = []
+                for h, off in allh[g]:
+                    p = ctypes.c_void_p()
+                    _lib.check(L.hm_ipc_open(h, ctypes.byref(p)), "hm_ipc_open")
+                    self._ipc_bases.append(p.value)
+                    ptrs.append(p.value + off)  # the handle maps the allocation base
+                self.peer_in.append(ptrs[0])
+                self.peer_out.append(ptrs[1])
+        except Exception as e:  # noqa: BLE001 - re-raised on every rank below
+            err = e
+        if not _agree_all_ok(err is None, self.group, self.device):
+            self._close_peers()
+            raise PeerAccessError(f"peer weight mapping failed on some rank: {err}") from err
 
     # ---------------------------------------------------------------------------------------
     # transport "p2p": one-sided pushes into peer-mapped buffers (NVLink / NVSwitch)
@@ -203,15 +224,28 @@ class EPHarMoEnyBlock:
         allh = [None] * self.G
         dist.all_gather_object(allh, (bytes(buf.raw), int(off.value)), group=self.group)
         addrs = []
-        for g in range(self.G):
-            if g == self.me:
-                addrs.append(t.data_ptr())
-                continue
-            p = ctypes.c_void_p()
-            _lib.check(L.hm_ipc_open(allh[g][0], ctypes.byref(p)), "hm_ipc_open")
-            self._ipc_bases.append(p.value)
-            addrs.append(p.value + allh[g][1])
+        err = None
+        try:
+            for g in range(self.G):
+                if g == self.me:
+                    addrs.append(t.data_ptr())
+                    continue
+                p = ctypes.c_void_p()
+                _lib.check(L.hm_ipc_open(allh[g][0], ctypes.byref(p)), "hm_ipc_open")
+                self._ipc_bases.append(p.value)
+                addrs.append(p.value + allh[g][1])
+        except Exception as e:  # noqa: BLE001 - re-raised on every rank below
+            err = e
+        if not _agree_all_ok(err is None, self.group, self.device):
+            self._close_peers()
+            raise PeerAccessError(f"peer buffer mapping failed on some rank: {err}") from err
         return addrs
+
+    def _close_peers(self):
+        L = _lib.load()
+        for b in getattr(self, "_ipc_bases", []):
+            L.hm_ipc_close(ctypes.c_void_p(b))
+        self._ipc_bases = []
 
     def _setup_p2p(self):
         """Allocate this rank's peer-visible arena (flags, m_all rows, receive buffer + token

@@ -111,3 +111,78 @@ def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
         y0, y1, _, _ = res[r]
         assert np.array_equal(y0, y_ref[r * Tg:(r + 1) * Tg])
         assert np.array_equal(y1, y0)
+
+
+def _fallback_worker(rank, world, port, out_q):
+    import sys
+
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2506_12417_b200 import _lib
+        from paper_2506_12417_b200.block import MoEConfig
+        from paper_2506_12417_b200.ep import EPHarMoEnyBlock, PeerAccessError
+
+        if rank == 1:  # this rank cannot map its peer's memory
+            real_check = _lib.check
+
+            def failing_check(rc, what):
+                if what == "hm_ipc_open":
+                    raise RuntimeError("injected: peer mapping refused")
+                return real_check(rc, what)
+
+            _lib.check = failing_check
+        cfg = MoEConfig(rank=rank, world_size=world, transport="p2p", max_tokens_per_rank=T // world, **KW)
+        raised = False
+        try:
+            EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
+        except PeerAccessError:
+            raised = True
+        cfg = MoEConfig(rank=rank, world_size=world, transport="nccl", fetch_source="host",
+                        max_tokens_per_rank=T // world, **KW)
+        blk = EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
+        g = torch.Generator(device="cuda").manual_seed(99)
+        x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
+        Tg = T // world
+        y = blk(x[rank * Tg:(rank + 1) * Tg].contiguous()).cpu()
+        out_q.put((rank, raised, y.view(torch.int16).numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_access_failure_is_collective():
+    """A rank that cannot map peer memory makes EVERY rank raise PeerAccessError at the same
+    point, so all of them can rebuild with the NCCL transport + host fetch (what bench.py does)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    out_q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, world, port, out_q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, raised, y = out_q.get(timeout=120)
+            res[r] = (raised, y)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+    assert res[0][0] and res[1][0], "both ranks must see the failure"
+    ref = HarMoEnyBlock.random(MoEConfig(**KW), seed=7, device="cuda", zipf_s=1.3, std=0.05)
+    g = torch.Generator(device="cuda").manual_seed(99)
+    x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
+    y_ref = ref(x).cpu().view(torch.int16).numpy()
+    Tg = T // world
+    for r in range(world):
+        assert np.array_equal(res[r][1], y_ref[r * Tg:(r + 1) * Tg])
