@@ -104,9 +104,12 @@ int launch_dispatch_push(const void*, const int32_t*, const int32_t*, const int3
 int launch_fetch_experts(const int32_t*, const int32_t*, const unsigned long long*, const unsigned long long*, size_t,
                          size_t, void*, void*, int, int, int32_t*, int32_t*, int32_t*, int, int, cudaStream_t);
 
+// Flag publish by a kernel (used when stream memory operations are unavailable): the stream
+// order makes every earlier kernel's writes complete first; the system-scope release orders
+// them before the flag for a consumer on another GPU (peer flags over NVLink).
 __global__ void publish_flag_kernel(int32_t* flag, int epoch) {
   __threadfence_system();
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
 }
 
 }  // namespace hm
@@ -217,12 +220,20 @@ int hm_stream_signal(void* const* flags, int n, uint32_t value, void* stream) {
   std::call_once(g_driver_once, load_driver_entry_points);
   if (n < 0 || (n > 0 && flags == nullptr)) return set_error(HM_EINVAL, "stream_signal: bad flag list");
   cudaStream_t s = as_stream(stream);
+  static bool memops_ok = true;  // cleared once the driver refuses a stream write (e.g. to peer memory)
   for (int i = 0; i < n; ++i) {
-    if (g_write32 != nullptr) {
+    if (g_write32 != nullptr && memops_ok) {
       const CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flags[i]),
                                    (cuuint32_t)value, CU_STREAM_WRITE_VALUE_DEFAULT);
-      if (r != CUDA_SUCCESS) return set_error(HM_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
-    } else {
+      if (r == CUDA_ERROR_NOT_SUPPORTED || r == CUDA_ERROR_INVALID_VALUE) {
+        memops_ok = false;  // fall through to the kernel publish for this and later flags
+      } else if (r != CUDA_SUCCESS) {
+        return set_error(HM_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+      } else {
+        continue;
+      }
+    }
+    {
       publish_flag_kernel<<<1, 1, 0, s>>>(reinterpret_cast<int32_t*>(flags[i]), (int)value);
       const int rc = check_launch("stream_signal");
       if (rc) return rc;
