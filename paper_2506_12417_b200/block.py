@@ -1,14 +1,16 @@
 """The HarMoEny MoE block on B200: Alg. 1 as a chain of
 hand-written sm_100a kernels behind the C ABI.
 
-    forward(x):                                   kernels (csrc/)
+    forward(x) (LOCAL, this module):              kernels (csrc/)
       1 router: logits, top-k, weights            hm_router_topk      (K1, tcgen05)
         per-tile histogram + (token,slot) ranks   (fused K2)
-      2 metadata exchange m_all                   hm_hist_scan + all_gather (EP)
-      3 schedule S = rebalance(initial_assign)    hm_schedule         (K3, bit-exact)
-      4 scatter tokens                            hm_dispatch_layout + hm_permute (K4) + all_to_all (EP)
-      5 experts (+ async fetch)                   hm_grouped_gemm x2  (K5, tcgen05) + hm_fetch_expert (K6)
-      6 gather + reconstruct                      all_to_all (EP) + hm_combine (K7)
+      2+3 metadata, schedule S, layout            hm_plan: histogram reduce + K3 (bit-exact) + layout
+      4 scatter tokens                            hm_permute (K4): index-only when FFN1 gathers rows
+                                                  itself (top_k >= 4, >= 256 rows/expert), else copies
+      5 experts                                   hm_grouped_gemm x2  (K5, tcgen05 cta_group::2)
+      6 gather + reconstruct                      FFN2 rows land token-major; hm_combine (K7)
+    EP (ep.py) adds the metadata exchange, the dispatch / return over NVLink (or NCCL) and the
+    async expert fetch (K6).
 
 Two placements of the G ranks:
 
