@@ -119,7 +119,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw.instant,power.limit"
 
     def __init__(self, index: int, enabled: bool = True):
         self.index, self.enabled, self.proc, self.lines = index, enabled, None, []
@@ -149,7 +149,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw, plim = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -160,12 +160,21 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:]):
+            if len(parts) >= 8:
+                try:
+                    pw.append(float(parts[6]))
+                    plim = float(parts[7])
+                except ValueError:
+                    pass
+            for n, v in zip(names, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:  # board power during the timed loop (is the step at the power cap?)
+            out.update(power_w_median=float(np.median(pw)), power_w_max=float(np.max(pw)), power_limit_w=plim)
+        return out
 
 
 # ------------------------------------------------------------------------------------------
