@@ -274,16 +274,18 @@ def round_bf16(x) -> np.ndarray:
 # --------------------------------------------------------------------------------------------
 # numeric stages (restatement; rounding points mirror the CUDA kernels)
 # --------------------------------------------------------------------------------------------
-def router(x_bits, wg_bits, bias, k: int, renormalize: bool):
+def router(x_bits, wg_bits, bias, k: int, renormalize: bool, idx=None):
     """Step 1.  logits = x Wg^T (+bias) in fp32; top-k over the
     fp32 logits with lowest-index ties; weights = softmax probabilities of the
-    selected experts (renormalised over the k when ``renormalize``)."""
+    selected experts (renormalised over the k when ``renormalize``).  ``idx`` [T, k]
+    overrides the selection (the weights are still the oracle's softmax at those experts):
+    used to check the rest of the block on tokens whose top-k is an oracle near-tie."""
     x = bf16_to_f32(x_bits)
     wg = bf16_to_f32(wg_bits)
     logits = (x.astype(np.float64) @ wg.T.astype(np.float64)).astype(np.float32)
     if bias is not None:
         logits = (logits + np.asarray(bias, np.float32)[None, :]).astype(np.float32)
-    idx = topk_lowest_index(logits, k)
+    idx = topk_lowest_index(logits, k) if idx is None else np.asarray(idx, np.int64)
     mx = logits.max(axis=1, keepdims=True)
     ex = np.exp((logits - mx).astype(np.float32))
     p = ex / ex.sum(axis=1, keepdims=True, dtype=np.float32)
@@ -296,6 +298,38 @@ def router(x_bits, wg_bits, bias, k: int, renormalize: bool):
 def topk_lowest_index(logits, k: int) -> np.ndarray:
     order = np.argsort(-logits, axis=1, kind="stable")
     return order[:, :k]
+
+
+def topk_min_gap(logits, k: int) -> np.ndarray:
+    """Smallest gap between consecutive sorted logits among the top k+1 per row: the top-k
+    SET and ORDER are decided by gaps at least this large (inf when k == E == 1)."""
+    s = -np.sort(-np.asarray(logits, np.float64), axis=1)
+    kk = min(k + 1, logits.shape[1])
+    if kk < 2:
+        return np.full(logits.shape[0], np.inf)
+    return np.min(s[:, : kk - 1] - s[:, 1:kk], axis=1)
+
+
+NEAR_TIE_REL = 1e-4  # a top-k decided by a logit gap below this * max(1, max|logit|) is a near tie
+
+
+def routing_parity(idx_gpu, logits, idx_ref, k: int):
+    """Strict routing check (SURVEY.md §7 "Hard parts"): the GPU's top-k must equal the
+    oracle's on every token, except tokens whose oracle top-k is decided by a near tie
+    (gap < NEAR_TIE_REL * max(1, max|logit|) of the row).  Returns (agree mask, number of
+    near-tie tokens, number of disagreeing tokens); raises AssertionError on any
+    disagreement outside the near ties."""
+    idx_gpu = np.asarray(idx_gpu)
+    agree = np.all(idx_gpu == np.asarray(idx_ref), axis=1)
+    gap = topk_min_gap(logits, k)
+    near = gap < NEAR_TIE_REL * np.maximum(1.0, np.abs(np.asarray(logits, np.float64)).max(axis=1))
+    bad = ~agree & ~near
+    if bad.any():
+        t = int(np.nonzero(bad)[0][0])
+        raise AssertionError(f"router: {int(bad.sum())} tokens disagree with the oracle outside near ties "
+                             f"(first t={t}: gpu {idx_gpu[t].tolist()} oracle {np.asarray(idx_ref)[t].tolist()}, "
+                             f"gap {gap[t]:.3e})")
+    return agree, int(near.sum()), int((~agree).sum())
 
 
 def topk_margin(logits, k: int) -> np.ndarray:
@@ -323,11 +357,13 @@ def expert_ffn(xe_f32, w1_bits, w2_bits, act: str, w3_bits=None):
     return round_bf16(y.astype(np.float32))
 
 
-def moe_block(x_bits, wg_bits, bias, w1_bits, w2_bits, k, act, renormalize, w3_bits=None, return_scale=False):
+def moe_block(x_bits, wg_bits, bias, w1_bits, w2_bits, k, act, renormalize, w3_bits=None, return_scale=False,
+              idx=None):
     """Full single-rank block: router -> per-expert FFN -> weighted combine.
     The schedule never changes the math (each token row is computed by its
-    expert's weights wherever it runs), so the oracle output is G-independent."""
-    logits, idx, w = router(x_bits, wg_bits, bias, k, renormalize)
+    expert's weights wherever it runs), so the oracle output is G-independent.
+    ``idx`` overrides the routing (see ``router``)."""
+    logits, idx, w = router(x_bits, wg_bits, bias, k, renormalize, idx=idx)
     x = bf16_to_f32(x_bits)
     T = x.shape[0]
     E = wg_bits.shape[0]

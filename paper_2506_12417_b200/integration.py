@@ -104,10 +104,31 @@ class HarMoEnyLayer(nn.Module):
         return y
 
 
+def _routing_config(moe_module: nn.Module, router, config: MoEConfig) -> MoEConfig:
+    """Take the routing semantics from the module being replaced: ``norm_topk_prob`` (HF
+    Qwen2/Qwen3-MoE routers; shipped Qwen1.5/2-MoE checkpoints use False) sets
+    ``renormalize``, and a module ``top_k`` / ``num_experts_per_tok`` that disagrees with the
+    config is an error rather than a silent change of the routing."""
+    import dataclasses
+
+    for obj in (router, moe_module):
+        k = getattr(obj, "top_k", None) or getattr(obj, "num_experts_per_tok", None)
+        if isinstance(k, int) and k != config.top_k:
+            raise ValueError(f"MoEConfig.top_k={config.top_k} but the replaced module routes top-{k}")
+    for obj in (router, moe_module):
+        ntp = getattr(obj, "norm_topk_prob", None)
+        if isinstance(ntp, bool):
+            if ntp != config.renormalize:
+                config = dataclasses.replace(config, renormalize=ntp)
+            break
+    return config
+
+
 def build_block(moe_module: nn.Module, path_to_experts: str, path_to_router_linear_layer: str, config: MoEConfig,
                 device=None):
     experts = _get_path(moe_module, path_to_experts)
     router = _get_path(moe_module, path_to_router_linear_layer)
+    config = _routing_config(moe_module, router, config)
     wg = router.weight.detach() if isinstance(router, nn.Module) else router.detach()
     w1, w2, w3 = extract_expert_weights(experts, config.activation, d_model=wg.shape[-1])
     if config.world_size > 1:
@@ -168,10 +189,14 @@ def patch_moesim(moesim_module=None):
         from . import ops
         from .policies import _to_i32
 
-        home = np.asarray(placement.home, np.int64)
-        if config.policy is moesim_module.SchedulingPolicy.EVEN_SPLIT:  # engine.py:292-293
+        if config.policy is moesim_module.SchedulingPolicy.EVEN_SPLIT:  # engine.py:292-293 (placement unused)
             policy, home = ops.HM_POLICY_EVEN_SPLIT, np.zeros(m_all.num_experts, np.int64)
         else:
+            # the reference's initial_assign check (policies.py:111-112): never hand the kernel
+            # a home vector of the wrong length or with ranks outside the routing matrix
+            if placement.num_experts != m_all.num_experts or placement.num_gpus != m_all.num_gpus:
+                raise ValueError("placement dimensions do not match routing matrix")
+            home = np.asarray(placement.home, np.int64)
             do_rb = config.policy is moesim_module.SchedulingPolicy.REBALANCE and flags.rebalancing_enabled
             policy = ops.HM_POLICY_REBALANCE if do_rb else ops.HM_POLICY_NONE
         S, _, _ = ops.schedule(_to_i32(m_all.counts, "build_schedule"), _to_i32(home, "home"),

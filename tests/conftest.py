@@ -36,3 +36,72 @@ def golden():
         return dict(np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False))
 
     return load
+
+
+# ------------------------------------------------------------------------------------------
+# strict block parity against the oracle (GPU tests)
+# ------------------------------------------------------------------------------------------
+ATOL, RTOL, FROB = 1e-2, 2e-2, 5e-3  # BASELINE.md §2 / SURVEY.md §8(c) stated bar
+
+
+def _bits(t):
+    return t.contiguous().view(__import__("torch").int16).cpu().numpy().view(np.uint16)
+
+
+def block_weight_bits(blk):
+    """(wg, w1, w2, w3, bias) of a HarMoEnyBlock as the oracle takes them (bf16 bit patterns)."""
+    cfg = blk.cfg
+    E, f, d = cfg.num_experts, cfg.d_ff, cfg.d_model
+    wg = _bits(blk.wg[:E])
+    if cfg.activation == "swiglu":
+        w13 = _bits(blk.w_in).reshape(E, f // 128, 2, 128, d)
+        w1, w3 = w13[:, :, 0].reshape(E, f, d), w13[:, :, 1].reshape(E, f, d)
+    else:
+        w1, w3 = _bits(blk.w_in).reshape(E, f, d), None
+    w2 = _bits(blk.w_out).reshape(E, d, f)
+    bias = None if blk.bias is None else blk.bias.cpu().numpy()
+    return wg, w1, w2, w3, bias
+
+
+def check_block_parity(blk, x, y, idx_gpu, rows=None, residual=None, what="", scale_bar=False):
+    """The strict bar for a block forward (VERDICT r1 'next' #1):
+
+    * routing: the GPU's top-k equals the oracle's on EVERY token of ``x`` except oracle near
+      ties (``orc.routing_parity``; the near-tie count is printed);
+    * output: on ``rows`` (default all tokens) the oracle block evaluated WITH THE GPU'S
+      ROUTING (so near-tie tokens are checked too) meets |y - y_ref| <= 1e-2 + 2e-2 |y_ref|
+      elementwise and relative Frobenius <= 5e-3.  ``scale_bar`` reports the stated
+      elementwise bar's worst ratio and enforces the bar relative to sum_j w_j |Y_j| instead
+      (Mixtral's K = 14336 expert outputs).
+    Returns a dict of the measured figures."""
+    from oracle import moe_oracle as orc
+
+    cfg = blk.cfg
+    k = cfg.top_k
+    wg, w1, w2, w3, bias = block_weight_bits(blk)
+    xb = _bits(x)
+    logits, idx_ref, _ = orc.router(xb, wg, bias, k, cfg.renormalize)
+    idx_gpu = np.asarray(idx_gpu)
+    agree, n_near, n_diff = orc.routing_parity(idx_gpu, logits, idx_ref, k)
+    rows = np.arange(xb.shape[0]) if rows is None else np.asarray(rows)
+    y_ref, _, _, _, scale = orc.moe_block(xb[rows], wg, bias, w1, w2, k, cfg.activation, cfg.renormalize, w3,
+                                          return_scale=True, idx=idx_gpu[rows])
+    yr = orc.bf16_to_f32(y_ref).astype(np.float64)
+    if residual is not None:
+        yr = yr + orc.bf16_to_f32(_bits(residual)[rows]).astype(np.float64)
+    yg = orc.bf16_to_f32(_bits(y)[rows]).astype(np.float64)
+    err = np.abs(yg - yr)
+    stated = ATOL + RTOL * np.abs(yr)
+    worst_stated = float((err / stated).max()) if err.size else 0.0
+    frob = float(np.linalg.norm(yg - yr) / max(np.linalg.norm(yr), 1e-30))
+    out = dict(tokens=int(xb.shape[0]), checked_rows=int(len(rows)), near_ties=n_near, disagree=n_diff,
+               max_err=float(err.max()) if err.size else 0.0, worst_ratio_stated=worst_stated, frob=frob)
+    print(f"[parity] {what}: {out}")
+    if scale_bar:
+        bound = ATOL + RTOL * scale.astype(np.float64)
+        assert np.all(err <= bound), f"{what}: worst ratio vs sum_j w_j|Y_j| bar {(err / bound).max()}"
+    else:
+        assert np.all(err <= stated), (f"{what}: {(err > stated).sum()} elements out of the stated bar, "
+                                       f"worst ratio {worst_stated:.3f}, max |dy| {err.max():.3e}")
+    assert frob <= FROB, f"{what}: relative Frobenius error {frob}"
+    return out

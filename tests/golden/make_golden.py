@@ -20,6 +20,8 @@ scheduler kernel are pinned to the reference, not to a restatement:
                         (workload.py:183-232), resampled alpha, 5 batches x 3 layers
 * trace_g4_e16_schedules.npz - the reference build_schedule (engine.py:287-299)
                         of every (batch, layer) of that trace, per placement and q
+* wide_schedules.npz  - totals >= 2^21 tokens and G*E*G beyond shared memory (the
+                        64-bit rebalance loop of the CUDA scheduler)
 * baseline_policies.npz - even_split_assign (policies.py:174-203) on the
                         baseline-shape + acceptance matrices; affinity_placement
                         (policies.py:206-229) on random popularity profiles
@@ -126,6 +128,38 @@ def baseline_shapes():
                     for q in (1, 32, 256, 1499):
                         out.append(_run(m, home, q))
                         names.append(f"{name}|s={s}|G={G}|{pl}|q={q}")
+    d = _pack(out)
+    d["names"] = np.array(names)
+    return d
+
+
+def wide_schedules():
+    """Instances that leave the CUDA scheduler's packed 32-bit fast loop: totals >= 2^21
+    tokens (the (value, index) keys no longer fit 32 bits) and G*E*G too large for the
+    shared-memory copy (2*G*E*G*4 B > 200 KB, S scanned in global memory).  Both take the
+    64-bit loop of hm_sched.cu; the reference answers come from moesim itself."""
+    out, names = [], []
+    rng = np.random.default_rng(2021)
+    # BASELINE shapes at 2^21+ assignments (Zipf top-k, blocked = hot experts on GPU 0)
+    for (E, k, G, Tg, s) in ((128, 8, 8, 40000, 1.0), (128, 1, 4, 600000, 1.5), (8, 2, 8, 140000, 0.5),
+                             (128, 8, 2, 140000, 0.0)):
+        m = zipf_routing_matrix(G, Tg, E, k, s, 11)
+        assert m.sum() >= 1 << 21
+        for pl in ("round_robin", "blocked"):
+            home = (round_robin_placement if pl == "round_robin" else blocked_placement)(E, G).home
+            for q in (1, 32, 1499):
+                out.append(_run(m, home, q))
+                names.append(f"E={E}|k={k}|G={G}|Tg={Tg}|s={s}|{pl}|q={q}")
+    # S too large for shared memory: G=16/E=256, G=32/E=64, G=12/E=512 (random skew, small and
+    # large totals)
+    for (G, E) in ((16, 256), (32, 64), (12, 512)):
+        for tokens in (50_000, 3_000_000):
+            probs = rng.dirichlet(np.full(G * E, 0.3))
+            m = rng.multinomial(tokens, probs).reshape(G, E)
+            home = [int(x) for x in rng.integers(0, G, size=E)]
+            for q in (1, 17):
+                out.append(_run(m, home, q))
+                names.append(f"G={G}|E={E}|tokens={tokens}|q={q}")
     d = _pack(out)
     d["names"] = np.array(names)
     return d
@@ -238,7 +272,7 @@ def main():
     print("moesim", moesim.__version__, "numpy", np.__version__)
     for name, fn in [("fig4", fig4), ("acceptance_c2", acceptance_c2), ("baseline_shapes", baseline_shapes),
                      ("plan_order", plan_order), ("trace_g4_e16_schedules", trace_files),
-                     ("baseline_policies", baseline_policies)]:
+                     ("baseline_policies", baseline_policies), ("wide_schedules", wide_schedules)]:
         if len(sys.argv) > 1 and name not in sys.argv[1:]:  # regenerate only the named fixtures
             continue
         d = fn()

@@ -151,3 +151,51 @@ def test_extract_expert_weights_hf_layouts():
     assert torch.equal(w2[2], hf.down_proj[2])
     with pytest.raises(ValueError):
         extract_expert_weights(Fused(), "swiglu", d_model=5)
+
+
+def test_patch_moesim_rejects_mismatched_placement():
+    """The patched build_schedule keeps the reference's dimension check (policies.py:111-112)
+    instead of handing the kernel an out-of-range home vector (checked before any GPU call)."""
+    import sys
+
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "moesim")):
+        pytest.skip("reference not installed in baseline/_ref")
+    sys.path.insert(0, ref)
+    import moesim
+
+    from paper_2506_12417_b200.integration import patch_moesim
+
+    restore = patch_moesim(moesim)
+    try:
+        m = moesim.RoutingMatrix(np.ones((2, 4), np.int64))
+        cfg = moesim.SchedulerConfig(token_threshold_q=1)
+        for pl in (moesim.round_robin_placement(4, 3), moesim.round_robin_placement(5, 2)):
+            with pytest.raises(ValueError, match="placement dimensions"):
+                moesim.engine.build_schedule(m, pl, cfg, moesim.SimFlags())
+    finally:
+        restore()
+
+
+def test_replace_moe_layer_takes_routing_semantics_from_the_module():
+    """norm_topk_prob of the replaced HF router sets MoEConfig.renormalize (shipped Qwen2-MoE
+    checkpoints use False); a top_k that disagrees with the module is an error."""
+    import torch
+    from torch import nn
+
+    from paper_2506_12417_b200 import MoEConfig
+    from paper_2506_12417_b200.integration import _routing_config
+
+    class Router(nn.Module):
+        def __init__(self, k, ntp):
+            super().__init__()
+            self.top_k, self.norm_topk_prob = k, ntp
+            self.weight = nn.Parameter(torch.zeros(16, 256))
+
+    cfg = MoEConfig(d_model=256, num_experts=16, d_ff=256, top_k=4)
+    assert cfg.renormalize is True
+    assert _routing_config(nn.Module(), Router(4, False), cfg).renormalize is False
+    assert _routing_config(nn.Module(), Router(4, True), cfg).renormalize is True
+    assert _routing_config(nn.Module(), nn.Linear(256, 16), cfg).renormalize is True  # no attribute: keep
+    with pytest.raises(ValueError, match="top-2"):
+        _routing_config(nn.Module(), Router(2, True), cfg)

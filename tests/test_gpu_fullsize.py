@@ -9,7 +9,8 @@ The oracle cannot run a 16k-token Qwen-128 block in seconds, so at the named sha
 * the block output is bit-identical whatever the schedule (harmony / static / even split)
   and however many logical GPUs the batch is split over: the schedule moves rows between
   GPUs, never changes their math;
-* a sample of tokens matches the oracle within the stated bf16 tolerance.
+* routing equals the oracle's on every token outside near ties, and 1,024 sampled tokens
+  match the oracle block within the stated bar (1e-2 + 2e-2|y_ref|, Frobenius <= 5e-3).
 """
 
 import numpy as np
@@ -17,6 +18,7 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
+from conftest import check_block_parity  # noqa: E402
 from oracle import moe_oracle as orc  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -40,12 +42,13 @@ def bits(t):
     return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-@pytest.mark.parametrize("name", ["switch128", "qwen128", "mixtral8"])
-def test_fullsize_properties(name):
+@pytest.mark.parametrize("name,T", [("switch128", 4096), ("qwen128", 16384), ("mixtral8", 4096),
+                                    ("mixtral8", 16384)])
+def test_fullsize_properties(name, T):
     from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig, random_weights
 
     dev = _cuda()
-    d, f, E, k, act, T, G = SHAPES[name]
+    d, f, E, k, act, _, G = SHAPES[name]
     q = 4 if name == "switch128" else 32  # below the (source, expert) bucket sizes
     x = torch.randn((T, d), device=dev, generator=torch.Generator(device=dev).manual_seed(5)).to(torch.bfloat16)
     base = dict(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q, placement="blocked")
@@ -74,28 +77,12 @@ def test_fullsize_properties(name):
             pos = inv.cpu().numpy().reshape(-1)
             assert np.array_equal(np.sort(pos), np.arange(T * k)), "scatter positions must be a permutation"
         if (ranks, policy) == (G, "harmony"):
+            # routing exact on ALL T tokens outside oracle near ties; the output of >= 1024
+            # sampled tokens (oracle evaluated with the GPU's routing) within the stated bar
             idx = st.extras["topk_idx"].cpu().numpy()
-            sample = np.linspace(0, T - 1, 12).astype(int)
-            wg = bits(blk.wg[:E])
-            if act == "swiglu":
-                w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, d)
-                w1, w3 = w13[:, :, 0].reshape(E, f, d), w13[:, :, 1].reshape(E, f, d)
-            else:
-                w1, w3 = bits(blk.w_in).reshape(E, f, d), None
-            w2 = bits(blk.w_out).reshape(E, d, f)
-            y_ref, idx_ref, _, _, scale = orc.moe_block(bits(x)[sample], wg, blk.bias.cpu().numpy(), w1, w2, k,
-                                                        act, blk.cfg.renormalize, w3, return_scale=True)
-            ok = np.all(idx[sample] == idx_ref, axis=1)
-            assert ok.mean() >= 0.75, f"router indices disagree on {(~ok).sum()} of {len(sample)} sampled tokens"
-            yg = orc.bf16_to_f32(bits(y)[sample])[ok].astype(np.float64)
-            yr = orc.bf16_to_f32(y_ref)[ok].astype(np.float64)
-            err = np.abs(yg - yr)
-            # elementwise bar relative to the magnitude of the combined terms sum_j w_j |Y_j|
-            # (Mixtral's d_ff = 14336 reductions: one bf16 ulp of a Y_j survives a cancelling sum)
-            bound = ATOL + RTOL * scale[ok].astype(np.float64)
-            assert np.all(err <= bound), f"{name}: max |dy| {err.max()}, worst ratio {(err / bound).max()}"
-            frob = np.linalg.norm(yg - yr) / max(np.linalg.norm(yr), 1e-30)
-            assert frob <= 5e-3, f"{name}: relative Frobenius error {frob}"
+            sample = np.linspace(0, T - 1, 1024).astype(int)
+            figures = check_block_parity(blk, x, y, idx, rows=sample, what=f"{name} T={T} G={G}")
+            assert figures["checked_rows"] >= 1024
         del blk
         torch.cuda.empty_cache()
     ref = outs[(G, "harmony")]

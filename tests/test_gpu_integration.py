@@ -38,6 +38,28 @@ def _moesim():
     return moesim
 
 
+def _assert_hf_parity(got, ref, x, gate_w, k, what):
+    """The stated bar (|y - y_ref| <= 1e-2 + 2e-2 |y_ref| elementwise, relative
+    Frobenius <= 5e-3) against the module's own fp32 forward, on every token except those whose
+    top-k, computed in fp64 from the module's gate weights, is decided by a near tie (there the
+    fp32 HF router and the bf16-input tcgen05 router may legitimately pick different experts;
+    the near-tie count is printed)."""
+    from oracle import moe_oracle as orc
+
+    d = x.shape[-1]
+    logits = x.reshape(-1, d).double().cpu().numpy() @ gate_w.detach().double().cpu().numpy().T
+    near = orc.topk_min_gap(logits, k) < orc.NEAR_TIE_REL * np.maximum(1.0, np.abs(logits).max(axis=1))
+    g = got.reshape(-1, d).double().cpu().numpy()[~near]
+    r = ref.reshape(-1, d).double().cpu().numpy()[~near]
+    err = np.abs(g - r)
+    bar = 1e-2 + 2e-2 * np.abs(r)
+    frob = float(np.linalg.norm(g - r) / np.linalg.norm(r))
+    print(f"[hf parity] {what}: {int(near.sum())} near-tie tokens of {len(near)}, worst ratio "
+          f"{float((err / bar).max()):.3f}, Frobenius {frob:.2e}")
+    assert np.all(err <= bar), f"{what}: {(err > bar).sum()} elements out of the stated bar"
+    assert frob <= 5e-3, f"{what}: relative Frobenius error {frob}"
+
+
 def test_patch_moesim_simulate_run_identical():
     _cuda()
     moesim = _moesim()
@@ -148,14 +170,13 @@ def test_replace_moe_layer_matches_torch_reference():
     x = torch.randn((4, 64, d), device=dev).to(torch.bfloat16).float()
     with torch.no_grad():
         ref = model[0](x)
+    gate_w = model[0].mlp.gate.weight.detach().clone()
     cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=k, activation="swiglu", eq_tokens=8)
     n = replace_moe_layer(model, _Layer, _MoE, "experts", "gate", cfg, device=dev)
     assert n == 2
     with torch.no_grad():
         got = model[0](x)
-    err = (got - ref).abs()
-    tol = 2e-2 + 3e-2 * ref.abs()
-    assert (err <= tol).float().mean() > 0.98  # near-tie routing flips aside
+    _assert_hf_parity(got - x, ref - x, x, gate_w, k, "torch MoE layer")
 
 
 def _hf_reference_block(block_cls, config, dev):
@@ -167,7 +188,7 @@ def _hf_reference_block(block_cls, config, dev):
     return blk
 
 
-@pytest.mark.parametrize("arch", ["qwen3_moe", "mixtral", "qwen2_moe"])
+@pytest.mark.parametrize("arch", ["qwen3_moe", "mixtral", "qwen2_moe", "qwen2_moe_hf_default"])
 def test_replace_moe_layer_on_transformers_blocks(arch):
     """The paper's drop-in API on the real transformers 5 MoE blocks (fused [E, 2f, d] experts,
     TopK routers): the B200 block reproduces the HF block's own forward within the bf16 bar."""
@@ -175,12 +196,16 @@ def test_replace_moe_layer_on_transformers_blocks(arch):
     from paper_2506_12417_b200 import MoEConfig, replace_moe_layer
 
     d, f, E, k = 256, 256, 16, 2 if arch == "mixtral" else 4
-    if arch == "qwen2_moe":  # the paper's Qwen family: routed experts + a gated shared expert
+    if arch.startswith("qwen2_moe"):  # the paper's Qwen family: routed experts + a gated shared expert
         from transformers.models.qwen2_moe.configuration_qwen2_moe import Qwen2MoeConfig as C
         from transformers.models.qwen2_moe.modeling_qwen2_moe import Qwen2MoeSparseMoeBlock as B
 
+        # "qwen2_moe_hf_default": the config's own default norm_topk_prob (False, as shipped
+        # Qwen1.5/2-MoE checkpoints) - the replaced layer must not renormalise the top-k weights
+        extra = {} if arch == "qwen2_moe_hf_default" else dict(norm_topk_prob=True)
         conf = C(hidden_size=d, moe_intermediate_size=f, shared_expert_intermediate_size=512, num_experts=E,
-                 num_experts_per_tok=k, norm_topk_prob=True)
+                 num_experts_per_tok=k, **extra)
+        assert arch != "qwen2_moe_hf_default" or conf.norm_topk_prob is False
     elif arch == "qwen3_moe":
         from transformers.models.qwen3_moe.configuration_qwen3_moe import Qwen3MoeConfig as C
         from transformers.models.qwen3_moe.modeling_qwen3_moe import Qwen3MoeSparseMoeBlock as B
@@ -204,16 +229,15 @@ def test_replace_moe_layer_on_transformers_blocks(arch):
     x = torch.randn((2, 96, d), device=dev).to(torch.bfloat16).float()
     with torch.no_grad():
         ref = model(x)
-    cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=k, activation="swiglu", eq_tokens=4, renormalize=True)
+    gate_w = model.mlp.gate.weight.detach().clone()
+    # renormalize is taken from the module's norm_topk_prob where it has one (Qwen2/3-MoE)
+    cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=k, activation="swiglu", eq_tokens=4)
     assert replace_moe_layer(model, Parent, B, "experts", "gate", cfg, device=dev) == 1
+    assert model.mlp.block.cfg.renormalize is (arch != "qwen2_moe_hf_default")
     with torch.no_grad():
         got = model(x)
     assert got.shape == ref.shape
-    err = (got - ref).abs()
-    tol = 2e-2 + 3e-2 * ref.abs()
-    assert (err <= tol).float().mean() > 0.98, f"{arch}: {(err > tol).float().mean():.3%} out of tolerance"
-    frob = float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref))
-    assert frob < 3e-2, f"{arch}: relative Frobenius error {frob}"
+    _assert_hf_parity(got, ref, x, gate_w, k, arch)
 
 
 def test_replace_moe_layer_in_a_transformers_model():
@@ -273,12 +297,10 @@ def test_replace_moe_layer_on_switch_transformers():
     x = torch.randn((1, T, d), device=dev).to(torch.bfloat16).float()
     with torch.no_grad():
         ref = model(x)
+    gate_w = model.mlp.router.classifier.weight.detach().clone()
     cfg = MoEConfig(d_model=d, num_experts=E, d_ff=f, top_k=1, activation="relu", eq_tokens=4)
     assert replace_moe_layer(model, Parent, SwitchTransformersSparseMLP, "experts", "router.classifier", cfg,
                              device=dev) == 1
     with torch.no_grad():
         got = model(x)
-    err = (got - ref).abs()
-    tol = 2e-2 + 3e-2 * ref.abs()
-    assert (err <= tol).float().mean() > 0.98
-    assert float(torch.linalg.norm(got - ref) / torch.linalg.norm(ref)) < 3e-2
+    _assert_hf_parity(got, ref, x, gate_w, 1, "switch_transformers")

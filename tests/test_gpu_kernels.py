@@ -10,7 +10,7 @@ import pytest
 
 torch = pytest.importorskip("torch")
 
-from conftest import iter_packed  # noqa: E402
+from conftest import check_block_parity, iter_packed  # noqa: E402
 from oracle import moe_oracle as orc  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -41,7 +41,7 @@ def assert_close(y, y_ref, what=""):
 # ------------------------------------------------------------------------------------------
 # K3 scheduler
 # ------------------------------------------------------------------------------------------
-@pytest.mark.parametrize("pack", ["fig4", "acceptance_c2", "baseline_shapes"])
+@pytest.mark.parametrize("pack", ["fig4", "acceptance_c2", "baseline_shapes", "wide_schedules"])
 def test_schedule_kernel_bit_exact(golden, pack):
     from paper_2506_12417_b200 import ops
 
@@ -58,6 +58,27 @@ def test_schedule_kernel_bit_exact(golden, pack):
         n += 1
         if pack == "acceptance_c2" and n >= 600:
             break
+
+
+def test_fused_planner_wide_totals_bit_exact(golden):
+    """The fused planner (hm_plan, m_all given) also leaves the packed 32-bit loop once the
+    batch holds >= 2^21 assignments; S / iterations / loads still equal moesim's."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    n = 0
+    for inst in iter_packed(golden("wide_schedules")):
+        G, E = inst["m"].shape
+        if 2 * G * E * G * 4 > 64 * 1024 or inst["m"].sum() < (1 << 21):
+            continue
+        m = torch.from_numpy(inst["m"].astype(np.int32)).to(dev)
+        home = torch.from_numpy(inst["home"].astype(np.int32)).to(dev)
+        p = ops.plan(home, G, E, inst["q"], True, ops.HM_LAYOUT_LOCAL, m_all=m)
+        assert np.array_equal(p.S.cpu().numpy(), inst["S"]), f"instance {inst['i']}"
+        assert int(p.iters.item()) == inst["iters"]
+        assert np.array_equal(p.loads.cpu().numpy(), inst["S"].sum(axis=(0, 1)))
+        n += 1
+    assert n >= 20
 
 
 def test_even_split_kernel_bit_exact(golden):
@@ -169,11 +190,9 @@ def test_router_topk_hist(E, k, d, n_ranks, Tg, bias, integer):
     if integer:
         assert np.array_equal(idx, idx_ref)
     else:
-        margin = orc.topk_margin(logits, k)
-        ok = margin > 1e-4 * np.maximum(1.0, np.abs(logits).max(axis=1))
-        assert ok.mean() > 0.95
-        # exact set and order wherever the top-k is not a near tie
-        assert np.array_equal(idx[ok], idx_ref[ok])
+        # exact set and order on every token whose top-k is not an oracle near tie
+        _, n_near, n_diff = orc.routing_parity(idx, logits, idx_ref, k)
+        print(f"[router] E={E} k={k}: {n_near} near-tie tokens, {n_diff} differ (all near ties)")
     np.testing.assert_allclose(w.cpu().numpy()[np.all(idx == idx_ref, axis=1)],
                                w_ref[np.all(idx == idx_ref, axis=1)], rtol=2e-5, atol=1e-6)
     # histogram + ranks are exact functions of the GPU's own indices
@@ -282,24 +301,11 @@ def test_block_matches_oracle(arch, G):
         torch.bfloat16)
     y = blk(x)
     torch.cuda.synchronize()
-    # oracle on identical bf16 inputs
-    E, f, d = cfg.num_experts, cfg.d_ff, cfg.d_model
-    wg = bits(blk.wg[:E])
-    if cfg.activation == "swiglu":
-        w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, d)
-        w1 = w13[:, :, 0].reshape(E, f, d)
-        w3 = w13[:, :, 1].reshape(E, f, d)
-    else:
-        w1 = bits(blk.w_in).reshape(E, f, d)
-        w3 = None
-    w2 = bits(blk.w_out).reshape(E, d, f)
-    bias = None if blk.bias is None else blk.bias.cpu().numpy()
-    y_ref, idx_ref, w_ref, logits = orc.moe_block(bits(x), wg, bias, w1, w2, cfg.top_k, cfg.activation,
-                                                  cfg.renormalize, w3)
+    # oracle on identical bf16 inputs: routing exact outside near ties, every token's output
+    # within the stated bar (near-tie tokens evaluated with the GPU's routing)
+    E = cfg.num_experts
     idx = blk.stats.extras["topk_idx"].cpu().numpy()
-    agree = np.all(idx == idx_ref, axis=1)
-    assert agree.mean() > 0.97
-    assert_close(orc.bf16_to_f32(bits(y))[agree], orc.bf16_to_f32(y_ref)[agree], f"block {arch} G={G}")
+    check_block_parity(blk, x, y, idx, what=f"block {arch} G={G}")
     # schedule of the block == oracle schedule on the GPU's histogram
     m_all = blk.stats.m_all.cpu().numpy()
     S_ref, it_ref = orc.schedule(m_all, blk.home_np, cfg.eq_tokens, True)
@@ -399,21 +405,14 @@ def test_stack_matches_oracle_and_graph():
     x = torch.randn((512, 256), device=dev).to(torch.bfloat16)
     y = st(x).clone()
     torch.cuda.synchronize()
-    E, f, d = 16, 256, 256
     h_gpu = x
     for blk in st.layers:
         # each layer checked on the GPU's own input (near-tie routing flips would otherwise
         # compound across layers); residual: kernel accumulates x + sum_j w Y_j in fp32
         h_next = blk(h_gpu).clone()
         torch.cuda.synchronize()
-        w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, d)
-        y_moe, idx_ref, _, _ = orc.moe_block(bits(h_gpu), bits(blk.wg[:E]), blk.bias.cpu().numpy(),
-                                             w13[:, :, 0].reshape(E, f, d), bits(blk.w_out).reshape(E, d, f), 2,
-                                             "swiglu", True, w13[:, :, 1].reshape(E, f, d))
-        ok = np.all(blk.stats.extras["topk_idx"].cpu().numpy() == idx_ref, axis=1)
-        assert ok.mean() > 0.97
-        ref = orc.bf16_to_f32(bits(h_gpu)) + orc.bf16_to_f32(y_moe)
-        assert_close(orc.bf16_to_f32(bits(h_next))[ok], ref[ok], "stack layer")
+        check_block_parity(blk, h_gpu, h_next, blk.stats.extras["topk_idx"].cpu().numpy(), residual=h_gpu,
+                           what="stack layer")
         h_gpu = h_next
     assert torch.equal(h_gpu, y)  # chained layer calls == stack forward
     cap = st.capture(512)
@@ -467,18 +466,7 @@ def test_block_ragged_and_tiny_batches(T, G, E, k, act):
     assert np.array_equal(blk.stats.schedule.cpu().numpy().sum(axis=2), m_all)
     if T == 0:
         return
-    wg = bits(blk.wg[:E])
-    f = 256
-    if act == "swiglu":
-        w13 = bits(blk.w_in).reshape(E, f // 128, 2, 128, 256)
-        w1, w3 = w13[:, :, 0].reshape(E, f, 256), w13[:, :, 1].reshape(E, f, 256)
-    else:
-        w1, w3 = bits(blk.w_in).reshape(E, f, 256), None
-    w2 = bits(blk.w_out).reshape(E, 256, f)
-    y_ref, idx_ref, _, _ = orc.moe_block(bits(x), wg, blk.bias.cpu().numpy(), w1, w2, k, act, cfg.renormalize, w3)
-    ok = np.all(blk.stats.extras["topk_idx"].cpu().numpy() == idx_ref, axis=1)
-    assert ok.mean() >= 0.9
-    assert_close(orc.bf16_to_f32(bits(y))[ok], orc.bf16_to_f32(y_ref)[ok], f"T={T} G={G} E={E} k={k}")
+    check_block_parity(blk, x, y, blk.stats.extras["topk_idx"].cpu().numpy(), what=f"T={T} G={G} E={E} k={k}")
 
 
 def test_config_rejects_untileable_shapes():

@@ -22,7 +22,7 @@ def test_fig4_exact(golden):
     assert S1.sum(axis=(0, 1)).tolist() == [5, 5, 5]
 
 
-@pytest.mark.parametrize("pack", ["acceptance_c2", "baseline_shapes"])
+@pytest.mark.parametrize("pack", ["acceptance_c2", "baseline_shapes", "wide_schedules"])
 def test_schedule_matches_reference(golden, pack):
     n = 0
     for inst in iter_packed(golden(pack)):
@@ -30,7 +30,7 @@ def test_schedule_matches_reference(golden, pack):
         assert np.array_equal(S, inst["S"]), f"instance {inst['i']}"
         assert it == inst["iters"], f"instance {inst['i']}"
         n += 1
-    assert n > 100
+    assert n > 30
 
 
 def test_placements_match_reference():
