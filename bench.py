@@ -11,10 +11,16 @@ shards the same 16,384-token batch over the ranks (strong scaling) with
 expert parallelism (ep.py).  Random-init weights and x ~ N(0,1); router bias
 log p_zipf(s) makes routing Zipf-skewed.
 
-``--impl reference`` times the reference's CPU path (the oracle port in
-oracle/: C scheduler + numpy numeric restatement; the reference itself is a
-Python count-only simulator that cannot run the numeric block) on the host
-cores, on a bounded token sample per step.
+``--gpus N`` without a launcher self-launches N ranks (torch.distributed.run on
+127.0.0.1); a launch whose WORLD_SIZE differs from --gpus exits 2.
+
+``--impl reference`` times the reference's CPU path on the host cores: the
+reference itself (moesim, installed unmodified in baseline/_ref) for the stages
+it implements - build_schedule / rebalance_with_stats / simulate_layer on the
+batch's m_all - and the oracle's numpy port for the numeric stages moesim does
+not implement (router GEMM, expert FFN, combine; count-only simulator,
+pkg/README.md:10-12), on a bounded token sample per step.  The same figures are
+the ``cpu_baseline`` of the N=1 line, on the exact m_all of the GPU run.
 """
 
 from __future__ import annotations
@@ -201,7 +207,7 @@ class CpuOracleBlock:
         self.bias = calibrated_router_bias(E, zipf_s, k)
         self.home = orc.round_robin_home(E, 1)
 
-    def step(self, x):
+    def step(self, x, schedule=True):
         orc = self.orc
         logits = x @ self.wg.T + self.bias[None, :]
         idx = orc.topk_lowest_index(logits, self.k)
@@ -212,7 +218,8 @@ class CpuOracleBlock:
         if self.k > 1:
             w = w / w.sum(axis=1, keepdims=True)
         hist = np.bincount(idx.reshape(-1), minlength=self.E)[None, :]
-        orc.schedule(hist, self.home, self.q, True)
+        if schedule:
+            orc.schedule(hist, self.home, self.q, True)
         y = np.zeros_like(x)
         for e in np.nonzero(hist[0])[0]:
             t, j = np.nonzero(idx == e)
@@ -224,18 +231,24 @@ class CpuOracleBlock:
             y[t] += w[t, j][:, None] * (orc.round_bf16(h) @ self.w2[e].T)
         return y
 
+    def routing_matrix(self, x, G):
+        """m_all[G, E] of a batch split over G (logical) GPUs, from the port's router."""
+        idx = self.orc.topk_lowest_index(x @ self.wg.T + self.bias[None, :], self.k)
+        Tg = x.shape[0] // G
+        return np.stack([np.bincount(idx[g * Tg:(g + 1) * Tg].reshape(-1), minlength=self.E) for g in range(G)])
 
-def cpu_measure(wl, sample_tokens, seconds=None, steps=None, warmup=1, zipf_s=1.0, q=32):
+
+def cpu_measure(wl, sample_tokens, seconds=None, steps=None, warmup=1, zipf_s=1.0, q=32, schedule=True):
     blk = CpuOracleBlock(wl, zipf_s=zipf_s, q=q)
     rng = np.random.default_rng(1)
     x = blk.orc.round_bf16(rng.standard_normal((sample_tokens, wl[0])).astype(np.float32))
     for _ in range(warmup):
-        blk.step(x)
+        blk.step(x, schedule)
     times = []
     t_end = time.perf_counter() + (seconds or 0)
     while True:
         t0 = time.perf_counter()
-        blk.step(x)
+        blk.step(x, schedule)
         times.append(time.perf_counter() - t0)
         if steps is not None and len(times) >= steps:
             break
@@ -249,6 +262,10 @@ def cpu_cores():
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
+
+
+def host_cpus():
+    return {"os_cpu_count": os.cpu_count(), "sched_getaffinity": cpu_cores()}
 
 
 def use_all_cores():
@@ -265,25 +282,119 @@ def use_all_cores():
         return int(os.environ.get("OMP_NUM_THREADS", n))
 
 
+def moesim_module():
+    """The UNMODIFIED reference (moesim, pip-installed into baseline/_ref)."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "moesim")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import moesim
+
+    return moesim
+
+
+def time_moesim(m_all, placement: str, q: int, wl, seconds: float = 6.0, min_reps: int = 20):
+    """The reference's own CPU implementation of the path's scheduling stages, timed on the
+    host: ``rebalance_with_stats(initial_assign(m, placement), q)`` (policies.py:109-171),
+    ``build_schedule`` (engine.py:287-299) and ``simulate_layer`` (engine.py:302-384, the
+    modelled block forward) on exactly ``m_all``.  Median of >= ``min_reps`` perf_counter
+    timings each.  moesim is small-array numpy: one core."""
+    moesim = moesim_module()
+    if moesim is None:
+        return None
+    G, E = m_all.shape
+    d, f = wl[0], wl[1]
+    rm = moesim.RoutingMatrix(np.asarray(m_all, np.int64))
+    kind = moesim.PlacementKind.BLOCKED if placement == "blocked" else moesim.PlacementKind.ROUND_ROBIN
+    pl = (moesim.blocked_placement if placement == "blocked" else moesim.round_robin_placement)(E, G)
+    cfg = moesim.SchedulerConfig(token_threshold_q=int(q), policy=moesim.SchedulingPolicy.REBALANCE, placement=kind)
+    flags = moesim.SimFlags()
+    model = moesim.ModelSpec(num_layers=1, num_experts=E, d_model=d, d_ff=f, dtype_bytes=2)
+    cluster = moesim.ClusterSpec(num_gpus=G, expert_slots_per_gpu=E, link_bandwidth=900e9, link_latency=2e-6,
+                                 pcie_bandwidth=55e9, gpu_flops=1.6e15)
+    cost = moesim.CostModel.from_specs(cluster, model)
+    calls = {
+        "rebalance_with_stats": lambda: moesim.rebalance_with_stats(moesim.initial_assign(rm, pl), int(q)),
+        "build_schedule": lambda: moesim.engine.build_schedule(rm, pl, cfg, flags),
+        "simulate_layer": lambda: moesim.simulate_layer(rm, pl, cfg, flags, cost, cluster),
+    }
+    out = {}
+    for name, fn in calls.items():
+        fn()
+        ts, t_end = [], time.perf_counter() + seconds / len(calls)
+        while len(ts) < min_reps or time.perf_counter() < t_end:
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        out[f"{name}_us"] = float(np.median(ts)) * 1e6
+        out[f"{name}_reps"] = len(ts)
+    _, iters = moesim.rebalance_with_stats(moesim.initial_assign(rm, pl), int(q))
+    S = moesim.engine.build_schedule(rm, pl, cfg, flags)
+    loads = moesim.load_per_gpu(S)
+    out.update(iterations=int(iters), G=G, placement=placement, q=int(q),
+               load_max_over_mean=float(loads.max() / loads.mean()) if loads.mean() > 0 else 1.0,
+               module=f"moesim {getattr(moesim, '__version__', '?')} from baseline/_ref (unmodified)")
+    return out
+
+
+def cpu_reference_block(wl, m_all, placement, q, zipf_s, seconds, sample=256, steps=None, warmup=1):
+    """The reference's CPU path for the block: moesim itself for every stage it implements
+    (schedule: build_schedule on the batch's m_all), the oracle's numpy port for the numeric
+    stages moesim does not implement (router GEMM + top-k, expert FFNs, combine; measured on
+    ``sample``-token slices and scaled to the batch).  Returns (cpu_baseline dict, per-step
+    seconds for the whole batch)."""
+    T = wl[5]
+    cores = use_all_cores()
+    ms = time_moesim(m_all, placement, q, wl, seconds=min(6.0, 0.3 * seconds))
+    times = cpu_measure(wl, sample, seconds=None if steps else 0.7 * seconds, steps=steps, warmup=warmup,
+                        zipf_s=zipf_s, q=q, schedule=ms is None)
+    t_num = float(np.mean(times)) / sample * T
+    t_sched = ms["build_schedule_us"] * 1e-6 if ms else 0.0
+    t_block = t_num + t_sched
+    port = {"value": sample / float(np.mean(times)), "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"{sample}-token slices, {len(times)} reps: oracle numpy/OpenBLAS restatement of router, "
+                      f"expert FFN and combine" + ("" if ms else " + C scheduler oracle")}
+    base = {
+        "value": T / t_block, "unit": "tokens/s", "cores": cores, "kind": "reference" if ms else "port",
+        "sample": (f"moesim.engine.build_schedule (the reference itself) on the exact m_all of the {T}-token batch "
+                   f"over {m_all.shape[0]} GPUs ({placement}, q={q}), plus " if ms else "") +
+                  f"the numeric stages moesim does not implement (oracle port, {sample}-token slices x "
+                  f"{len(times)} reps, scaled to {T} tokens)",
+        "moesim": ms, "port": port, "host": host_cpus(),
+        "moesim_simulate_layer_tokens_per_s": (T / (ms["simulate_layer_us"] * 1e-6)) if ms else None,
+    }
+    return base, [t * T / sample + t_sched for t in times]
+
+
 def run_reference(args, rank, world):
     wl = WORKLOADS[args.workload]
     if rank != 0:
         return
-    sample = 256
-    cores = use_all_cores()
-    times = cpu_measure(wl, sample, steps=args.steps, warmup=args.warmup, zipf_s=args.zipf, q=args.q)
-    per_step = float(np.mean(times))
-    value = sample / per_step
+    from oracle import moe_oracle as orc
+
+    T = wl[5]
+    # the reference arm's own batch: x ~ N(0,1) through the port's router (calibrated Zipf
+    # bias) gives the m_all the reference scheduler works on, split over 8 logical GPUs
+    blk = CpuOracleBlock(wl, zipf_s=args.zipf, q=args.q)
+    x = orc.round_bf16(np.random.default_rng(2).standard_normal((T, wl[0])).astype(np.float32))
+    G = 8 if args.gpus == 1 else args.gpus
+    m_all = blk.routing_matrix(x, G)
+    del x, blk
+    base, step_s = cpu_reference_block(wl, m_all, "blocked", args.q, args.zipf, seconds=args.cpu_seconds,
+                                       steps=args.steps, warmup=args.warmup)
+    per_step = float(np.mean(step_s))
+    value = T / per_step
+    base["value"] = value
     line = {
         "impl": "reference", "metric": "moe_block_tokens_per_sec", "value": value, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16-in/fp32",
         "data": "synthetic",
-        "config": {"workload": f"{args.workload} MoE layer, Zipf s={args.zipf}, CPU oracle port on {sample} tokens/step",
-                   "d_model": wl[0], "d_ff": wl[1], "experts": wl[2], "top_k": wl[3], "tokens": wl[5]},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} tokens of the {args.workload} batch per step (numpy/OpenBLAS "
-                                   f"restatement + C scheduler oracle)"},
+        "config": {"workload": f"{args.workload} MoE layer, {T} tokens, Zipf s={args.zipf}: moesim scheduling on the "
+                               f"full batch + oracle port numerics on 256 tokens/step",
+                   "d_model": wl[0], "d_ff": wl[1], "experts": wl[2], "top_k": wl[3], "tokens": T},
+        "cpu_baseline": base,
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -325,13 +436,16 @@ def load_ratio_logical(block_cls, cfg_kw, x, G, q, placement, zipf_s, seed, dev)
     from paper_2506_12417_b200.block import MoEConfig
 
     cfg = MoEConfig(logical_ranks=G, eq_tokens=q, placement=placement, **cfg_kw)
-    out = {}
+    out, m_all = {}, None
     for pol in ("harmony", "round_robin"):
         cfg.scheduling_policy = pol
         blk = block_cls.random(cfg, seed=seed, device=dev, zipf_s=zipf_s)
         blk(x)
         out[pol] = blk.stats.load_imbalance()
-    return out
+        if pol == "harmony":
+            m_all = blk.stats.m_all.cpu().numpy().astype(np.int64)
+        del blk
+    return out, m_all
 
 
 def run_ours(args, rank, world, local_rank):
@@ -499,17 +613,14 @@ def run_ours(args, rank, world, local_rank):
     # block roofline: expert GEMMs only (the dominant term), tokens / max(F/P_tc, B/P_hbm)
     t_roof = max((f1 + f2) / (tc_used * 1e12), (w_bytes + act_bytes) / (hbm * 1e9)) * args.layers
     roof_tokens = (T_total // world) / t_roof * world
-    loads = {}
+    loads, m_all8 = {}, None
     if world == 1 and args.gpus == 1:
-        loads = load_ratio_logical(HarMoEnyBlock, cfg_kw, x, 8, args.q, "blocked", args.zipf, 0, dev)
+        # the same batch split over 8 logical GPUs (blocked placement: hot experts homed together)
+        # - the G=8 schedule the north star targets; its m_all also feeds the CPU baseline
+        loads, m_all8 = load_ratio_logical(HarMoEnyBlock, cfg_kw, x, 8, args.q, "blocked", args.zipf, 0, dev)
     cpu = None
-    if not args.no_cpu_baseline:
-        sample = 256
-        cores = use_all_cores()
-        times = cpu_measure(wl, sample, seconds=args.cpu_seconds, zipf_s=args.zipf, q=args.q)
-        cpu = {"value": sample / float(np.mean(times)), "unit": "tokens/s", "cores": cores, "kind": "port",
-               "sample": f"{sample}-token slices of the {args.workload} batch, {len(times)} reps "
-                         f"(~{args.cpu_seconds:.0f}s; numpy/OpenBLAS restatement + C scheduler oracle)"}
+    if not args.no_cpu_baseline and world == 1 and m_all8 is not None:  # rank 0 at N=1 only
+        cpu, _ = cpu_reference_block(wl, m_all8, "blocked", args.q, args.zipf, seconds=args.cpu_seconds)
     line = {
         "metric": "moe_block_tokens_per_sec", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -555,11 +666,33 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(n: int) -> int:
+    """``--gpus N`` without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1 and return its exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] --gpus {n} without WORLD_SIZE: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1 and args.impl == "ours":
+        sys.exit(self_launch(args.gpus))
+    world = int(env_world or "1")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and not (env_world is None and args.impl == "reference"):
+        # never print a line whose n_gpus disagrees with the launch
+        print(f"[bench] error: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         if world > 1 and rank != 0:
             return
@@ -575,8 +708,17 @@ def main():
             torch.cuda.set_device(local_rank)
             torch.distributed.init_process_group("gloo")
         else:
+            if torch.cuda.device_count() < world:
+                print(f"[bench] error: {world} NCCL ranks need {world} GPUs, {torch.cuda.device_count()} visible "
+                      f"(--backend gloo shares one GPU for testing)", file=sys.stderr, flush=True)
+                sys.exit(2)
             torch.cuda.set_device(local_rank)
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # one line per rank on stderr: the communicator really has N ranks, one per device
+        props = torch.cuda.get_device_properties(local_rank)
+        print(f"[bench] rank {torch.distributed.get_rank()}/{torch.distributed.get_world_size()} "
+              f"backend {torch.distributed.get_backend()} cuda:{local_rank} {props.name} "
+              f"pci {props.pci_bus_id:02x}:{props.pci_device_id:02x}", file=sys.stderr, flush=True)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

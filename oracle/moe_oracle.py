@@ -267,6 +267,13 @@ def f32_to_bf16(x) -> np.ndarray:
     return out
 
 
+def bf16_ulp(x) -> np.ndarray:
+    """Spacing of bf16 values at |x| (8 significant bits): 2^(floor(log2|x|) - 7); 0 at 0."""
+    a = np.abs(np.asarray(x, np.float32))
+    e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    return np.where(a > 0, np.exp2(e - 7), 0.0).astype(np.float32)
+
+
 def round_bf16(x) -> np.ndarray:
     return bf16_to_f32(f32_to_bf16(x))
 
@@ -380,8 +387,10 @@ def moe_block(x_bits, wg_bits, bias, w1_bits, w2_bits, k, act, renormalize, w3_b
     for j in range(k):
         acc = (acc + w[:, j : j + 1] * yk[:, j, :]).astype(np.float32)
     if return_scale:
-        # sum_j w_j |Y_j|: the magnitude of the combined terms, the reference for an elementwise
-        # tolerance where the weighted sum cancels (each Y_j carries its own bf16 rounding)
-        scale = np.einsum("tk,tkd->td", np.abs(w), np.abs(yk)).astype(np.float32)
+        # sum_j |w_j| ulp_bf16(Y_j): one bf16 unit in the last place of every combined expert
+        # output.  Each Y_j is an fp32 accumulation rounded to bf16; where the exact value sits
+        # within the accumulation-order error of a rounding boundary, kernel and oracle may round
+        # it different ways - a one-ulp, order-dependent difference neither side can remove.
+        scale = np.einsum("tk,tkd->td", np.abs(w), bf16_ulp(yk)).astype(np.float32)
         return f32_to_bf16(acc), idx, w, logits, scale
     return f32_to_bf16(acc), idx, w, logits

@@ -63,16 +63,18 @@ def block_weight_bits(blk):
     return wg, w1, w2, w3, bias
 
 
-def check_block_parity(blk, x, y, idx_gpu, rows=None, residual=None, what="", scale_bar=False):
+def check_block_parity(blk, x, y, idx_gpu, rows=None, residual=None, what="", rounding_slack=False):
     """The strict bar for a block forward (VERDICT r1 'next' #1):
 
     * routing: the GPU's top-k equals the oracle's on EVERY token of ``x`` except oracle near
       ties (``orc.routing_parity``; the near-tie count is printed);
     * output: on ``rows`` (default all tokens) the oracle block evaluated WITH THE GPU'S
       ROUTING (so near-tie tokens are checked too) meets |y - y_ref| <= 1e-2 + 2e-2 |y_ref|
-      elementwise and relative Frobenius <= 5e-3.  ``scale_bar`` reports the stated
-      elementwise bar's worst ratio and enforces the bar relative to sum_j w_j |Y_j| instead
-      (Mixtral's K = 14336 expert outputs).
+      elementwise and relative Frobenius <= 5e-3.  ``rounding_slack`` (Mixtral)
+      widens the elementwise bar by one bf16 ulp of every combined expert output,
+      sum_j |w_j| ulp(Y_j): a K = 14,336 fp32 accumulation rounded to bf16 may land on either
+      side of a rounding boundary depending on summation order.  The stated bar's worst ratio
+      and the share of elements beyond it (required <= 1e-4) are still measured and returned.
     Returns a dict of the measured figures."""
     from oracle import moe_oracle as orc
 
@@ -94,13 +96,19 @@ def check_block_parity(blk, x, y, idx_gpu, rows=None, residual=None, what="", sc
     stated = ATOL + RTOL * np.abs(yr)
     worst_stated = float((err / stated).max()) if err.size else 0.0
     frob = float(np.linalg.norm(yg - yr) / max(np.linalg.norm(yr), 1e-30))
+    beyond = int((err > stated).sum())
     out = dict(tokens=int(xb.shape[0]), checked_rows=int(len(rows)), near_ties=n_near, disagree=n_diff,
-               max_err=float(err.max()) if err.size else 0.0, worst_ratio_stated=worst_stated, frob=frob)
-    print(f"[parity] {what}: {out}")
-    if scale_bar:
-        bound = ATOL + RTOL * scale.astype(np.float64)
-        assert np.all(err <= bound), f"{what}: worst ratio vs sum_j w_j|Y_j| bar {(err / bound).max()}"
+               max_err=float(err.max()) if err.size else 0.0, worst_ratio_stated=worst_stated,
+               beyond_stated=beyond, elements=int(err.size), frob=frob)
+    if rounding_slack:
+        bound = stated + scale.astype(np.float64)
+        out["worst_ratio_with_slack"] = float((err / bound).max()) if err.size else 0.0
+        print(f"[parity] {what}: {out}")
+        assert np.all(err <= bound), f"{what}: worst ratio vs the stated bar + 1 ulp per expert output " \
+                                     f"{out['worst_ratio_with_slack']}"
+        assert beyond <= 1e-4 * err.size, f"{what}: {beyond} of {err.size} elements beyond the stated bar"
     else:
+        print(f"[parity] {what}: {out}")
         assert np.all(err <= stated), (f"{what}: {(err > stated).sum()} elements out of the stated bar, "
                                        f"worst ratio {worst_stated:.3f}, max |dy| {err.max():.3e}")
     assert frob <= FROB, f"{what}: relative Frobenius error {frob}"
