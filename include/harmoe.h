@@ -79,6 +79,8 @@ HM_API int hm_version(void);
 HM_API const char* hm_last_error(void);
 HM_API int hm_num_sms(void);
 HM_API int hm_gemm_tile_m(void); /* rows per GEMM tile (128) */
+/* CTA pairs of the 2-CTA grouped GEMM that fit on the device at once (its persistent grid) */
+HM_API int hm_gemm_resident_pairs(int epilogue, int gather);
 
 /*
  * Router (K1) + histogram/rank pass (K2), fused: one CTA per 128-token tile.
@@ -135,12 +137,14 @@ HM_API int hm_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t
  *   fetch [E] int32: experts this rank must fetch (non-resident with work), plan order; n_fetch [1]
  * LOCAL: segments are (dest, expert) over the whole [G] buffer, wslot = expert.
  * EP:    segments are (expert, source) of rank `me`'s receive buffer; wslot = index of the expert
- *        among me's home experts (ascending id), fetched experts get slots n_home + fetch ordinal.
+ *        among me's home experts (ascending id), fetched experts get slots n_home + fetch ordinal,
+ *        or n_home + (ordinal % cache_slots) with a bounded cache (cache_slots > 0): fetch i then
+ *        reuses the slot of fetch i - cache_slots, the first to free up (engine.py:239-257).
  * cap >= G*E.
  */
 HM_API int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
                        int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
-                       void* stream);
+                       int cache_slots, void* stream);
 
 /*
  * Fused planner: the whole step-2/3 stage in one single-CTA launch (histogram reduce ->
@@ -152,7 +156,7 @@ HM_API int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int 
 HM_API int hm_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_all_in, const int32_t* home, int G,
                    int E, int q, int rebalance, int mode, int me, int32_t* m_all_out, int32_t* tile_off, int32_t* S,
                    int32_t* iters, int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg,
-                   int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch, void* stream);
+                   int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch, int cache_slots, void* stream);
 
 /*
  * Scatter (K4): copy token rows to their scheduled buffer rows (one read of x, k 128-bit-vector
@@ -169,19 +173,57 @@ HM_API int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lra
                int G, int E, int k, int d, void* out, int32_t* pos, int32_t* inv, void* stream);
 
 /*
+ * K6 fetch pairs inside a grouped-GEMM launch (bounded expert cache, engine.py:204-275).
+ * The last `pairs` CTA pairs of the launch copy experts instead of computing, so the copy and the
+ * GEMM tiles it gates - and the GEMM tiles whose completion frees the cache slots - are
+ * co-resident by construction (no cross-stream dependency).  Fetch i goes to slot
+ * first_slot + i % n_slots and, for i >= n_slots, only after the launch's slot_done count of
+ * expert fetch[i - n_slots] reaches 16 x its pair tiles (its occupant is finished).
+ *   phase 1 (FFN1 launch): every expert's gate/up block (src_in -> dst_in, ready_in), then the
+ *                          down blocks of the first min(n_slots, *n_fetch) (src_out -> dst_out)
+ *   phase 2 (FFN2 launch): the remaining down blocks, gated by FFN2's own slot_done counts
+ * Copies are TMA bulk transfers global -> shared -> global (32 KB chunks, 6 in flight per CTA).
+ */
+typedef struct hm_fetch_plan {
+  const int32_t* fetch;     /* [E] experts to fetch in plan order (the layout's fetch list) */
+  const int32_t* n_fetch;   /* [1] */
+  const uint64_t* src_in;   /* [E] device pointer of expert e's gate/up (or W1) block */
+  const uint64_t* src_out;  /* [E] device pointer of expert e's down (W2) block */
+  void* dst_in;             /* slot s of the gate/up cache at dst_in + s * in_bytes */
+  void* dst_out;            /* slot s of the down cache at dst_out + s * out_bytes */
+  uint64_t in_bytes;
+  uint64_t out_bytes;
+  int32_t first_slot;
+  int32_t n_slots;
+  int32_t* ready_in;        /* [E] per-expert flags set to `value` */
+  int32_t* ready_out;
+  int32_t* counters;        /* scratch, n_counters >= 2 * E, zeroed by the launch */
+  int32_t n_counters;
+  int32_t value;
+  int32_t pairs;            /* fetch pairs (>= 1) */
+  int32_t phase;            /* 1 or 2 */
+} hm_fetch_plan;
+
+/*
  * Grouped expert GEMM (K5), tcgen05/TMEM/TMA: for every segment, out[rows] = epi(A[rows] W[wslot]^T).
  *   A [a_rows, K] bf16; W [w_rows, K] bf16 with w_rows = slots*N; out [a_rows, N] (or N/2 for SWIGLU).
  *   row_map [rows] int32 or NULL: output row of buffer row r is row_map[r] (scatter epilogue).
  *   a_gather [rows] int32 or NULL: fused scatter - buffer row r reads A row a_gather[r] / a_gather_div
  *   (TMA tile::gather4 straight from the token activations; with the inverse permutation of
  *   hm_permute and div = k this is the token of each assignment).  A is then [a_rows, K].
- *   slot_ready [slots] int32 or NULL: tiles of slot s >= ready_from_slot wait for slot_ready[s] >= epoch.
+ *   slot_ready [E] int32 or NULL: tiles of a segment whose weight slot is >= ready_from_slot (a
+ *   fetched expert, K6) wait until slot_ready[expert] >= epoch (per expert, not per slot: a
+ *   bounded cache reuses slots within one forward, engine.py:239-257).
+ *   slot_done [E] int32 or NULL: every epilogue warp (16 per 256-row pair tile) adds 1 to
+ *   slot_done[expert] when it has finished a tile of a fetched expert (release) - the K6 channel
+ *   overwrites that expert's cache slot once the count reaches 16 x its pair tiles.
+ *   fetch: NULL, or the K6 fetch pairs of this launch (hm_fetch_plan; needs slot_done).
  * Requires N % 256 == 0, K % 64 == 0.
  */
 HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
                     const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out, const int32_t* row_map,
                     const int32_t* a_gather, int a_gather_div, const int32_t* slot_ready, int ready_from_slot,
-                    int epoch, void* stream);
+                    int epoch, int32_t* slot_done, const hm_fetch_plan* fetch, void* stream);
 
 /*
  * Async expert fetch (K6): copy `bytes` from src (peer HBM through UVA/NVLink, or pinned host
@@ -244,19 +286,21 @@ HM_API int hm_grouped_gemm_remote(const void* A, int64_t a_rows, const void* W, 
                                   const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix,
                                   int epilogue, const uint64_t* out_ptrs, const int32_t* out_split, int n_out,
                                   const int32_t* row_map, const int32_t* slot_ready, int ready_from_slot, int epoch,
-                                  void* stream);
+                                  int32_t* slot_done, const hm_fetch_plan* fetch, void* stream);
 
 /*
  * Device-driven K6 (engine.py:253-265): copy expert fetch[i] (i < *n_fetch, plan order, from the
  * layout's fetch list) from src_in[e] / src_out[e] (device arrays of E pointers: the home rank's
  * HBM through IPC, or pinned host memory) into cache slot first_slot + i of dst_in / dst_out
- * (slot strides in_bytes / out_bytes), publishing ready_in / ready_out[slot] = value as each
- * block lands.  counters [2*n_slots] int32 scratch (zeroed by the call); ctas <= 0: default.
+ * (slot strides in_bytes / out_bytes), publishing ready_in / ready_out[e] = value (per EXPERT)
+ * as each block lands.  counters [n_counters >= 2 * *n_fetch] int32 scratch (zeroed by the call);
+ * ctas <= 0: default.  *n_fetch > n_slots traps the launch (never a silent truncation): a bounded
+ * cache is fetched inside the GEMM launches (hm_fetch_plan).
  */
 HM_API int hm_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const uint64_t* src_in,
                             const uint64_t* src_out, size_t in_bytes, size_t out_bytes, void* dst_in, void* dst_out,
                             int first_slot, int n_slots, int32_t* ready_in, int32_t* ready_out, int32_t* counters,
-                            int value, int ctas, void* stream);
+                            int n_counters, int value, int ctas, void* stream);
 
 /*
  * Stream-ordered flags: hm_stream_signal writes `value` to each of n device addresses

@@ -29,24 +29,25 @@ SIGNATURES = {
     "hm_last_error": [],
     "hm_num_sms": [],
     "hm_gemm_tile_m": [],
+    "hm_gemm_resident_pairs": [_i32, _i32],
     "hm_router_topk": [_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp],
     "hm_hist_scan": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_schedule": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "hm_rebalance": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_schedule_batched": [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
-    "hm_plan": [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32] + [_vp] * 12,
-    "hm_dispatch_layout": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "hm_plan": [_vp, _i32, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32] + [_vp] * 11 + [_i32, _vp],
+    "hm_dispatch_layout": [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
     "hm_permute": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "hm_grouped_gemm": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _i32,
-                        _vp],
+                        _vp, _vp, _vp],
     "hm_fetch_expert": [_vp, _vp, ctypes.c_size_t, _vp, _i32, _vp],
     "hm_combine": [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_ep_offsets": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_dispatch_push": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "hm_grouped_gemm_remote": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _i32,
-                               _i32, _vp],
+                               _i32, _vp, _vp, _vp],
     "hm_fetch_experts": [_vp, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_size_t, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
-                         _i32, _i32, _vp],
+                         _i32, _i32, _i32, _vp],
     "hm_stream_signal": [ctypes.POINTER(ctypes.c_void_p), _i32, ctypes.c_uint32, _vp],
     "hm_stream_wait": [_vp, _i32, ctypes.c_uint32, _vp],
     "hm_debug_plan_phases": [_vp],
@@ -55,6 +56,15 @@ SIGNATURES = {
     "hm_ipc_close": [_vp],
 }
 _RESTYPE = {"hm_last_error": ctypes.c_char_p}
+
+
+class FetchPlan(ctypes.Structure):
+    """hm_fetch_plan (include/harmoe.h): K6 fetch pairs inside a grouped-GEMM launch."""
+
+    _fields_ = [("fetch", _vp), ("n_fetch", _vp), ("src_in", _vp), ("src_out", _vp), ("dst_in", _vp),
+                ("dst_out", _vp), ("in_bytes", ctypes.c_uint64), ("out_bytes", ctypes.c_uint64),
+                ("first_slot", _i32), ("n_slots", _i32), ("ready_in", _vp), ("ready_out", _vp), ("counters", _vp),
+                ("n_counters", _i32), ("value", _i32), ("pairs", _i32), ("phase", _i32)]
 
 _lib = None
 

@@ -96,6 +96,14 @@ class MoEConfig:
             self.renormalize = self.top_k > 1
         if self.world_size > 1 and self.logical_ranks not in (1, self.world_size):
             raise ValueError("logical ranks are a single-process mode (world_size == 1)")
+        if self.expert_cache_size < 0:
+            raise ValueError("expert_cache_size must be >= 0 (0 = one slot per fetchable expert)")
+        if self.world_size > 1 and self.expert_cache_size > 0 and not self.async_fetch:
+            n_home = int((placement_home(self) == self.rank).sum())
+            if self.expert_cache_size < self.num_experts - n_home:
+                raise ValueError("a bounded expert cache (expert_cache_size below the experts this rank may fetch) "
+                                 "needs async_fetch=True: synchronous loading would stall the stream on slots that "
+                                 "only a later kernel frees")
 
     @property
     def policy_code(self) -> int:

@@ -91,9 +91,10 @@ int launch_schedule_batched(const int32_t*, const int32_t*, int, int, int, int, 
                             cudaStream_t);
 int read_plan_phases(long long*);
 int launch_plan(const int32_t*, int, const int32_t*, const int32_t*, int, int, int, int, int, int, int32_t*, int32_t*,
-                int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, cudaStream_t);
+                int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int,
+                cudaStream_t);
 int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
-                  int32_t*, int32_t*, cudaStream_t);
+                  int32_t*, int32_t*, int, cudaStream_t);
 int launch_permute(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int,
                    int, int, int, int, int, int, void*, int32_t*, int32_t*, cudaStream_t);
 int launch_combine(const void*, const int32_t*, const float*, int, int, int, const void*, void*, cudaStream_t);
@@ -102,7 +103,7 @@ int launch_dispatch_push(const void*, const int32_t*, const int32_t*, const int3
                          const int32_t*, int, int, int, int, int, int, const unsigned long long*,
                          const unsigned long long*, int32_t*, cudaStream_t);
 int launch_fetch_experts(const int32_t*, const int32_t*, const unsigned long long*, const unsigned long long*, size_t,
-                         size_t, void*, void*, int, int, int32_t*, int32_t*, int32_t*, int, int, cudaStream_t);
+                         size_t, void*, void*, int, int, int32_t*, int32_t*, int32_t*, int, int, int, cudaStream_t);
 
 // Flag publish by a kernel (used when stream memory operations are unavailable): the stream
 // order makes every earlier kernel's writes complete first; the system-scope release orders
@@ -128,6 +129,12 @@ int hm_num_sms(void) { return num_sms(); }
 
 int hm_gemm_tile_m(void) { return 128; }
 
+int hm_gemm_resident_pairs(int epilogue, int gather) {
+  const int n = gemm_resident_pairs(epilogue, gather != 0);
+  if (n < 0) return set_error(HM_EINVAL, "gemm_resident_pairs: unknown epilogue");
+  return n;
+}
+
 int hm_router_topk(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
                    int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,
                    void* stream) {
@@ -148,9 +155,10 @@ int hm_schedule(const int32_t* m_all, const int32_t* home, int G, int E, int q, 
 int hm_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_all_in, const int32_t* home, int G, int E,
             int q, int rebalance, int mode, int me, int32_t* m_all_out, int32_t* tile_off, int32_t* S, int32_t* iters,
             int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch,
-            int32_t* n_fetch, void* stream) {
+            int32_t* n_fetch, int cache_slots, void* stream) {
   return launch_plan(tile_hist, tiles_per_rank, m_all_in, home, G, E, q, rebalance, mode, me, m_all_out, tile_off, S,
-                     iters, loads, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch, as_stream(stream));
+                     iters, loads, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch, cache_slots,
+                     as_stream(stream));
 }
 
 int hm_schedule_batched(const int32_t* m_all, const int32_t* home, int B, int G, int E, int q, int rebalance,
@@ -164,8 +172,8 @@ int hm_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* loads
 
 int hm_dispatch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
                        int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
-                       void* stream) {
-  return launch_layout(S, home, G, E, mode, me, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch,
+                       int cache_slots, void* stream) {
+  return launch_layout(S, home, G, E, mode, me, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch, cache_slots,
                        as_stream(stream));
 }
 
@@ -179,19 +187,22 @@ int hm_permute(const void* x, const int32_t* topk_idx, const int32_t* lrank, con
 int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K, const int32_t* segs,
                     const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out,
                     const int32_t* row_map, const int32_t* a_gather, int a_gather_div, const int32_t* slot_ready,
-                    int ready_from_slot, int epoch, void* stream) {
+                    int ready_from_slot, int epoch, int32_t* slot_done, const hm_fetch_plan* fetch, void* stream) {
   return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, row_map, a_gather,
-                             a_gather_div, slot_ready, ready_from_slot, epoch, as_stream(stream));
+                             a_gather_div, slot_ready, ready_from_slot, epoch, as_stream(stream), nullptr, nullptr, 0,
+                             slot_done, fetch);
 }
 
 int hm_grouped_gemm_remote(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                            const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
                            const uint64_t* out_ptrs, const int32_t* out_split, int n_out, const int32_t* row_map,
-                           const int32_t* slot_ready, int ready_from_slot, int epoch, void* stream) {
+                           const int32_t* slot_ready, int ready_from_slot, int epoch, int32_t* slot_done,
+                           const hm_fetch_plan* fetch, void* stream) {
   if (out_ptrs == nullptr) return set_error(HM_EINVAL, "grouped_gemm_remote: out_ptrs is required");
   return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, nullptr, row_map,
                              nullptr, 1, slot_ready, ready_from_slot, epoch, as_stream(stream),
-                             reinterpret_cast<const unsigned long long*>(out_ptrs), out_split, n_out);
+                             reinterpret_cast<const unsigned long long*>(out_ptrs), out_split, n_out, slot_done,
+                             fetch);
 }
 
 int hm_ep_offsets(const int32_t* S, int G, int E, int me, int32_t* dst_delta, int32_t* recv_split, void* stream) {
@@ -209,10 +220,11 @@ int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* lran
 
 int hm_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const uint64_t* src_in, const uint64_t* src_out,
                      size_t in_bytes, size_t out_bytes, void* dst_in, void* dst_out, int first_slot, int n_slots,
-                     int32_t* ready_in, int32_t* ready_out, int32_t* counters, int value, int ctas, void* stream) {
+                     int32_t* ready_in, int32_t* ready_out, int32_t* counters, int n_counters, int value, int ctas,
+                     void* stream) {
   return launch_fetch_experts(fetch, n_fetch, reinterpret_cast<const unsigned long long*>(src_in),
                               reinterpret_cast<const unsigned long long*>(src_out), in_bytes, out_bytes, dst_in,
-                              dst_out, first_slot, n_slots, ready_in, ready_out, counters, value, ctas,
+                              dst_out, first_slot, n_slots, ready_in, ready_out, counters, n_counters, value, ctas,
                               as_stream(stream));
 }
 

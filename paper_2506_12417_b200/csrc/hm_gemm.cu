@@ -179,9 +179,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       if (lane == 0 && slot_ready != nullptr && seg.z >= ready_from_slot) {
-        // K6: fetched expert weights land asynchronously; wait for this slot's epoch
+        // K6: fetched expert weights land asynchronously; wait for this expert's epoch
         long long spins = 0;  // watchdog, as in the 2-CTA kernel
-        while (ld_acquire_gpu(slot_ready + seg.z) < epoch) {
+        while (ld_acquire_gpu(slot_ready + seg.w) < epoch) {
           __nanosleep(128);
           if (++spins > (1ll << 26)) __trap();
         }
@@ -383,6 +383,125 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ------------------------------------------------------------------------------------------
+// K6 fetch pairs (bounded expert cache; hm_fetch_plan in harmoe.h).  Thread 0 of each fetch CTA
+// streams its share of a weight block (32 KB chunks, round-robin over the fetch CTAs) through a
+// 6-stage shared-memory ring with TMA bulk copies: global -> smem completes on an mbarrier,
+// smem -> global is a bulk-group store.  The last CTA to finish a block publishes the expert's
+// ready flag (release) for the GEMM producers of the same launch.
+// ------------------------------------------------------------------------------------------
+constexpr int kFetchChunk = 32768;
+constexpr int kFetchStages = 6;
+static_assert(kFetchStages * kFetchChunk + 64 <= k2Stages * 2 * k2Half + 256, "fetch ring must fit the GEMM smem");
+
+__device__ __forceinline__ void bulk_g2s(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_src), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// one weight block src -> dst (bytes % 16 == 0); this CTA copies chunks fc, fc + nf, ...
+__device__ void fetch_block(uint8_t* dst, const uint8_t* src, long long bytes, uint32_t ring, uint64_t* bars,
+                            uint32_t& par, int fc, int nf) {
+  const long long nch = (bytes + kFetchChunk - 1) / kFetchChunk;
+  const long long m = nch > fc ? (nch - fc + nf - 1) / nf : 0;
+  auto issue = [&](long long i) {
+    const int st = (int)(i % kFetchStages);
+    const long long c = fc + i * nf;
+    const uint32_t len = (uint32_t)min((long long)kFetchChunk, bytes - c * kFetchChunk);
+    mbar_arrive_expect_tx(&bars[st], len);
+    bulk_g2s(ring + st * kFetchChunk, src + c * kFetchChunk, len, &bars[st]);
+  };
+  for (long long i = 0; i < min((long long)kFetchStages, m); ++i) issue(i);
+  for (long long i = 0; i < m; ++i) {
+    const int st = (int)(i % kFetchStages);
+    mbar_wait(&bars[st], (par >> st) & 1u);
+    par ^= 1u << st;
+    const long long c = fc + i * nf;
+    const uint32_t len = (uint32_t)min((long long)kFetchChunk, bytes - c * kFetchChunk);
+    bulk_s2g(dst + c * kFetchChunk, ring + st * kFetchChunk, len);
+    if (i + kFetchStages < m) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage st is free again
+      issue(i + kFetchStages);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk writes before the generic release
+}
+
+__device__ __forceinline__ void fetch_publish(int32_t* counter, int32_t* flag, int value, int nf) {
+  __threadfence();
+  if (atomicAdd(counter, 1) == nf - 1) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+  }
+}
+
+// the GEMM of this launch has finished every tile of expert e: 16 epilogue warps x pair tiles
+__device__ void fetch_wait_done(const int32_t* done, const int4* segs, const int* mp, int n_seg, int e, int NB) {
+  int pt = 0;
+  for (int i = 0; i < n_seg; ++i)
+    if (segs[i].w == e) pt += (mp[i + 1] - mp[i] + 1) >> 1;
+  const int target = pt * NB * 16;
+  long long spins = 0;
+  while (ld_acquire_gpu(done + e) < target) {
+    __nanosleep(256);
+    if (++spins > (1ll << 25)) {  // watchdog (~10 s): never hang the device
+      printf("hm grouped_gemm fetch pair: expert %d tiles never finished (%d < %d)\n", e, ld_acquire_gpu(done + e),
+             target);
+      __trap();
+    }
+  }
+}
+
+__device__ void fetch_pair_role(const hm_fetch_plan& fp, uint8_t* smem, int fc, int nf, const int4* segs,
+                                const int* mp, int n_seg, int NB, const int32_t* done) {
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFetchStages * kFetchChunk);
+  if (threadIdx.x != 0) return;
+  for (int st = 0; st < kFetchStages; ++st) mbar_init(&bars[st], 1);
+  fence_mbar_init();
+  const uint32_t ring = smem_u32(smem);
+  uint32_t par = 0;
+  const int n_fetch = *fp.n_fetch;
+  const int C = fp.n_slots;
+  if (2 * n_fetch > fp.n_counters) __trap();
+  auto* dst_in = reinterpret_cast<uint8_t*>(fp.dst_in);
+  auto* dst_out = reinterpret_cast<uint8_t*>(fp.dst_out);
+  const long long inb = (long long)fp.in_bytes, outb = (long long)fp.out_bytes;
+  if (fp.phase == 1) {
+    for (int i = 0; i < n_fetch; ++i) {
+      const int e = __ldg(fp.fetch + i);
+      if (i >= C) fetch_wait_done(done, segs, mp, n_seg, __ldg(fp.fetch + i - C), NB);
+      fetch_block(dst_in + (long long)(fp.first_slot + i % C) * inb,
+                  reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(fp.src_in) + e)),
+                  inb, ring, bars, par, fc, nf);
+      fetch_publish(fp.counters + 2 * i, fp.ready_in + e, fp.value, nf);
+    }
+    for (int i = 0; i < min(C, n_fetch); ++i) {
+      const int e = __ldg(fp.fetch + i);
+      fetch_block(dst_out + (long long)(fp.first_slot + i) * outb,
+                  reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(fp.src_out) + e)),
+                  outb, ring, bars, par, fc, nf);
+      fetch_publish(fp.counters + 2 * i + 1, fp.ready_out + e, fp.value, nf);
+    }
+  } else {
+    for (int i = C; i < n_fetch; ++i) {
+      const int e = __ldg(fp.fetch + i);
+      fetch_wait_done(done, segs, mp, n_seg, __ldg(fp.fetch + i - C), NB);
+      fetch_block(dst_out + (long long)(fp.first_slot + i % C) * outb,
+                  reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(fp.src_out) + e)),
+                  outb, ring, bars, par, fc, nf);
+      fetch_publish(fp.counters + 2 * i + 1, fp.ready_out + e, fp.value, nf);
+    }
+  }
+}
+
 template <int kEpi, bool kGather>
 __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kGemmThreads, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -394,9 +513,16 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
                              int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
                              const int* __restrict__ a_gather, int a_gather_div, int a_src_rows,
                              const unsigned long long* __restrict__ out_ptrs, const int* __restrict__ out_split,
-                             int n_out) {
+                             int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (fplan.pairs > 0 && (int)(blockIdx.x >> 1) >= (int)(gridDim.x >> 1) - fplan.pairs) {
+    // K6 fetch pair: both CTAs of the cluster leave before any TMEM / cluster barrier
+    const int fc = (int)blockIdx.x - ((int)gridDim.x - 2 * fplan.pairs);
+    fetch_pair_role(fplan, smem, fc, 2 * fplan.pairs, reinterpret_cast<const int4*>(segs_g), mprefix_g, *n_seg_ptr,
+                    N / kBN, slot_done);
+    return;
+  }
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * 2 * k2Half);
   uint64_t* empty = full + k2Stages;
   uint64_t* tfull = empty + k2Stages;
@@ -410,7 +536,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
   const int lane = threadIdx.x % 32;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1;
-  const int npairs = gridDim.x >> 1;
+  const int npairs = (gridDim.x >> 1) - fplan.pairs;  // compute pairs (fetch pairs, if any, are the last)
   const int n_seg = *n_seg_ptr;
   const bool seg_in_smem = n_seg <= kMaxSmemSegs;
   if (seg_in_smem) {
@@ -475,10 +601,18 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         if (slot_ready != nullptr && seg.z >= ready_from_slot) {
           // watchdog: a fetch that never lands is a bug upstream; fail the launch instead of
           // hanging the device (~10 s)
+#ifdef HM_DEBUG_K6
+          printf("gemm pair %d rank %d tile %d: wait expert %d slot %d flag %d epoch %d\n", pair, rank, t, seg.w, seg.z,
+                 ld_acquire_gpu(slot_ready + seg.w), epoch);
+#endif
           long long spins = 0;
-          while (ld_acquire_gpu(slot_ready + seg.z) < epoch) {
+          while (ld_acquire_gpu(slot_ready + seg.w) < epoch) {
             __nanosleep(128);
-            if (++spins > (1ll << 26)) __trap();
+            if (++spins > (1ll << 26)) {
+              printf("hm grouped_gemm: fetched expert %d (slot %d) never became ready (%d < epoch %d)\n", seg.w,
+                     seg.z, ld_acquire_gpu(slot_ready + seg.w), epoch);
+              __trap();
+            }
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
@@ -694,6 +828,15 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         }
         __syncwarp();
       }
+      // K6 slot reuse: this warp is done with the tile, so its weight loads (TMA, consumed by
+      // the MMAs before tfull fired) are complete; a fetch may overwrite a fetched expert's
+      // cache slot once all 16 epilogue warps of all its tiles have counted here
+      if (slot_done != nullptr && seg.z >= ready_from_slot && lane == 0) {
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(slot_done + seg.w) : "memory");
+#ifdef HM_DEBUG_K6
+        if (ew == 0 && rank == 0) printf("gemm pair %d tile %d: done expert %d\n", pair, t, seg.w);
+#endif
+      }
     }
   }
 
@@ -735,11 +878,59 @@ static bool use_2cta() {
   return v == 1;
 }
 
+// Co-resident CTA pairs of the 2-CTA kernel (cudaOccupancyMaxActiveClusters for its cluster
+// shape, block and smem), cached per device and variant.  The persistent walk assigns tiles to
+// pairs statically, so launching more pairs than can be resident would leave the extra pairs'
+// tiles waiting for a whole pair to retire - and deadlock a GEMM that waits on a concurrent
+// kernel (bounded-cache K6).
+template <int kEpi, bool kGather>
+static int resident_pairs_of() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cache[64] = {0};
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    cudaFuncSetAttribute(grouped_gemm_2cta_kernel<kEpi, kGather>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGemm2Smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(num_sms() & ~1));
+    cfg.blockDim = dim3(kGemmThreads + (kGather ? kALoadWarps * 32 : 0));
+    cfg.dynamicSmemBytes = kGemm2Smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, grouped_gemm_2cta_kernel<kEpi, kGather>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / 2;
+    }
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+int gemm_resident_pairs(int epilogue, bool gather) {
+  switch (epilogue * 2 + (gather ? 1 : 0)) {
+    case kEpiStore * 2: return resident_pairs_of<kEpiStore, false>();
+    case kEpiStore * 2 + 1: return resident_pairs_of<kEpiStore, true>();
+    case kEpiRelu * 2: return resident_pairs_of<kEpiRelu, false>();
+    case kEpiRelu * 2 + 1: return resident_pairs_of<kEpiRelu, true>();
+    case kEpiSwiGLU * 2: return resident_pairs_of<kEpiSwiGLU, false>();
+    case kEpiSwiGLU * 2 + 1: return resident_pairs_of<kEpiSwiGLU, true>();
+    default: return -1;
+  }
+}
+
 int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                         const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
                         const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
-                        const unsigned long long* out_ptrs, const int32_t* out_split, int n_out) {
+                        const unsigned long long* out_ptrs, const int32_t* out_split, int n_out, int32_t* slot_done,
+                        const hm_fetch_plan* fetch) {
   if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
     return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
@@ -748,6 +939,21 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     return set_error(HM_EINVAL, "grouped_gemm: remote output needs out_split and n_out >= 1");
   if (out_ptrs != nullptr && !use_2cta())
     return set_error(HM_EINVAL, "grouped_gemm: remote output needs the 2-CTA kernel (unset HM_GEMM_1CTA)");
+  if (slot_done != nullptr && !use_2cta())
+    return set_error(HM_EINVAL, "grouped_gemm: slot_done counters need the 2-CTA kernel (unset HM_GEMM_1CTA)");
+  hm_fetch_plan fplan = {};
+  if (fetch != nullptr) {
+    fplan = *fetch;
+    if (slot_done == nullptr || !use_2cta())
+      return set_error(HM_EINVAL, "grouped_gemm: fetch pairs need slot_done and the 2-CTA kernel");
+    if (fplan.pairs < 1 || (fplan.phase != 1 && fplan.phase != 2) || fplan.n_slots < 1 || fplan.fetch == nullptr ||
+        fplan.n_fetch == nullptr || fplan.src_in == nullptr || fplan.src_out == nullptr || fplan.ready_in == nullptr ||
+        fplan.ready_out == nullptr || fplan.counters == nullptr || fplan.n_counters < 2 ||
+        fplan.in_bytes % 16 != 0 || fplan.out_bytes % 16 != 0)
+      return set_error(HM_EINVAL, "grouped_gemm: incomplete fetch plan");
+    const cudaError_t me = cudaMemsetAsync(fplan.counters, 0, sizeof(int32_t) * fplan.n_counters, stream);
+    if (me != cudaSuccess) return set_error(HM_ECUDA, "grouped_gemm fetch counters: %s", cudaGetErrorString(me));
+  }
   if (a_rows <= 0) return HM_OK;
   CUtensorMap ta, tb;
   // gathered A: 1-row boxes fetched four at a time by tile::gather4
@@ -775,8 +981,12 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
       if (rc) return rc;
     }
     const bool gather = a_gather != nullptr;
+    // every pair resident at once (static tile walk; the fetch pairs and the compute pairs wait
+    // on each other); fetch pairs come out of the same budget
+    const int pairs = min(num_sms() / 2, gemm_resident_pairs(epilogue, gather));
+    if (pairs - fplan.pairs < 1) return set_error(HM_EINVAL, "grouped_gemm: no compute pair left beside the fetch pairs");
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(grid & ~1));
+    cfg.gridDim = dim3((unsigned)(2 * pairs));
     cfg.blockDim = dim3(kGemmThreads + (gather ? kALoadWarps * 32 : 0));
     cfg.dynamicSmemBytes = kGemm2Smem;
     cfg.stream = stream;
@@ -796,7 +1006,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, ta64, tb64, half_tiles, s4,          \
                            mtile_prefix, n_seg, o, N, K,                                                          \
                            ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
-                           (int)a_rows, out_ptrs, out_split, n_out);                                              \
+                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan);                            \
   } while (0)
     switch (epilogue * 2 + (gather ? 1 : 0)) {
       case kEpiStore * 2: HM_GEMM2(kEpiStore, false); break;

@@ -25,7 +25,9 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
                         const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
                         const unsigned long long* out_ptrs = nullptr, const int32_t* out_split = nullptr,
-                        int n_out = 0);
+                        int n_out = 0, int32_t* slot_done = nullptr, const hm_fetch_plan* fetch = nullptr);
+
+int gemm_resident_pairs(int epilogue, bool gather);
 
 int launch_router(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
                   int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,

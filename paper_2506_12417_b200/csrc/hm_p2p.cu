@@ -15,8 +15,10 @@
 //                        receive buffer, with its token-major index (t*k + j) beside it.
 //   fetch_kernel         K6 driven from the device: copies the plan's fetch list (peer HBM
 //                        over NVLink, or pinned host memory) into the cache slots in plan
-//                        order and publishes a ready flag per slot (the FFN GEMM producer
-//                        waits per slot), so the fetch list never visits the host.
+//                        order and publishes a ready flag per expert (the FFN GEMM producer
+//                        waits per expert), so the fetch list never visits the host.  (A
+//                        bounded cache is fetched by pairs inside the GEMM launch instead,
+//                        hm_gemm.cu, so fetch and GEMM are co-resident by construction.)
 //
 // The FFN2 GEMM stores its rows straight into the source rank's token-major output
 // (hm_gemm.cu remote epilogue), which is the combine all-to-all fused into the GEMM.
@@ -156,15 +158,18 @@ __global__ void __launch_bounds__(kFetchThreads)
                  const unsigned long long* __restrict__ src_in, const unsigned long long* __restrict__ src_out,
                  int64_t in16, int64_t out16, uint4* __restrict__ dst_in, uint4* __restrict__ dst_out, int first_slot,
                  int n_slots, int32_t* __restrict__ ready_in, int32_t* __restrict__ ready_out,
-                 int32_t* __restrict__ counters, int value) {
-  const int n_fetch = min(*n_fetch_p, n_slots);
+                 int32_t* __restrict__ counters, int n_counters, int value) {
+  const int n_fetch = *n_fetch_p;
+  // more fetches than slots (a bounded cache belongs to the in-GEMM fetch pairs, hm_gemm.cu):
+  // fail the launch loudly rather than leave the GEMM waiting on (or reading) unfilled slots
+  if (n_fetch > n_slots || 2 * n_fetch > n_counters) __trap();
   for (int i = 0; i < n_fetch; ++i) {
     const int e = __ldg(fetch + i);
     const int slot = first_slot + i;
     copy_block(dst_in + (int64_t)slot * in16, reinterpret_cast<const uint4*>(__ldg(src_in + e)), in16);
-    block_done(counters + 2 * i, ready_in + slot, value);
+    block_done(counters + 2 * i, ready_in + e, value);
     copy_block(dst_out + (int64_t)slot * out16, reinterpret_cast<const uint4*>(__ldg(src_out + e)), out16);
-    block_done(counters + 2 * i + 1, ready_out + slot, value);
+    block_done(counters + 2 * i + 1, ready_out + e, value);
   }
 }
 
@@ -206,15 +211,16 @@ int launch_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* 
 int launch_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const unsigned long long* src_in,
                          const unsigned long long* src_out, size_t in_bytes, size_t out_bytes, void* dst_in,
                          void* dst_out, int first_slot, int n_slots, int32_t* ready_in, int32_t* ready_out,
-                         int32_t* counters, int value, int ctas, cudaStream_t stream) {
+                         int32_t* counters, int n_counters, int value, int ctas, cudaStream_t stream) {
   if (in_bytes % 16 != 0 || out_bytes % 16 != 0) return set_error(HM_EINVAL, "fetch_experts: sizes must be 16-byte multiples");
   if (n_slots <= 0) return HM_OK;
-  cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int32_t) * 2 * n_slots, stream);
+  if (n_counters < 2) return set_error(HM_EINVAL, "fetch_experts: counters too small");
+  cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int32_t) * n_counters, stream);
   if (e != cudaSuccess) return set_error(HM_ECUDA, "fetch_experts memset: %s", cudaGetErrorString(e));
   fetch_kernel<<<ctas > 0 ? ctas : 32, kFetchThreads, 0, stream>>>(
       fetch, n_fetch, src_in, src_out, (int64_t)(in_bytes / 16), (int64_t)(out_bytes / 16),
       reinterpret_cast<uint4*>(dst_in), reinterpret_cast<uint4*>(dst_out), first_slot, n_slots, ready_in, ready_out,
-      counters, value);
+      counters, n_counters, value);
   return check_launch("fetch_experts");
 }
 

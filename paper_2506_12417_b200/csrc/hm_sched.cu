@@ -390,6 +390,7 @@ struct LayoutOut {
   int32_t* mprefix;
   int32_t* fetch;
   int32_t* n_fetch;
+  int cache_slots;  // EP: fetch cache slots (0 = one per fetched expert); fetch i -> slot n_home + i % cache_slots
 };
 
 // plan-order sort key (ascending = execution order): residents first, then more tokens,
@@ -599,8 +600,11 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       wslot = 0;
       for (int e2 = 0; e2 < e; ++e2) wslot += (home[e2] == me);
     } else {
-      wslot = n_home + (oo - n_res_work);
-      o.fetch[oo - n_res_work] = e;
+      // bounded cache: fetch i reuses the slot of fetch i - cache_slots, the one whose occupant
+      // finishes first (fetched experts compute in plan order; engine.py:239-257)
+      const int fi = oo - n_res_work;
+      wslot = n_home + (o.cache_slots > 0 ? fi % o.cache_slots : fi);
+      o.fetch[fi] = e;
     }
     int sidx = s_cnt[oo];
     for (int g = 0; g < G; ++g) {
@@ -799,12 +803,13 @@ static int check_layout_args(int G, int E, int mode, int me) {
 
 int launch_layout(const int32_t* S, const int32_t* home, int G, int E, int mode, int me, int32_t* slot_base,
                   int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch,
-                  cudaStream_t stream) {
+                  int cache_slots, cudaStream_t stream) {
   int rc = check_layout_args(G, E, mode, me);
   if (rc) return rc;
+  if (cache_slots < 0) return set_error(HM_EINVAL, "dispatch_layout: cache_slots must be >= 0");
   const size_t smem = (size_t)layout_scratch_ints(G, E) * sizeof(int);
   cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
+  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch, cache_slots};
   layout_kernel<<<1, kPlanThreads, smem, stream>>>(S, home, G, E, mode, me, o);
   return check_launch("dispatch_layout");
 }
@@ -821,8 +826,9 @@ static bool use_plan_g1() {  // HM_PLAN_G1=0: the general planner at G = 1 too (
 int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_in, const int32_t* home, int G, int E,
                 int q, int rebalance, int mode, int me, int32_t* m_out, int32_t* tile_off, int32_t* S, int32_t* iters,
                 int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix,
-                int32_t* fetch, int32_t* n_fetch, cudaStream_t stream) {
+                int32_t* fetch, int32_t* n_fetch, int cache_slots, cudaStream_t stream) {
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
+  if (cache_slots < 0) return set_error(HM_EINVAL, "plan: cache_slots must be >= 0");
   int rc = check_layout_args(G, E, mode, me);
   if (rc) return rc;
   if (rebalance < HM_POLICY_NONE || rebalance > HM_POLICY_EVEN_SPLIT)
@@ -832,7 +838,7 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   if (!hist && m_in == nullptr) return set_error(HM_EINVAL, "plan: need tile_hist or m_all");
   const size_t smem = (size_t)(E + G * E + 2 * G * E * G + layout_scratch_ints(G, E)) * sizeof(int);
   if (smem > 200 * 1024) return set_error(HM_EINVAL, "plan: G*E*G too large for the fused planner; use hm_schedule");
-  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch};
+  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch, cache_slots};
   if (hist && G == 1 && use_plan_g1()) {
     const size_t smem1 = (size_t)(3 * E + 2) * sizeof(int) + 8 + (size_t)E * 8;
     cudaFuncSetAttribute(plan_g1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);

@@ -127,7 +127,21 @@ class EPHarMoEnyBlock:
         self.home = torch.from_numpy(self.home_np).to(device)
         self.home_experts = [e for e in range(E) if self.home_np[e] == self.me]
         self.n_home = len(self.home_experts)
-        self.n_cache = cfg.expert_cache_size if cfg.expert_cache_size > 0 else E - self.n_home
+        # K6 cache slots beside the home experts.  expert_cache_size = 0: one per expert this rank
+        # could ever fetch.  A smaller cache is the reference's bounded expert cache
+        # (engine.py:204-275): fetch i overwrites the slot of fetch i - n_cache once the GEMMs have
+        # finished that expert (the earliest slot to free up, fetched experts running in plan
+        # order).  Home slots are never overwritten: they are the master copies the other ranks
+        # fetch from over NVLink (the reference's overwritable residents assume a host master).
+        n_fetchable = E - self.n_home
+        self.n_cache = cfg.expert_cache_size if cfg.expert_cache_size > 0 else n_fetchable
+        self.bounded = 0 < self.n_cache < n_fetchable
+        # bounded cache: the channel must wait on the GEMMs' progress (a slot frees when its
+        # occupant's tiles are done) while the GEMMs wait on the channel, so the copy runs as
+        # FETCH_PAIRS CTA pairs inside each GEMM launch (hm_fetch_plan): co-resident by
+        # construction.  A separate copy kernel or copy-engine stream cannot guarantee that
+        # (measured: a stream aliasing the GEMM's hardware queue serialises behind it and
+        # deadlocks)
         if cfg.activation == "swiglu":
             if w3 is None:
                 raise ValueError("SwiGLU experts need w3")
@@ -158,8 +172,13 @@ class EPHarMoEnyBlock:
         else:
             raise ValueError("fetch_source must be 'peer' or 'host'")
         del w_in_all, w_out_all
-        self.ready_in = torch.zeros(slots, dtype=torch.int32, device=device)
-        self.ready_out = torch.zeros(slots, dtype=torch.int32, device=device)
+        # per-EXPERT ready flags (a bounded cache reuses slots within one forward) and the GEMMs'
+        # per-expert tile completion counters (slot reuse)
+        self.ready_in = torch.zeros(E, dtype=torch.int32, device=device)
+        self.ready_out = torch.zeros(E, dtype=torch.int32, device=device)
+        self.done_in = torch.zeros(E, dtype=torch.int32, device=device)
+        self.done_out = torch.zeros(E, dtype=torch.int32, device=device)
+        self._fetch_sources()
         self.epoch = 0
         self.fetch_stream = torch.cuda.Stream(device=device)
         self._last_gemm = None
@@ -170,6 +189,37 @@ class EPHarMoEnyBlock:
             self._setup_p2p()
             # ours: router, hist_scan, plan, ep_offsets, dispatch_push, fetch, gemm1, gemm2, combine
             self.KERNELS_PER_FORWARD = 9
+
+    FETCH_PAIRS = 2  # CTA pairs of each GEMM launch that run the bounded-cache K6 channel
+
+    def _fetch_sources(self):
+        """Device tables of every expert's weight blocks at its home rank (NVLink, CUDA IPC) or
+        in pinned host memory: the sources of the device-driven K6 (fetch kernel or the fetch
+        pairs inside the GEMM launches)."""
+        cfg, E, d = self.cfg, self.cfg.num_experts, self.cfg.d_model
+        in_bytes, out_bytes = self.n_in * d * 2, d * cfg.d_ff * 2
+        src_in, src_out = [], []
+        for e in range(E):
+            h, hs = int(self.home_np[e]), self._hslot[e]
+            if self.fetch_source == "host":
+                src_in.append(self.w_in_host[e].data_ptr())
+                src_out.append(self.w_out_host[e].data_ptr())
+            else:
+                src_in.append(self.peer_in[h] + hs * in_bytes)
+                src_out.append(self.peer_out[h] + hs * out_bytes)
+        i64 = dict(dtype=torch.int64, device=self.device)
+        self._src_host = (src_in, src_out)
+        self.fetch_src_in = torch.tensor(src_in, **i64)
+        self.fetch_src_out = torch.tensor(src_out, **i64)
+        self.fetch_counters = torch.zeros(2 * E, dtype=torch.int32, device=self.device)
+
+    def _fetch_plan(self, lay, phase: int, value: int):
+        """hm_fetch_plan of a bounded cache: fetch i -> slot n_home + i % n_cache once expert
+        fetch[i - n_cache]'s tiles are done (engine.py:239-257 overwrite order)."""
+        d, f = self.cfg.d_model, self.cfg.d_ff
+        return ops.fetch_plan(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.w_in, self.w_out,
+                              self.n_in * d * 2, d * f * 2, self.n_home, self.n_cache, self.ready_in, self.ready_out,
+                              self.fetch_counters, value, phase, pairs=self.FETCH_PAIRS)
 
     @classmethod
     def random(cls, cfg: MoEConfig, seed: int = 0, device="cuda", zipf_s=None, std: float = 0.02, group=None):
@@ -287,29 +337,16 @@ class EPHarMoEnyBlock:
         self.mall_row_addrs = [b + lay["m_all"] + me * E * 4 for b in bases]
         base0 = self.arena.data_ptr() + lay["flags"]
         self.local_flag_addrs = [[base0 + (c * G + g) * 4 for g in range(G)] for c in range(3)]
-        # device fetch sources: expert e at its home rank (NVLink) or in pinned host memory
-        in_bytes, out_bytes = self.n_in * d * 2, d * cfg.d_ff * 2
-        src_in, src_out = [], []
-        for e in range(E):
-            h, hs = int(self.home_np[e]), self._hslot[e]
-            if self.fetch_source == "host":
-                src_in.append(self.w_in_host[e].data_ptr())
-                src_out.append(self.w_out_host[e].data_ptr())
-            else:
-                src_in.append(self.peer_in[h] + hs * in_bytes)
-                src_out.append(self.peer_out[h] + hs * out_bytes)
-        self.fetch_src_in = torch.tensor(src_in, **i64)
-        self.fetch_src_out = torch.tensor(src_out, **i64)
-        self.fetch_counters = torch.zeros(2 * max(self.n_cache, 1), dtype=torch.int32, device=self.device)
         self.dst_delta = torch.empty(G, dtype=torch.int32, device=self.device)
         self.recv_split = torch.empty(G + 1, dtype=torch.int32, device=self.device)
         dist.barrier(group=self.group)  # every arena zeroed and mapped before anyone signals
 
     def _p2p_stages(self, st, s):
-        """The p2p forward as three stream-ordered stages over the state dict ``st`` (input
-        st["x"]): "dispatch" (router, metadata push, plan, fused scatter + dispatch push),
-        "gemm1" (device-driven fetch forked onto the fetch stream + FFN1, joined), "combine"
-        (FFN2 storing into the source ranks + combine).  Each stage is graph-capturable."""
+        """The p2p forward as stream-ordered stages over the state dict ``st`` (input st["x"]):
+        "dispatch" (router, metadata push, plan, fused scatter + dispatch push), "gemm1"
+        (device-driven fetch forked onto the fetch stream + FFN1, joined; bounded cache: fetch
+        pairs inside FFN1), "combine" (FFN2 storing into the source ranks - bounded cache: with
+        its fetch pairs - + combine).  Each stage is graph-capturable."""
         cfg, G, E, me = self.cfg, self.G, self.cfg.num_experts, self.me
         k, d = cfg.top_k, cfg.d_model
         L = _lib.load()
@@ -329,7 +366,7 @@ class EPHarMoEnyBlock:
             ops.stream_wait(self.flags[0], 1, s)
             ops.stream_signal(self.local_flag_addrs[0], 0, s)
             p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
-                         stream=s)
+                         cache_slots=self.n_cache if self.bounded else 0, stream=s)
             m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
             ops.ep_offsets(p.S, me, self.dst_delta, self.recv_split, stream=s)
             pos = torch.empty((Tg, k), dtype=torch.int32, device=self.device)
@@ -342,30 +379,39 @@ class EPHarMoEnyBlock:
             self.stats = BlockStats(m_all=m_all, schedule=p.S, iters=p.iters, loads=p.loads,
                                     extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=p.layout))
 
+        # K6 from the device-side fetch list on the fetch stream, overlapping FFN1 (async), or in
+        # stream order ahead of it (sync ablation: the GEMM's ready-flag waits pass at once); a
+        # bounded cache runs it inside the GEMM launches instead (fetch pairs, see __init__)
+        fs = self.fetch_stream if cfg.async_fetch else s
+
         def gemm1():
             lay = st["plan"].layout
-            # K6 from the device-side fetch list on the fetch stream, overlapping FFN1 (async), or
-            # in stream order ahead of it (sync ablation: the GEMM's ready-flag waits pass at once)
-            fs = self.fetch_stream if cfg.async_fetch else s
-            if self.n_cache > 0:
+            kw = {}
+            if self.bounded:
+                kw = dict(slot_done=self.done_in, fetch=self._fetch_plan(lay, 1, 1))
+            elif self.n_cache > 0:
                 if fs is not s:
                     fs.wait_stream(s)
                 ops.fetch_experts(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.n_in * d * 2,
                                   d * cfg.d_ff * 2, self.w_in, self.w_out, self.n_home, self.n_cache, self.ready_in,
                                   self.ready_out, self.fetch_counters, value=1, stream=fs)
             ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
-                             slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s)
-            if self.n_cache > 0 and fs is not s:
+                             slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s, **kw)
+            if self.n_cache > 0 and fs is not s and not self.bounded:
                 s.wait_stream(fs)
 
         def combine():
             lay = st["plan"].layout
+            kw = dict(slot_done=self.done_out, fetch=self._fetch_plan(lay, 2, 1)) if self.bounded else {}
             ops.grouped_gemm_remote(self.h_buf, self.w_out.view(-1, cfg.d_ff), d, lay, ops.HM_EPI_STORE,
                                     self.p2p_out, self.recv_split, self.recv_tok, slot_ready=self.ready_out,
-                                    ready_from_slot=self.n_home, epoch=1, stream=s)
+                                    ready_from_slot=self.n_home, epoch=1, stream=s, **kw)
             if self.n_cache > 0:
-                self.ready_in[self.n_home:].zero_()
-                self.ready_out[self.n_home:].zero_()
+                self.ready_in.zero_()
+                self.ready_out.zero_()
+                if self.bounded:
+                    self.done_in.zero_()
+                    self.done_out.zero_()
             ops.stream_signal(self.y_addrs, 1, s)
             ops.stream_wait(self.flags[2], 1, s)
             ops.stream_signal(self.local_flag_addrs[2], 0, s)
@@ -410,8 +456,11 @@ class EPHarMoEnyBlock:
         return CapturedForward(graphs, x, st["y"], self.stats)
 
     def _fetch(self, experts):
-        """K6: one transfer channel (the fetch stream), plan order, overwrite semantics:
-        fetched experts land in cache slots n_home + i and publish ready flags."""
+        """K6 on the copy engines (no SM taken from the GEMMs): one transfer channel (the fetch
+        stream), plan order, fetched experts in cache slots n_home + i, a ready flag per expert.
+        (A bounded cache is fetched by the pairs inside the GEMM launches instead.)"""
+        if self.bounded:
+            return
         if len(experts) > self.n_cache:
             raise RuntimeError(f"{len(experts)} experts to fetch exceed the {self.n_cache} cache slots")
         d, f = self.cfg.d_model, self.cfg.d_ff
@@ -425,19 +474,12 @@ class EPHarMoEnyBlock:
         L = _lib.load()
         for i, e in enumerate(experts):
             slot = self.n_home + i
-            h = int(self.home_np[e])
-            hs = self._hslot[e]
-            if self.fetch_source == "host":
-                src_in = self.w_in_host[e].data_ptr()
-                src_out = self.w_out_host[e].data_ptr()
-            else:
-                src_in = self.peer_in[h] + hs * in_bytes
-                src_out = self.peer_out[h] + hs * out_bytes
+            src_in, src_out = self._src_host[0][e], self._src_host[1][e]
             _lib.check(L.hm_fetch_expert(self.w_in[slot].data_ptr(), src_in, in_bytes,
-                                         self.ready_in[slot:].data_ptr(), self.epoch, s.cuda_stream),
+                                         self.ready_in[e:].data_ptr(), self.epoch, s.cuda_stream),
                        "hm_fetch_expert")
             _lib.check(L.hm_fetch_expert(self.w_out[slot].data_ptr(), src_out, out_bytes,
-                                         self.ready_out[slot:].data_ptr(), self.epoch, s.cuda_stream),
+                                         self.ready_out[e:].data_ptr(), self.epoch, s.cuda_stream),
                        "hm_fetch_expert")
 
     def forward(self, x: torch.Tensor, stream=None, marks=None) -> torch.Tensor:
@@ -465,7 +507,8 @@ class EPHarMoEnyBlock:
             hist, tile_off = ops.hist_scan(tile_hist, 1, tiles, stream=s)
             mark("router")
             m_all = exchange_metadata(hist, self.group)
-            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP, me, m_all=m_all, stream=s)
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP, me, m_all=m_all,
+                         cache_slots=self.n_cache if self.bounded else 0, stream=s)
             S, iters, loads, lay = p.S, p.iters, p.loads, p.layout
             self.S_host.copy_(S, non_blocking=True)
             self.fetch_host[:E].copy_(lay.fetch, non_blocking=True)
@@ -480,12 +523,18 @@ class EPHarMoEnyBlock:
             mark("permute")
             recv = exchange_tokens(send, send_counts, recv_counts, self.group)
             mark("dispatch_a2a")
+            dn_in = dict(slot_done=self.done_in, fetch=self._fetch_plan(lay, 1, self.epoch)) if self.bounded else {}
+            dn_out = dict(slot_done=self.done_out, fetch=self._fetch_plan(lay, 2, self.epoch)) if self.bounded else {}
             h = ops.grouped_gemm(recv, self.w_in.view(-1, cfg.d_model), self.n_in, lay, self.epi_in,
-                                 slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=self.epoch, stream=s)
+                                 slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=self.epoch, stream=s,
+                                 **dn_in)
             mark("gemm1")
             yr = ops.grouped_gemm(h, self.w_out.view(-1, cfg.d_ff), cfg.d_model, lay, ops.HM_EPI_STORE,
                                   slot_ready=self.ready_out, ready_from_slot=self.n_home, epoch=self.epoch,
-                                  stream=s)
+                                  stream=s, **dn_out)
+            if self.bounded:  # the next forward's fetch pairs wait on fresh counts
+                self.done_in.zero_()
+                self.done_out.zero_()
             self._last_gemm = torch.cuda.Event()
             self._last_gemm.record(s)
             mark("gemm2")

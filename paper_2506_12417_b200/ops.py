@@ -152,7 +152,7 @@ class Layout:
         self.mtile_prefix, self.fetch, self.n_fetch = mtile_prefix, fetch, n_fetch
 
 
-def dispatch_layout(S, home, mode: int, me: int = 0, stream=None) -> Layout:
+def dispatch_layout(S, home, mode: int, me: int = 0, cache_slots: int = 0, stream=None) -> Layout:
     _require_cuda(S, home)
     G, E, _ = S.shape
     dev = S.device
@@ -164,7 +164,7 @@ def dispatch_layout(S, home, mode: int, me: int = 0, stream=None) -> Layout:
     fetch = torch.empty(E, dtype=torch.int32, device=dev)
     n_fetch = torch.empty(1, dtype=torch.int32, device=dev)
     _lib.call("hm_dispatch_layout", _ptr(S), _ptr(home), G, E, int(mode), int(me), _ptr(slot_base), _ptr(segs),
-              _ptr(n_seg), _ptr(mprefix), _ptr(fetch), _ptr(n_fetch), _stream(stream))
+              _ptr(n_seg), _ptr(mprefix), _ptr(fetch), _ptr(n_fetch), int(cache_slots), _stream(stream))
     return Layout(slot_base, segs, n_seg, mprefix, fetch, n_fetch)
 
 
@@ -178,7 +178,7 @@ class Plan:
 
 
 def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, tile_hist=None,
-         tiles_per_rank: int = 0, m_all=None, stream=None) -> Plan:
+         tiles_per_rank: int = 0, m_all=None, cache_slots: int = 0, stream=None) -> Plan:
     """Fused planner: (hist reduce) + schedule + layout in one launch."""
     _require_cuda(home, tile_hist, m_all)
     dev = home.device
@@ -195,7 +195,8 @@ def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, 
     _lib.call("hm_plan", _ptr(tile_hist), int(tiles_per_rank), _ptr(m_all), _ptr(home), G, E, int(q),
               _policy(rebalance), int(mode), int(me), _ptr(m_out) if tile_hist is not None else None,
               _ptr(tile_off), _ptr(S), _ptr(iters), _ptr(loads), _ptr(lay.slot_base), _ptr(lay.segs),
-              _ptr(lay.n_seg), _ptr(lay.mtile_prefix), _ptr(lay.fetch), _ptr(lay.n_fetch), _stream(stream))
+              _ptr(lay.n_seg), _ptr(lay.mtile_prefix), _ptr(lay.fetch), _ptr(lay.n_fetch), int(cache_slots),
+              _stream(stream))
     return Plan(m_out, tile_off, S, iters, loads, lay)
 
 
@@ -223,7 +224,7 @@ def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per
 
 def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=None, slot_ready=None,
                  ready_from_slot: int = 0, epoch: int = 0, a_gather=None, a_gather_div: int = 1, out_rows=None,
-                 stream=None):
+                 slot_done=None, fetch=None, stream=None):
     """K5.  A [rows, K] bf16, W [slots*N, K] bf16 -> out [rows, N or N/2] bf16
     (row r written to row_map[r] when a row map is given).  With a_gather, buffer row r
     reads A[a_gather[r] // a_gather_div] (cp.async loader warps in the 2-CTA kernel, TMA
@@ -232,9 +233,10 @@ def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=
         segs, n_seg, mprefix = layout_or_segs.segs, layout_or_segs.n_seg, layout_or_segs.mtile_prefix
     else:
         segs, n_seg, mprefix = layout_or_segs
-    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready, row_map, a_gather)
+    _require_cuda(A, W, segs, n_seg, mprefix, slot_ready, row_map, a_gather, slot_done)
     _require_dtype(torch.bfloat16, A, W, out, what="grouped_gemm operands")
-    _require_dtype(torch.int32, segs, n_seg, mprefix, row_map, a_gather, slot_ready, what="grouped_gemm index tensors")
+    _require_dtype(torch.int32, segs, n_seg, mprefix, row_map, a_gather, slot_ready, slot_done,
+                   what="grouped_gemm index tensors")
     rows, K = A.shape
     if a_gather is not None:
         rows_out = out_rows if out_rows is not None else a_gather.numel()
@@ -245,8 +247,26 @@ def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=
         out = torch.empty((max(rows_out, 1), ncols), dtype=torch.bfloat16, device=A.device)
     _lib.call("hm_grouped_gemm", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(segs), _ptr(n_seg), _ptr(mprefix),
               int(epilogue), _ptr(out), _ptr(row_map), _ptr(a_gather), int(a_gather_div), _ptr(slot_ready),
-              int(ready_from_slot), int(epoch), _stream(stream))
+              int(ready_from_slot), int(epoch), _ptr(slot_done), _fetch_ref(fetch), _stream(stream))
     return out
+
+
+def fetch_plan(fetch, n_fetch, src_in, src_out, dst_in, dst_out, in_bytes: int, out_bytes: int, first_slot: int,
+               n_slots: int, ready_in, ready_out, counters, value: int, phase: int, pairs: int = 2):
+    """hm_fetch_plan for the K6 fetch pairs of a grouped-GEMM launch (bounded expert cache):
+    phase 1 = the FFN1 launch, 2 = the FFN2 launch.  Keep the returned object alive until the
+    launch call returns (the struct is copied into the kernel parameters)."""
+    _require_cuda(fetch, n_fetch, src_in, src_out, dst_in, dst_out, ready_in, ready_out, counters)
+    _require_dtype(torch.int32, fetch, n_fetch, ready_in, ready_out, counters, what="fetch plan index tensors")
+    return _lib.FetchPlan(_ptr(fetch), _ptr(n_fetch), _ptr(src_in), _ptr(src_out), _ptr(dst_in), _ptr(dst_out),
+                          int(in_bytes), int(out_bytes), int(first_slot), int(n_slots), _ptr(ready_in),
+                          _ptr(ready_out), _ptr(counters), counters.numel(), int(value), int(pairs), int(phase))
+
+
+def _fetch_ref(fp):
+    import ctypes
+
+    return None if fp is None else ctypes.addressof(fp)
 
 
 def fetch_expert(dst, src, ready_flag=None, epoch: int = 0, stream=None):
@@ -299,23 +319,25 @@ def dispatch_push(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, me: int
 
 
 def grouped_gemm_remote(A, W, N: int, layout: "Layout", epilogue: int, out_ptrs, out_split, row_map, slot_ready=None,
-                        ready_from_slot: int = 0, epoch: int = 0, a_rows: int | None = None, stream=None):
+                        ready_from_slot: int = 0, epoch: int = 0, a_rows: int | None = None, slot_done=None,
+                        fetch=None, stream=None):
     """K5 with the rows of each segment stored into the owning source rank's buffer (peer pointer)."""
-    _require_cuda(A, W, out_ptrs, out_split, row_map, slot_ready)
+    _require_cuda(A, W, out_ptrs, out_split, row_map, slot_ready, slot_done)
     rows = A.shape[0] if a_rows is None else int(a_rows)
     K = A.shape[1]
     _lib.call("hm_grouped_gemm_remote", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(layout.segs),
               _ptr(layout.n_seg), _ptr(layout.mtile_prefix), int(epilogue), _ptr(out_ptrs), _ptr(out_split),
-              out_ptrs.numel(), _ptr(row_map), _ptr(slot_ready), int(ready_from_slot), int(epoch), _stream(stream))
+              out_ptrs.numel(), _ptr(row_map), _ptr(slot_ready), int(ready_from_slot), int(epoch), _ptr(slot_done),
+              _fetch_ref(fetch), _stream(stream))
 
 
 def fetch_experts(fetch, n_fetch, src_in, src_out, in_bytes: int, out_bytes: int, dst_in, dst_out, first_slot: int,
                   n_slots: int, ready_in, ready_out, counters, value: int = 1, ctas: int = 0, stream=None):
-    """Device-driven K6 over the layout's fetch list (no host round trip)."""
+    """Device-driven K6 over the layout's fetch list (no host round trip); ready flags per expert."""
     _require_cuda(fetch, n_fetch, src_in, src_out, dst_in, dst_out, ready_in, ready_out, counters)
     _lib.call("hm_fetch_experts", _ptr(fetch), _ptr(n_fetch), _ptr(src_in), _ptr(src_out), int(in_bytes),
               int(out_bytes), _ptr(dst_in), _ptr(dst_out), int(first_slot), int(n_slots), _ptr(ready_in),
-              _ptr(ready_out), _ptr(counters), int(value), int(ctas), _stream(stream))
+              _ptr(ready_out), _ptr(counters), counters.numel(), int(value), int(ctas), _stream(stream))
 
 
 def stream_signal(addresses, value: int, stream=None):

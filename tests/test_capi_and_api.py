@@ -199,3 +199,17 @@ def test_replace_moe_layer_takes_routing_semantics_from_the_module():
     assert _routing_config(nn.Module(), nn.Linear(256, 16), cfg).renormalize is True  # no attribute: keep
     with pytest.raises(ValueError, match="top-2"):
         _routing_config(nn.Module(), Router(2, True), cfg)
+
+
+def test_bounded_cache_needs_async_fetch():
+    """Synchronous loading (fetches in stream order ahead of FFN1) cannot wait for cache slots
+    that only FFN1 / FFN2 free, so a bounded expert cache with async_fetch=False is rejected."""
+    from paper_2506_12417_b200 import MoEConfig
+
+    kw = dict(d_model=256, num_experts=16, d_ff=256, top_k=2, world_size=2, rank=0)
+    MoEConfig(expert_cache_size=2, **kw)  # async: fine
+    MoEConfig(expert_cache_size=8, async_fetch=False, **kw)  # every fetchable expert has a slot
+    with pytest.raises(ValueError, match="async_fetch"):
+        MoEConfig(expert_cache_size=2, async_fetch=False, **kw)
+    with pytest.raises(ValueError, match="expert_cache_size"):
+        MoEConfig(expert_cache_size=-1, **kw)

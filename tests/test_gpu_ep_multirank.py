@@ -31,7 +31,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, fetch_source, transport, out_q):
+def _worker(rank, world, port, fetch_source, transport, out_q, cache=0):
     import sys
 
     sys.path.insert(0, REPO)
@@ -43,7 +43,8 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
         from paper_2506_12417_b200.ep import EPHarMoEnyBlock
 
         cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, transport=transport.split("-")[0],
-                        max_tokens_per_rank=T // world, async_fetch="sync" not in transport, **KW)
+                        max_tokens_per_rank=T // world, async_fetch="sync" not in transport,
+                        expert_cache_size=cache, **KW)
         blk = EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
         g = torch.Generator(device="cuda").manual_seed(99)
         x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
@@ -65,16 +66,20 @@ def _worker(rank, world, port, fetch_source, transport, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fetch_source,transport,world", [("peer", "nccl", 2), ("host", "nccl", 2),
-                                                           ("peer", "p2p", 2), ("host", "p2p", 2),
-                                                           ("peer", "p2p", 4), ("peer", "p2p-graph", 2),
-                                                           ("host", "p2p-graph", 4), ("peer", "nccl-sync", 2),
-                                                           ("peer", "p2p-sync", 2)])
-def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
+@pytest.mark.parametrize("fetch_source,transport,world,cache", [
+    ("peer", "nccl", 2, 0), ("host", "nccl", 2, 0), ("peer", "p2p", 2, 0), ("host", "p2p", 2, 0),
+    ("peer", "p2p", 4, 0), ("peer", "p2p-graph", 2, 0), ("host", "p2p-graph", 4, 0), ("peer", "nccl-sync", 2, 0),
+    ("peer", "p2p-sync", 2, 0),
+    # bounded expert cache (engine.py:204-275 overwrite semantics): fewer slots than fetches
+    ("peer", "nccl", 2, 1), ("host", "nccl", 4, 1), ("peer", "p2p", 2, 1), ("host", "p2p", 4, 1),
+    ("peer", "p2p-graph", 2, 1), ("peer", "p2p-graph", 4, 1), ("peer", "nccl", 4, 1)])
+def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world, cache):
     """transport "nccl": exchanges through the process group (gloo here, host-staged);
     transport "p2p": one-sided pushes into the other ranks' IPC-mapped buffers + stream flags,
     no collective and no host round trip inside the forward.  "-sync": the synchronous-loading
-    ablation (expert fetches in stream order ahead of FFN1, SimFlags.async_loading_enabled=False)."""
+    ablation (expert fetches in stream order ahead of FFN1, SimFlags.async_loading_enabled=False).
+    cache > 0: expert_cache_size slots, fewer than the experts a rank fetches, so fetches reuse
+    slots as the GEMMs finish their occupants; outputs stay bit-identical."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
@@ -82,7 +87,7 @@ def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, fetch_source, transport, out_q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fetch_source, transport, out_q, cache))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -107,6 +112,8 @@ def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world):
     for r in range(1, world):
         assert np.array_equal(res[0][2], res[r][2]), "replicated schedules differ"
     assert sum(res[r][3] for r in range(world)) > 0, "the skewed schedule should make some rank fetch experts"
+    if cache:
+        assert max(res[r][3] for r in range(world)) > cache, "some rank must fetch more experts than it has slots"
     for r in range(world):
         y0, y1, _, _ = res[r]
         assert np.array_equal(y0, y_ref[r * Tg:(r + 1) * Tg])
@@ -186,3 +193,4 @@ def test_peer_access_failure_is_collective():
     Tg = T // world
     for r in range(world):
         assert np.array_equal(res[r][1], y_ref[r * Tg:(r + 1) * Tg])
+
