@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "hm_common.cuh"
@@ -232,13 +233,25 @@ int hm_stream_signal(void* const* flags, int n, uint32_t value, void* stream) {
   std::call_once(g_driver_once, load_driver_entry_points);
   if (n < 0 || (n > 0 && flags == nullptr)) return set_error(HM_EINVAL, "stream_signal: bad flag list");
   cudaStream_t s = as_stream(stream);
-  static bool memops_ok = true;  // cleared once the driver refuses a stream write (e.g. to peer memory)
+  // Per device: cleared once the driver refuses a stream write to a VALID address (e.g. peer
+  // memory on some driver / topology), after which flags are published by a kernel.  A refusal
+  // for an address that is not mapped at all stays an error (a bad flag pointer must not turn
+  // into an illegal-address fault inside the fallback kernel).
+  static std::atomic<int> memops_refused[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& refused = memops_refused[(dev >= 0 && dev < 64) ? dev : 0];
   for (int i = 0; i < n; ++i) {
-    if (g_write32 != nullptr && memops_ok) {
+    if (g_write32 != nullptr && refused.load(std::memory_order_relaxed) == 0) {
       const CUresult r = g_write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flags[i]),
                                    (cuuint32_t)value, CU_STREAM_WRITE_VALUE_DEFAULT);
       if (r == CUDA_ERROR_NOT_SUPPORTED || r == CUDA_ERROR_INVALID_VALUE) {
-        memops_ok = false;  // fall through to the kernel publish for this and later flags
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (g_addr_range == nullptr ||
+            g_addr_range(&base, &size, reinterpret_cast<CUdeviceptr>(flags[i])) != CUDA_SUCCESS)
+          return set_error(HM_EINVAL, "stream_signal: flag address %p is not mapped on this device", flags[i]);
+        refused.store(1, std::memory_order_relaxed);  // valid address: fall back to the kernel publish
       } else if (r != CUDA_SUCCESS) {
         return set_error(HM_ECUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
       } else {

@@ -231,17 +231,19 @@ class EPHarMoEnyBlock:
     def _open_peers(self):
         """Exchange CUDA IPC handles of every rank's home-expert weights (once)."""
         L = _lib.load()
-        hs = []
-        for t in (self.w_in, self.w_out):
-            buf = ctypes.create_string_buffer(64)
-            off = ctypes.c_size_t(0)
-            _lib.check(L.hm_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)), "hm_ipc_get_handle")
-            hs.append((bytes(buf.raw), int(off.value)))
+        hs, err = [], None
+        try:  # a failed export must not leave the other ranks waiting in the gather below
+            for t in (self.w_in, self.w_out):
+                hs.append(self._export_handle(L, t))
+        except Exception as e:  # noqa: BLE001 - reported on every rank below
+            hs, err = None, e
         allh = [None] * self.G
         dist.all_gather_object(allh, hs, group=self.group)
         self.peer_in, self.peer_out = [], []
         self._ipc_bases = []
-        err = None
+        if any(h is None for h in allh):
+            bad = [g for g, h in enumerate(allh) if h is None]
+            raise PeerAccessError(f"CUDA IPC export failed on rank(s) {bad}: {err}") from err
         try:
             for g in range(self.G):
                 if g == self.me:
@@ -265,14 +267,28 @@ class EPHarMoEnyBlock:
     # ---------------------------------------------------------------------------------------
     # transport "p2p": one-sided pushes into peer-mapped buffers (NVLink / NVSwitch)
     # ---------------------------------------------------------------------------------------
-    def _ipc_export_open(self, t: torch.Tensor):
-        """Exchange one IPC handle per rank for tensor `t`; returns every rank's device address."""
-        L = _lib.load()
+    @staticmethod
+    def _export_handle(L, t: torch.Tensor):
+        """(IPC handle bytes, offset of t inside the allocation the handle names)."""
         buf = ctypes.create_string_buffer(64)
         off = ctypes.c_size_t(0)
         _lib.check(L.hm_ipc_get_handle(t.data_ptr(), buf, ctypes.byref(off)), "hm_ipc_get_handle")
+        return bytes(buf.raw), int(off.value)
+
+    def _ipc_export_open(self, t: torch.Tensor):
+        """Exchange one IPC handle per rank for tensor `t`; returns every rank's device address.
+        Export or mapping failures on any rank raise PeerAccessError on every rank."""
+        L = _lib.load()
+        try:  # e.g. cudaIpcGetMemHandle refusing expandable-segment allocations
+            mine, err = self._export_handle(L, t), None
+        except Exception as e:  # noqa: BLE001 - reported on every rank below
+            mine, err = None, e
         allh = [None] * self.G
-        dist.all_gather_object(allh, (bytes(buf.raw), int(off.value)), group=self.group)
+        dist.all_gather_object(allh, mine, group=self.group)
+        if any(h is None for h in allh):
+            bad = [g for g, h in enumerate(allh) if h is None]
+            self._close_peers()
+            raise PeerAccessError(f"CUDA IPC export failed on rank(s) {bad}: {err}") from err
         addrs = []
         err = None
         try:

@@ -120,7 +120,7 @@ def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world, cache):
         assert np.array_equal(y1, y0)
 
 
-def _fallback_worker(rank, world, port, out_q):
+def _fallback_worker(rank, world, port, out_q, fail_at="hm_ipc_open"):
     import sys
 
     sys.path.insert(0, REPO)
@@ -136,7 +136,7 @@ def _fallback_worker(rank, world, port, out_q):
             real_check = _lib.check
 
             def failing_check(rc, what):
-                if what == "hm_ipc_open":
+                if what == fail_at:
                     raise RuntimeError("injected: peer mapping refused")
                 return real_check(rc, what)
 
@@ -159,9 +159,11 @@ def _fallback_worker(rank, world, port, out_q):
         dist.destroy_process_group()
 
 
-def test_peer_access_failure_is_collective():
-    """A rank that cannot map peer memory makes EVERY rank raise PeerAccessError at the same
-    point, so all of them can rebuild with the NCCL transport + host fetch (what bench.py does)."""
+@pytest.mark.parametrize("fail_at", ["hm_ipc_open", "hm_ipc_get_handle"])
+def test_peer_access_failure_is_collective(fail_at):
+    """A rank that cannot export or map peer memory makes EVERY rank raise PeerAccessError at the
+    same point, so all of them can rebuild with the NCCL transport + host fetch (what bench.py
+    does) - no rank is left waiting in a collective."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
@@ -170,7 +172,7 @@ def test_peer_access_failure_is_collective():
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_fallback_worker, args=(r, world, port, out_q)) for r in range(world)]
+    procs = [ctx.Process(target=_fallback_worker, args=(r, world, port, out_q, fail_at)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
