@@ -66,6 +66,10 @@ def parse():
                     help="EP (N>1): synchronous expert loading ablation (SimFlags.async_loading_enabled=False)")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="N=1: skip the other BASELINE configs (C1/C3/C4/C5) and the sustained-power loop")
+    ap.add_argument("--sustained-steps", type=int, default=300,
+                    help="N=1: back-to-back steps of the sustained-power measurement (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--eager", action="store_true", help="no CUDA graphs (launch every kernel from Python)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
@@ -448,6 +452,126 @@ def load_ratio_logical(block_cls, cfg_kw, x, G, q, placement, zipf_s, seed, dev)
     return out, m_all
 
 
+def _timed_steps(fn, steps, warmup, flush, stream):
+    """Per-step CUDA-event times (ms) of fn() with the L2 flushed between steps."""
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i, (a, b) in enumerate(ev):
+        flush.fill_(i)
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def extra_workloads(args, dev, peaks3):
+    """The other BASELINE configs, measured in the same run so the driver's BENCH line carries
+    them (configs[0] Switch-128 on 4 simulated GPUs, configs[2] Mixtral 8x7B layer, configs[3]
+    decoder stacks, configs[4] skew sweep).  Device-timed with CUDA events, L2 flushed between
+    steps, burst peaks (short loops); each entry states its config."""
+    import torch
+
+    from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
+    from paper_2506_12417_b200.stack import MoEStack
+
+    hbm, tc, tc_sus = peaks3
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    out = {}
+
+    def one(tag, wl_name, tokens, G, q, layers=1, steps=20, warmup=5, zipf=1.0, placement="round_robin"):
+        d, f, E, k, act, _ = WORKLOADS[wl_name]
+        wl = (d, f, E, k, act, tokens)
+        cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q, logical_ranks=G,
+                        placement=placement)
+        t0 = time.time()
+        blk = (MoEStack.random(cfg, layers, seed=0, device=dev, zipf_s=zipf) if layers > 1 else
+               HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=zipf))
+        x = torch.randn((tokens, d), device=dev, generator=torch.Generator(device=dev).manual_seed(1234)).to(
+            torch.bfloat16)
+        cap = blk.capture(tokens)
+        cap.x.copy_(x)
+        ms = _timed_steps(cap.replay, steps, warmup, flush, stream)
+        st = blk.stats[0] if layers > 1 else blk.stats
+        active = int((st.m_all.cpu().numpy().sum(axis=0) > 0).sum())
+        f1, f2, w_bytes, act_bytes, _ = algorithmic_work(wl, tokens, active)
+        per = float(np.mean(ms))
+        peak = tc_sus if per * steps >= 100.0 else tc  # >= 0.1 s of back-to-back steps: power-capped
+        t_roof = max((f1 + f2) / (peak * 1e12), (w_bytes + act_bytes) / (hbm * 1e9)) * layers
+        rec = {"config": tag, "tokens": tokens, "layers": layers, "logical_ranks": G, "q": q,
+               "placement": placement, "zipf_s": zipf, "steps": steps, "ms_per_step": per,
+               "value": tokens / (per / 1e3), "unit": "tokens/s",
+               "block_roofline_frac": (tokens / (per / 1e3)) / (tokens / t_roof),
+               "bound": "tensor" if (f1 + f2) / (tc * 1e12) >= (w_bytes + act_bytes) / (hbm * 1e9) else "hbm",
+               "peak_tflops": peak,
+               "load_max_over_mean": st.load_imbalance(), "setup_s": round(time.time() - t0, 1)}
+        del cap, blk, x
+        torch.cuda.empty_cache()
+        return rec
+
+    jobs = [
+        ("C1_switch128", lambda: one("BASELINE configs[0]: Switch-128 layer (d 768, d_ff 3072, 128 experts, top-1), "
+                                     "4096 tokens, 4 simulated GPUs, q=4", "switch128", 4096, 4, 4, steps=50)),
+        ("C3_mixtral8_16k", lambda: one("BASELINE configs[2]: Mixtral-8x7B layer (d 4096, d_ff 14336, 8 experts, "
+                                        "top-2), 16384 tokens", "mixtral8", 16384, 1, 32, steps=10, warmup=3)),
+        ("C3_mixtral8_4k", lambda: one("BASELINE configs[2]: Mixtral-8x7B layer, 4096 tokens", "mixtral8", 4096, 1, 32,
+                                       steps=10, warmup=3)),
+        ("C4_switch128_stack12", lambda: one("BASELINE configs[3]: 12-layer Switch-128 decoder stack (residual, "
+                                             "per-layer rebalancing), 4096 tokens, 4 simulated GPUs", "switch128",
+                                             4096, 4, 4, layers=12, steps=10, warmup=3)),
+        ("C4_qwen128_stack48", lambda: one("BASELINE configs[3]: 48-layer Qwen-128 decoder stack (Qwen3-30B-A3B "
+                                           "MoE shape), 16384 tokens", "qwen128", 16384, 1, 32, layers=48, steps=5,
+                                           warmup=2)),
+    ]
+    for key, job in jobs:
+        try:
+            out[key] = job()
+        except Exception as e:  # noqa: BLE001 - report, never drop the headline line
+            out[key] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+            torch.cuda.empty_cache()
+    # C5: skew sweep uniform -> Zipf 1.5, max/mean per-GPU load with rebalancing off / on at
+    # G = 2/4/8 (blocked placement: hot experts homed together), plus the one-GPU block rate
+    try:
+        sweep = []
+        for wl_name, tokens, q in (("qwen128", 16384, 32), ("switch128", 4096, 4)):
+            d, f, E, k, act, _ = WORKLOADS[wl_name]
+            x = torch.randn((tokens, d), device=dev, generator=torch.Generator(device=dev).manual_seed(1234)).to(
+                torch.bfloat16)
+            for zs in (0.0, 0.5, 1.0, 1.5):
+                rec = {"workload": wl_name, "tokens": tokens, "q": q, "zipf_s": zs}
+                for G in (2, 4, 8):
+                    for pol in ("round_robin", "harmony"):
+                        cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q,
+                                        logical_ranks=G, placement="blocked", scheduling_policy=pol)
+                        blk = HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=zs)
+                        blk(x)
+                        rec[f"G{G}_{'rebalanced' if pol == 'harmony' else 'static'}"] = round(
+                            blk.stats.load_imbalance(), 4)
+                        if pol == "harmony":
+                            rec[f"G{G}_moves"] = int(blk.stats.iters.item())
+                        del blk
+                cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q)
+                blk = HarMoEnyBlock.random(cfg, seed=0, device=dev, zipf_s=zs)
+                cap = blk.capture(tokens)
+                cap.x.copy_(x)
+                ms = float(np.mean(_timed_steps(cap.replay, 10, 3, flush, stream)))
+                rec["tokens_per_s_G1"] = tokens / (ms / 1e3)
+                del cap, blk
+                torch.cuda.empty_cache()
+                sweep.append(rec)
+        out["C5_skew_sweep"] = {"config": "BASELINE configs[4]: max/mean per-GPU token load, static placement vs "
+                                          "HarMoEny rebalancing, blocked placement, G logical GPUs on one B200",
+                                "rows": sweep}
+    except Exception as e:  # noqa: BLE001
+        out["C5_skew_sweep"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -505,6 +629,7 @@ def run_ours(args, rank, world, local_rank):
     # LOCAL and EP-p2p forwards never synchronise the host -> CUDA graphs (one per stage
     # group, so gemm1 keeps its own event bracket inside the timed region); EP over NCCL
     # runs eagerly (the all_to_all split sizes are host arguments)
+    cap = pipe = None
     ep_graph = world > 1 and args.transport == "p2p" and args.layers == 1 and not args.eager
     graphed = world == 1 and not args.eager
     if ep_graph:
@@ -585,6 +710,25 @@ def run_ours(args, rank, world, local_rank):
     e2e_value = T_total * e_steps / (e_ms / 1e3)
     nbytes = T_local * d * 2
 
+    # ---- sustained: the same step back to back long enough for the 1 kW power cap to engage
+    # (the default timed loop above is a short burst); reported beside the headline ----
+    sustained = None
+    if world == 1 and not args.no_extras and args.sustained_steps > 0:
+        ns = args.sustained_steps
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler2 = ClockSampler(local_rank, enabled=not args.no_clocks)
+        torch.cuda.synchronize()
+        with sampler2:
+            time.sleep(0.2 if not args.no_clocks else 0)
+            s0.record(stream)
+            for _ in range(ns):
+                step()
+            s1.record(stream)
+            torch.cuda.synchronize()
+        sus_ms = s0.elapsed_time(s1) / ns
+        sustained = {"value": T_total / (sus_ms / 1e3), "ms_per_step": sus_ms, "steps": ns,
+                     "l2": "not flushed (steps back to back)", "clocks": sampler2.summary()}
+
     if rank != 0:
         return
     hbm, tc, tc_sus, peak_kind = peaks()
@@ -595,9 +739,12 @@ def run_ours(args, rank, world, local_rank):
     tensor_bound = f1 / (tc * 1e12) >= g1_bytes / (hbm * 1e9)
     # the GEMM runs inside a loop of back-to-back steps: once that loop lasts long enough for
     # the 1 kW power cap to engage, the sustained cuBLAS figure is the honest denominator
-    long_region = t_step >= 100.0 or "sw_power_cap" in ((sampler.summary() or {}).get("reasons") or [])
+    # the sustained cuBLAS figure is the denominator once the timed loop lasts long enough for the
+    # 1 kW power cap to engage (>= 0.1 s); a short loop is quoted against the burst peak (the
+    # "sustained" object of the line gives the long-loop number)
+    long_region = t_step >= 100.0
     tc_used = tc_sus if (long_region and tc_sus) else tc
-    peak_src = "sustained (timed loop >= 0.1 s / power-capped)" if tc_used != tc else "burst (short timed loop)"
+    peak_src = "sustained (timed loop >= 0.1 s)" if tc_used != tc else "burst (short timed loop)"
     if tensor_bound:
         bound, achieved, peak, unit = "tensor", f1 / (g1_us * 1e-6) / 1e12, tc_used, "TFLOP/s"
         work_desc = f"{f1 / 1e9:.1f} GFLOP = 2 * {T_total // world * k} rows * {d} * {2 * f if act == 'swiglu' else f}"
@@ -663,6 +810,14 @@ def run_ours(args, rank, world, local_rank):
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
     }
+    if sustained is not None:
+        t_roof_sus = max((f1 + f2) / (tc_sus * 1e12), (w_bytes + act_bytes) / (hbm * 1e9)) * args.layers
+        sustained["block_roofline_frac_vs_sustained_peak"] = sustained["value"] / (T_total / t_roof_sus)
+        line["sustained"] = sustained
+    if world == 1 and not args.no_extras and args.layers == 1 and args.workload == "qwen128" and not args.tokens:
+        blk = x = flush = cap = pipe = step = fwd_host = None  # noqa: F841 - free the headline block
+        torch.cuda.empty_cache()
+        line["workloads"] = extra_workloads(args, dev, (hbm, tc, tc_sus))
     print(json.dumps(line), flush=True)
 
 

@@ -18,6 +18,8 @@ serialised into fixtures where cross-version stability matters.
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 
 
@@ -102,6 +104,14 @@ def zipf_topk_frequencies(num_experts: int, s: float, k: int, samples: int = 200
 
 def calibrated_router_bias(num_experts: int, s: float, k: int, noise_std: float = 1.0, iters: int = 200,
                            samples: int = 8192, seed: int = 0) -> np.ndarray:
+    """See _calibrated_router_bias (deterministic, memoised: stacks reuse it per layer)."""
+    return _calibrated_router_bias(int(num_experts), float(s), int(k), float(noise_std), int(iters), int(samples),
+                                   int(seed)).copy()
+
+
+@functools.lru_cache(maxsize=64)
+def _calibrated_router_bias(num_experts: int, s: float, k: int, noise_std: float, iters: int, samples: int,
+                            seed: int) -> np.ndarray:
     """Bias b such that top-k of (N(0, noise_std^2) logits + b) routes with the Zipf
     Gumbel-top-k shares.  The synthetic router's logits x.Wg are Gaussian (x ~ N(0,1),
     Wg ~ N(0, 1/d) -> std 1), whose light tails concentrate top-k far more than the
