@@ -62,6 +62,16 @@ __device__ __forceinline__ void router_top8_of_32(unsigned long long (&key)[32])
   }
 }
 
+// key[0..8) sorted descending (optimal 19-comparator network)
+__device__ __forceinline__ void router_sort8(unsigned long long (&k)[8]) {
+  ce_desc(k[0], k[2]); ce_desc(k[1], k[3]); ce_desc(k[4], k[6]); ce_desc(k[5], k[7]);
+  ce_desc(k[0], k[4]); ce_desc(k[1], k[5]); ce_desc(k[2], k[6]); ce_desc(k[3], k[7]);
+  ce_desc(k[0], k[1]); ce_desc(k[2], k[3]); ce_desc(k[4], k[5]); ce_desc(k[6], k[7]);
+  ce_desc(k[2], k[4]); ce_desc(k[3], k[5]);
+  ce_desc(k[1], k[4]); ce_desc(k[3], k[6]);
+  ce_desc(k[1], k[2]); ce_desc(k[3], k[4]); ce_desc(k[5], k[6]);
+}
+
 constexpr int kRBM = 128;
 constexpr int kRBK = 64;
 constexpr int kRMaxStages = 8;
@@ -433,6 +443,368 @@ __global__ void __maxnreg__(104)
   }
 }
 
+// ==========================================================================================
+// Router v2: split-K over a cluster of C CTAs per 128-token tile.
+//
+// One 128-row tile per cluster; CTA c of the cluster multiplies its K slice (k-blocks
+// [c*KB/C, (c+1)*KB/C)) into its own TMEM, then every CTA ships each row's partial logits to
+// the row's owner (CTA r / (128/C)) through distributed shared memory; owners add the C
+// partials in fixed order (so a token's logits never depend on the batch size) and run
+// softmax + top-k on their 128/C rows, one thread per (row, 32-expert part); the per-tile
+// histogram and the (token, slot)-order ranks combine the CTAs' counts through DSMEM too.
+// At 16k tokens this spreads the tile's loads and its selection work over C SMs instead of
+// one (grid 8x larger, several CTAs resident per SM); at small token counts (one EP rank's
+// 2k tokens = 16 tiles) it is the difference between 16 busy SMs and 128.
+// ==========================================================================================
+constexpr int kR2EpiWarps = 8;
+constexpr int kR2Threads = 64 + kR2EpiWarps * 32;
+
+struct R2Layout {  // shared-memory carve-up, identical on host and device
+  uint32_t region0;  // pipeline stages, later the partial-logit receive buffer
+  uint32_t recv;     // [C][R][E_pad + 4] fp32 (inside region0; row pitch padded against bank conflicts)
+  uint32_t bars;     // mbarriers + TMEM slot (256 B)
+  uint32_t sidx;     // [RR][k] int
+  uint32_t srank;    // [RR][k] int
+  uint32_t scnt;     // [NG][E_pad] int
+  uint32_t sccnt;    // [C][E_pad] int
+  uint32_t total;
+};
+
+__host__ __device__ inline R2Layout r2_layout(int C, int E, int E_pad, int k, int stages) {
+  const int R = 128 / C, RR = R < 32 ? 32 : R, NG = (R + 31) / 32;
+  R2Layout L{};
+  const uint32_t stage_bytes = (uint32_t)(kRA + (uint32_t)E_pad * kRBK * 2);
+  L.recv = 0;
+  const uint32_t need = (uint32_t)C * (E_pad + 4) * R * 4;
+  const uint32_t st = stages * stage_bytes;
+  L.region0 = ((need > st ? need : st) + 1023) / 1024 * 1024;
+  L.bars = L.region0;
+  L.sidx = L.bars + 256;
+  L.srank = L.sidx + RR * k * 4;
+  L.scnt = L.srank + RR * k * 4;
+  L.sccnt = L.scnt + NG * E_pad * 4;
+  L.total = L.sccnt + C * E_pad * 4;
+  (void)E;
+  return L;
+}
+
+template <int C>
+__global__ void __launch_bounds__(kR2Threads)
+    router_split_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                        const float* __restrict__ bias, int tokens_per_rank, int tiles_per_rank, int d, int E,
+                        int E_pad, int k, int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
+                        int32_t* __restrict__ tile_hist, int32_t* __restrict__ lrank, int stages, uint32_t tmem_cols) {
+  constexpr int R = 128 / C;
+  constexpr int RR = R < 32 ? 32 : R;
+  constexpr int NG = (R + 31) / 32;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const R2Layout L = r2_layout(C, E, E_pad, k, stages);
+  const uint32_t stage_b = (uint32_t)E_pad * kRBK * 2;
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + stages * kRA;
+  float* recv = reinterpret_cast<float*>(smem + L.recv);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* empty = full + kRMaxStages;
+  uint64_t* tfull = empty + kRMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  int* s_idx = reinterpret_cast<int*>(smem + L.sidx);
+  int* s_rank = reinterpret_cast<int*>(smem + L.srank);
+  int* s_cnt = reinterpret_cast<int*>(smem + L.scnt);
+  int* s_ccnt = reinterpret_cast<int*>(smem + L.sccnt);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t crank = cluster_ctarank();
+  const int tile = blockIdx.x / C;
+  const int rnk = tile / tiles_per_rank;
+  const int mt = tile - rnk * tiles_per_rank;
+  const int row0 = rnk * tokens_per_rank + mt * kRBM;
+  const int rows = min(kRBM, tokens_per_rank - mt * kRBM);
+  const int KB = d / kRBK;
+  const int kb0 = (int)crank * KB / C, kb1 = ((int)crank + 1) * KB / C;
+
+  if (warp == 0 && lane == 0) {
+    for (int st = 0; st < stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmap_x);
+    tma_prefetch_desc(&tmap_w);
+  }
+  if (warp == 1) tmem_alloc_rt(tmem_slot, tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_x = l2_policy_evict_first();
+      const uint64_t pol_w = l2_policy_evict_last();
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&full[st], kRA + stage_b);
+        tma_load_2d(smem_a + st * kRA, &tmap_x, &full[st], kb * kRBK, row0, pol_x);
+        tma_load_2d(smem_b + st * stage_b, &tmap_w, &full[st], kb * kRBK, 0, pol_w);
+        if (++st == stages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(kRBM, (uint32_t)E_pad);
+      int st = 0;
+      uint32_t ph = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        const uint64_t a0 = make_sdesc_sw128(smem_u32(smem_a + st * kRA));
+        const uint64_t b0 = make_sdesc_sw128(smem_u32(smem_b + st * stage_b));
+#pragma unroll
+        for (int kk = 0; kk < kRBK / 16; ++kk)
+          umma_bf16(tmem_base, a0 + (uint64_t)(kk * 2), b0 + (uint64_t)(kk * 2), idesc, (kb > kb0 || kk != 0));
+        umma_commit(&empty[st]);
+        if (++st == stages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      umma_commit(&tfull[0]);
+    }
+  } else {
+    mbar_wait(&tfull[0], 0);
+    tc_fence_after();
+  }
+  __syncwarp();
+  // #1: every CTA's MMAs are complete, so every CTA's stage buffers may now be overwritten
+  cluster_sync();
+
+  const int ew = warp - 2;              // epilogue warp 0..7 (warps 0/1 join the later phases)
+  const int etid = threadIdx.x - 64;    // 0..255 for epilogue threads
+  if (ew >= 0) {
+    // ship this CTA's partial logits: warp ew drains TMEM lane quarter (warp % 4) (hardware rule),
+    // 32-column chunks ew/4, ew/4 + 2, ...; row r goes to CTA r / R as [src][row][e] (16-byte
+    // remote stores)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t pitch = (uint32_t)E_pad + 4;
+    const uint32_t dst = mapa_shared(recv, (uint32_t)(r / R)) + ((crank * R + (uint32_t)(r % R)) * pitch) * 4;
+    const int nch = (E_pad + 31) / 32;
+    for (int ch = ew >> 2; ch < nch; ch += 2) {
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + ch * 32, a);
+      tmem_ld_wait();
+#pragma unroll
+      for (int jj = 0; jj < 32; jj += 4)
+        if (ch * 32 + jj < E_pad)
+          asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (ch * 32 + jj) * 4),
+                       "r"(a[jj]), "r"(a[jj + 1]), "r"(a[jj + 2]), "r"(a[jj + 3])
+                       : "memory");
+    }
+  }
+  // #2: all partials delivered to their owners
+  cluster_sync();
+
+  if (ew >= 0) {
+    // owner epilogue, lane-parallel: a row's experts are spread over LPR lanes (8 logits each);
+    // every lane sorts its 8 packed (value, ~expert) keys, LPR-lane butterfly merges leave the
+    // row's top-8 on every lane (ties: lowest expert id), then max / sum-exp by butterflies
+    // (exact-commutative pairwise adds: every lane holds the bit-identical sum)
+    const int lpr = E <= 128 ? 16 : 32;
+    const int rpw = 32 / lpr;  // rows per warp and pass
+    for (int rb = ew * rpw; rb < RR; rb += kR2EpiWarps * rpw) {
+      const int rl = rb + lane / lpr;
+      const int part = lane % lpr;
+      const bool have = rl < R;
+      const bool valid = have && (int)crank * R + rl < rows;
+      float v[8];
+      unsigned long long key[8];
+      float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (have && part * 8 < E_pad) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {  // fixed order over the K slices
+          const float4* src = reinterpret_cast<const float4*>(recv + ((uint32_t)c * R + rl) * (E_pad + 4) + part * 8);
+          const float4 lo = src[0], hi = src[1];
+          sum8[0] = __fadd_rn(sum8[0], lo.x); sum8[1] = __fadd_rn(sum8[1], lo.y);
+          sum8[2] = __fadd_rn(sum8[2], lo.z); sum8[3] = __fadd_rn(sum8[3], lo.w);
+          sum8[4] = __fadd_rn(sum8[4], hi.x); sum8[5] = __fadd_rn(sum8[5], hi.y);
+          sum8[6] = __fadd_rn(sum8[6], hi.z); sum8[7] = __fadd_rn(sum8[7], hi.w);
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int e = part * 8 + jj;
+        float x = -INFINITY;
+        if (have && e < E) {
+          x = sum8[jj];
+          if (bias != nullptr) x = __fadd_rn(x, __ldg(bias + e));
+        }
+        v[jj] = x;
+        unsigned long long kv = (static_cast<unsigned long long>(0x007FFFFFu) << 32) | 0x80000000u;  // -inf
+        if (have && e < E) {
+          uint32_t u = __float_as_uint(__fadd_rn(x, 0.0f));  // -0 == +0 like the float compare
+          u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+          kv = (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(e));
+        }
+        key[jj] = kv;
+      }
+      router_sort8(key);
+      for (int sh = 1; sh < lpr; sh <<= 1) {
+        unsigned long long o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = __shfl_xor_sync(0xffffffffu, key[i], sh);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) key[i] = key[i] > o[7 - i] ? key[i] : o[7 - i];
+#pragma unroll
+        for (int s2 = 4; s2 > 0; s2 >>= 1)
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if ((i & s2) == 0) ce_desc(key[i], key[i + s2]);
+      }
+      const uint32_t u0 = static_cast<uint32_t>(key[0] >> 32);
+      const float mx = __uint_as_float((u0 & 0x80000000u) ? (u0 & 0x7FFFFFFFu) : ~u0);
+      float ls = 0.0f;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (part * 8 + jj < E) ls = __fadd_rn(ls, expf(__fsub_rn(v[jj], mx)));
+      for (int sh = 1; sh < lpr; sh <<= 1) ls = __fadd_rn(ls, __shfl_xor_sync(0xffffffffu, ls, sh));
+      if (part == 0 && rl < RR) {
+        if (!valid) {
+          for (int j = 0; j < k; ++j) s_idx[rl * k + j] = -1;
+        } else {
+          const int64_t t = (int64_t)row0 + crank * R + rl;
+          float pr[8];
+          float psum = 0.0f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < k) {
+              const uint32_t u = static_cast<uint32_t>(key[j] >> 32);
+              const float tv = __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+              pr[j] = __fdiv_rn(expf(__fsub_rn(tv, mx)), ls);
+              psum = __fadd_rn(psum, pr[j]);
+            }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < k) {
+              const int id = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(key[j]));
+              topk_idx[t * k + j] = id;
+              topk_w[t * k + j] = renorm ? __fdiv_rn(pr[j], psum) : pr[j];
+              s_idx[rl * k + j] = id;
+            }
+        }
+      }
+    }
+    for (int i = etid; i < NG * E_pad; i += kR2EpiWarps * 32) s_cnt[i] = 0;
+    named_bar_sync(2, kR2EpiWarps * 32);
+
+    // rank pass: epilogue warp g walks row group g's assignments in (token, slot) order
+    if (ew < NG) {
+      const int g = ew;
+      for (int c = 0; c < k; ++c) {
+        const int a = g * 32 * k + c * 32 + lane;
+        const int e = s_idx[a];
+        const uint32_t mask = __match_any_sync(0xffffffffu, e);
+        const int cnt0 = (e >= 0) ? s_cnt[g * E_pad + e] : 0;
+        __syncwarp();
+        const int leader = 31 - __clz(mask);
+        if (e >= 0 && lane == leader) s_cnt[g * E_pad + e] = cnt0 + __popc(mask);
+        s_rank[a] = cnt0 + __popc(mask & lanemask_lt());
+        __syncwarp();
+      }
+    }
+    named_bar_sync(2, kR2EpiWarps * 32);
+    // this CTA's per-expert totals to every CTA of the cluster
+    for (int e = etid; e < E_pad; e += kR2EpiWarps * 32) {
+      int tot = 0;
+      for (int g = 0; g < NG; ++g) tot += s_cnt[g * E_pad + e];
+      for (int c = 0; c < C; ++c) st_cluster_s32(mapa_shared(s_ccnt + crank * E_pad + e, (uint32_t)c), tot);
+    }
+  }
+  __syncwarp();
+  // #3: all CTAs' totals in place
+  cluster_sync();
+  if (ew >= 0) {
+    for (int rl = etid; rl < R; rl += kR2EpiWarps * 32) {
+      if ((int)crank * R + rl >= rows) continue;
+      const int64_t t = (int64_t)row0 + crank * R + rl;
+      const int g = rl / 32;
+      for (int j = 0; j < k; ++j) {
+        const int e = s_idx[rl * k + j];
+        int off = 0;
+        for (int gg = 0; gg < g; ++gg) off += s_cnt[gg * E_pad + e];
+        for (int c = 0; c < (int)crank; ++c) off += s_ccnt[c * E_pad + e];
+        lrank[t * k + j] = s_rank[rl * k + j] + off;
+      }
+    }
+    for (int e = (int)crank + C * etid; e < E; e += C * kR2EpiWarps * 32) {
+      int tot = 0;
+      for (int c = 0; c < C; ++c) tot += s_ccnt[c * E_pad + e];
+      tile_hist[(int64_t)tile * E + e] = tot;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_rt(tmem_base, tmem_cols);
+  }
+}
+
+// HM_ROUTER_V2=1: the split-K cluster kernel above (opt-in experiment, profiles/r2_router_split.txt:
+// correct and bit-exact on the router tests, but slower than the one-CTA-per-tile kernel at
+// 16k tokens - 49-113 us vs 37-43 us cold for C = 2..8 - because launching thousands of
+// cluster CTAs and three cluster barriers per tile cost more than the split saves; it wins
+// only at small token counts (2k tokens: 27-31 us vs 39 us) and a token's logits must not
+// depend on the batch size, so the variant cannot be chosen per call)
+static bool use_router_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HM_ROUTER_V2");
+    v = (e != nullptr && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int C>
+static int launch_router_split(const CUtensorMap& tx, const CUtensorMap& tw, const float* bias, int tokens_per_rank,
+                               int tiles_per_rank, int n_tiles, int d, int E, int E_pad, int k, int renormalize,
+                               int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,
+                               cudaStream_t stream) {
+  const int KB = d / kRBK;
+  const int kbc = (KB + C - 1) / C;
+  int stages = kbc < 2 ? kbc : 2;
+  if (const char* e = getenv("HM_ROUTER_STAGES")) stages = std::max(1, std::min(kRMaxStages, std::min(kbc, atoi(e))));
+  const R2Layout L = r2_layout(C, E, E_pad, k, stages);
+  const size_t smem = 1024 + L.total;
+  uint32_t cols = 32;
+  while ((int)cols < E_pad) cols <<= 1;
+  cudaFuncSetAttribute(router_split_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_tiles * C));
+  cfg.blockDim = dim3(kR2Threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, router_split_kernel<C>, tx, tw, bias, tokens_per_rank,
+                                           tiles_per_rank, d, E, E_pad, k, renormalize, topk_idx, topk_w, tile_hist,
+                                           lrank, stages, cols);
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "router (split) launch: %s", cudaGetErrorString(e));
+  return check_launch("router_topk");
+}
+
 int launch_router(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
                   int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,
                   cudaStream_t stream) {
@@ -450,6 +822,23 @@ int launch_router(const void* x, const void* wg, const float* bias, int n_ranks,
   rc = make_tmap_2d_bf16(&tw, wg, (uint64_t)E_pad, (uint64_t)d, (uint32_t)E_pad, kRBK);
   if (rc) return rc;
   const int grid = n_ranks * tiles_per_rank;
+  if (!use_router_v1() && k <= 8) {
+    // cluster size by the model width only (never by the batch size: a token's logits must not
+    // depend on how many other tokens are routed with it): up to 8 k-slices of >= 1 k-block
+    const int KB = d / kRBK;
+    int C = KB >= 8 ? 8 : (KB >= 4 ? 4 : (KB >= 2 ? 2 : 1));
+    if (const char* ce = getenv("HM_ROUTER_C")) C = std::max(1, std::min(C, atoi(ce)));
+#define HM_R2(CC)                                                                                               \
+  return launch_router_split<CC>(tx, tw, bias, tokens_per_rank, tiles_per_rank, grid, d, E, E_pad, k, renormalize, \
+                                 topk_idx, topk_w, tile_hist, lrank, stream)
+    switch (C) {
+      case 1: HM_R2(1);
+      case 2: HM_R2(2);
+      case 4: HM_R2(4);
+      default: HM_R2(8);
+    }
+#undef HM_R2
+  }
   const int stages = router_stages(E_pad);
   const size_t smem = 1024 + (size_t)stages * (kRA + (size_t)E_pad * kRBK * 2) + 256 + kREpiSmem;
 #define HM_LAUNCH_ROUTER(KM)                                                                                 \
