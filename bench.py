@@ -534,6 +534,29 @@ def extra_workloads(args, dev, peaks3):
         except Exception as e:  # noqa: BLE001 - report, never drop the headline line
             out[key] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
             torch.cuda.empty_cache()
+    # C2 at G = 8: one EP rank's critical path measured kernel by kernel on this GPU (router on its
+    # 2,048 tokens, EP planner, dispatch push, FFN1/FFN2 over its receive buffer, combine), NVLink
+    # transfers and cross-rank handshakes modelled (tools/ep_projection.py)
+    try:
+        sys.path.insert(0, os.path.join(REPO, "tools"))
+        from ep_projection import project
+
+        for pl in ("round_robin", "blocked"):
+            pr = project(G=8, q=32, placement=pl, zipf_s=1.0, peak_tflops=tc)
+            crit = pr["per_rank"][pr["critical_rank"]]
+            out[f"C2_ep8_projection_{pl}"] = {
+                "config": f"BASELINE configs[1] at G=8 (expert-parallel, {pl} placement, q=32): the critical "
+                          f"rank's kernels measured at per-rank size on one B200, NVLink at 900 GB/s and "
+                          f"{pr['config']['handshake_us']} us per cross-rank handshake modelled",
+                "projected_step_us": pr["projected_step_us"], "projected_tokens_per_s": pr["projected_tokens_per_s"],
+                "gemm_roofline_us": pr["gemm_roofline_us"], "projected_roofline_frac": pr["projected_roofline_frac"],
+                "router_us": pr["router_us"], "moves": pr["moves"], "load_max_over_mean": pr["load_max_over_mean"],
+                "critical_rank": pr["critical_rank"],
+                "critical_rank_us": {k_: round(v_, 2) for k_, v_ in crit.items() if k_.endswith("_us")},
+                "critical_rank_recv_rows": crit["recv_rows"], "critical_rank_fetches": crit["fetched_experts"]}
+            torch.cuda.empty_cache()
+    except Exception as e:  # noqa: BLE001
+        out["C2_ep8_projection"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     # C5: skew sweep uniform -> Zipf 1.5, max/mean per-GPU load with rebalancing off / on at
     # G = 2/4/8 (blocked placement: hot experts homed together), plus the one-GPU block rate
     try:

@@ -1,0 +1,210 @@
+"""One EP rank's share of a G-GPU expert-parallel step, measured on ONE B200.
+
+Every kernel of rank `me`'s critical path runs for real at the per-rank size and is timed
+alone (CUDA-graph replay, L2 flushed before each call, CUDA events):
+
+  router      hm_router_topk on the rank's T/G tokens
+  plan        hm_plan (EP layout of rank `me`) on the m_all the metadata exchange delivers
+  dispatch    hm_dispatch_push of the rank's tokens (the G destination buffers are local here)
+  ffn1/ffn2   the grouped GEMMs over rank `me`'s receive buffer: one segment per (expert, source)
+              with the EP weight slots (home experts, then the fetched experts in plan order)
+  combine     hm_combine of the rank's T/G tokens
+
+What one GPU cannot measure is modelled explicitly and reported separately: NVLink transfer
+times at `nvlink_gbs` (dispatch rows out / in, FFN2 rows back, fetched expert weights) and a
+fixed cost per cross-rank flag handshake (metadata, tokens, outputs).  The fetch channel is
+modelled as the reference does (engine.py:204-275): one transfer at a time in plan order, a
+fetched expert's FFN1 tiles start when its gate/up block has landed, resident experts first.
+
+    python tools/ep_projection.py [--G 8] [--placement round_robin|blocked] [--q 32]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2506_12417_b200 import ops  # noqa: E402
+from paper_2506_12417_b200.block import MoEConfig, pack_w13, placement_home, random_weights  # noqa: E402
+
+
+def _graph_time_us(fn, flush, reps=10):
+    """Median device time of fn() replayed from a CUDA graph with the L2 flushed before each call."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    ts = []
+    for i in range(reps):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    return float(np.median(ts))
+
+
+def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placement="round_robin", zipf_s=1.0,
+            nvlink_gbs=900.0, handshake_us=4.0, peak_tflops=None, ranks=None, seed=0):
+    dev = torch.device("cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q, placement=placement,
+                    logical_ranks=G)
+    wg, w1, w2, w3, bias = random_weights(cfg, seed, dev, zipf_s)
+    wgp = torch.zeros((ops.e_pad(E), d), dtype=torch.bfloat16, device=dev)
+    wgp[:E] = wg
+    if act == "swiglu":
+        w_in_all = pack_w13(w1, w3).view(E, 2 * f, d)
+        n_in, epi = 2 * f, ops.HM_EPI_SWIGLU
+    else:
+        w_in_all = w1.reshape(E, f, d)
+        n_in, epi = f, ops.HM_EPI_RELU
+    w_out_all = w2.reshape(E, d, f)
+    Tg = T // G
+    x = torch.randn((T, d), device=dev, generator=torch.Generator(device=dev).manual_seed(1234)).to(torch.bfloat16)
+    # routing of every rank's tokens -> m_all (what the metadata exchange hands every rank)
+    idx, w, tile_hist, lrank = ops.router_topk(x, wgp, bias, G, Tg, k, k > 1, E=E)
+    tiles = (Tg + 127) // 128
+    m_all, tile_off = ops.hist_scan(tile_hist, G, tiles)
+    home = torch.from_numpy(placement_home(cfg)).to(dev)
+    home_np = placement_home(cfg)
+    bytes_tok = d * 2
+    out = {"config": dict(d_model=d, d_ff=f, experts=E, top_k=k, tokens=T, G=G, q=q, placement=placement,
+                          zipf_s=zipf_s, nvlink_gbs=nvlink_gbs, handshake_us=handshake_us)}
+    # rank-independent kernels
+    xr = x[:Tg].contiguous()
+    out["router_us"] = _graph_time_us(lambda: ops.router_topk(xr, wgp, bias, 1, Tg, k, k > 1, E=E), flush)
+    plan0 = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, ops.HM_LAYOUT_EP, 0, m_all=m_all)
+    torch.cuda.synchronize()
+    S = plan0.S.cpu().numpy().astype(np.int64)
+    loads = S.sum(axis=(0, 1))
+    out["moves"] = int(plan0.iters.item())
+    out["load_max_over_mean"] = float(loads.max() / loads.mean())
+    ranks = list(range(G)) if ranks is None else ranks
+    per_rank = {}
+    f1_flops_per_row = 2.0 * d * n_in
+    f2_flops_per_row = 2.0 * f * d
+    expert_bytes = (n_in * d + d * f) * 2
+    for me in ranks:
+        r = {}
+        r["plan_us"] = _graph_time_us(lambda: ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, ops.HM_LAYOUT_EP, me,
+                                                       m_all=m_all), flush)
+        p = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, ops.HM_LAYOUT_EP, me, m_all=m_all)
+        lay = p.layout
+        n_seg = int(lay.n_seg.item())
+        n_fetch = int(lay.n_fetch.item())
+        segs = lay.segs[:n_seg].cpu().numpy()
+        fetched = lay.fetch[:n_fetch].cpu().numpy().tolist()
+        rows = int(segs[:, 1].sum()) if n_seg else 0
+        r.update(recv_rows=rows, fetched_experts=n_fetch, segments=n_seg)
+        # dispatch push of my tokens into G local stand-ins for the destination buffers
+        dst_delta, recv_split = ops.ep_offsets(p.S, me)
+        cap = int(loads.max()) + 1
+        bufs = [torch.empty((cap, d), dtype=torch.bfloat16, device=dev) for _ in range(G)]
+        toks = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(G)]
+        i64 = dict(dtype=torch.int64, device=dev)
+        dst_rows = torch.tensor([b.data_ptr() for b in bufs], **i64)
+        dst_tok = torch.tensor([t.data_ptr() for t in toks], **i64)
+        sl = slice(me * Tg, (me + 1) * Tg)
+        idx_me, lrank_me = idx[sl].contiguous(), lrank[sl].contiguous()
+        toff_me = tile_off[me * tiles:(me + 1) * tiles].contiguous()
+        x_me = x[sl].contiguous()
+        r["dispatch_local_us"] = _graph_time_us(
+            lambda: ops.dispatch_push(x_me, idx_me, lrank_me, toff_me, p.S, lay.slot_base, dst_delta, me, dst_rows,
+                                      dst_tok), flush)
+        flows = S.sum(axis=1)
+        sent = int(flows[me].sum() - flows[me, me])
+        recv = int(flows[:, me].sum() - flows[me, me])
+        r["dispatch_nvlink_us"] = max(sent, recv) * bytes_tok / (nvlink_gbs * 1e3)
+        # my receive buffer and weight slots (home experts ascending, then fetched in plan order)
+        n_home = int((home_np == me).sum())
+        slot_experts = [e for e in range(E) if home_np[e] == me] + fetched
+        sidx = torch.tensor(slot_experts, dtype=torch.long, device=dev)
+        w_in = w_in_all[sidx].reshape(-1, d).contiguous()
+        w_out = w_out_all[sidx].reshape(-1, f).contiguous()
+        a = torch.randn((max(rows, 1), d), device=dev).to(torch.bfloat16)
+        h = torch.empty((max(rows, 1), n_in // (2 if act == "swiglu" else 1)), dtype=torch.bfloat16, device=dev)
+        y = torch.empty((max(rows, 1), d), dtype=torch.bfloat16, device=dev)
+        r["ffn1_us"] = _graph_time_us(lambda: ops.grouped_gemm(a, w_in, n_in, lay, epi, out=h), flush)
+        r["ffn2_us"] = _graph_time_us(lambda: ops.grouped_gemm(h, w_out, d, lay, ops.HM_EPI_STORE, out=y), flush)
+        # resident experts' share of FFN1 (their segments come first in plan order)
+        n_res_seg = int(sum(1 for s_ in segs if s_[2] < n_home))
+        rows_res = int(segs[:n_res_seg, 1].sum()) if n_res_seg else 0
+        if n_fetch and n_res_seg:
+            lay_res = ops.Layout(lay.slot_base, lay.segs, torch.tensor([n_res_seg], dtype=torch.int32, device=dev),
+                                 lay.mtile_prefix, lay.fetch, lay.n_fetch)
+            r["ffn1_resident_us"] = _graph_time_us(lambda: ops.grouped_gemm(a, w_in, n_in, lay_res, epi, out=h),
+                                                   flush)
+        else:
+            r["ffn1_resident_us"] = r["ffn1_us"] if not n_fetch else 0.0
+        # fetch channel (reference semantics): one expert at a time in plan order, gate/up block
+        # first; a fetched expert's FFN1 share starts when its gate/up block has landed
+        t_one = expert_bytes / (nvlink_gbs * 1e3)
+        t_in = t_one * (n_in * d) / (n_in * d + d * f)
+        t = r["ffn1_resident_us"]
+        fetched_rows = rows - rows_res
+        for j, e in enumerate(fetched):
+            rows_e = int(sum(s_[1] for s_ in segs if s_[3] == e))
+            share = (r["ffn1_us"] - r["ffn1_resident_us"]) * rows_e / max(fetched_rows, 1)
+            t = max(t, j * t_one + t_in) + share
+        r["fetch_nvlink_us"] = n_fetch * t_one
+        r["ffn1_with_fetch_us"] = max(t, r["ffn1_us"])
+        # FFN2 needs every down block; its rows for other ranks go back over NVLink in the epilogue
+        back = rows - int(S[me, :, me].sum())
+        r["return_nvlink_us"] = back * bytes_tok / (nvlink_gbs * 1e3)
+        # the channel ends at n_fetch * t_one after FFN1 started; FFN2 reaches its fetched experts
+        # (last in plan order) after its resident share
+        tail = r["ffn2_us"] * fetched_rows / max(rows, 1)
+        r["ffn2_with_fetch_us"] = max(r["ffn2_us"], r["return_nvlink_us"],
+                                      n_fetch * t_one - r["ffn1_with_fetch_us"] + tail)
+        yk = torch.randn((Tg * k, d), device=dev).to(torch.bfloat16)
+        w_me = w[sl].contiguous()
+        r["combine_us"] = _graph_time_us(lambda: ops.combine(yk, None, w_me), flush)
+        r["handshakes_us"] = 3 * handshake_us
+        r["step_us"] = (out["router_us"] + r["handshakes_us"] + r["plan_us"] +
+                        max(r["dispatch_local_us"], r["dispatch_nvlink_us"]) + r["ffn1_with_fetch_us"] +
+                        r["ffn2_with_fetch_us"] + r["combine_us"])
+        r["gemm_flops"] = rows * (f1_flops_per_row + f2_flops_per_row)
+        per_rank[me] = r
+        del bufs, toks, a, h, y, w_in, w_out
+        torch.cuda.empty_cache()
+    out["per_rank"] = per_rank
+    crit = max(per_rank, key=lambda m: per_rank[m]["step_us"])
+    out["critical_rank"] = crit
+    step = per_rank[crit]["step_us"]
+    out["projected_step_us"] = step
+    out["projected_tokens_per_s"] = T / (step * 1e-6)
+    if peak_tflops:
+        balanced = T * k * (f1_flops_per_row + f2_flops_per_row) / G
+        out["gemm_roofline_us"] = balanced / (peak_tflops * 1e12) * 1e6
+        out["projected_roofline_frac"] = out["gemm_roofline_us"] / step
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--G", type=int, default=8)
+    ap.add_argument("--placement", default="round_robin")
+    ap.add_argument("--q", type=int, default=32)
+    ap.add_argument("--zipf", type=float, default=1.0)
+    ap.add_argument("--peak", type=float, default=1631.3)
+    a = ap.parse_args()
+    res = project(G=a.G, q=a.q, placement=a.placement, zipf_s=a.zipf, peak_tflops=a.peak)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
