@@ -70,6 +70,9 @@ extern "C" {
 #define HM_LAYOUT_LOCAL 0 /* all G ranks on this device: buffer [dest][expert][source][rank] */
 #define HM_LAYOUT_EP 1    /* this process is rank `me`: send buffer [dest][expert][rank], */
                           /* receive buffer [source][expert][rank] (NCCL all_to_all chunks) */
+#define HM_LAYOUT_EP_EXPERT 2 /* rank `me`, one-sided p2p dispatch: every rank's receive buffer is */
+                              /* [expert][source][rank], slot_base[g,e,d] = that bucket's row in  */
+                              /* rank d's buffer; one GEMM segment per expert (all sources)       */
 
 /* diagnostics: %globaltimer stamps (ns) of the last hm_plan launch: start, after the histogram
  * reduce, after the schedule, after the layout (host buffer of 4 int64; synchronises the device) */
@@ -270,6 +273,9 @@ HM_API int hm_ep_offsets(const int32_t* S, int G, int E, int me, int32_t* dst_de
  * stored into dst_rows[d] (receive buffer of destination rank d, a peer pointer) at its
  * receive row, and t*k + j into dst_tok[d] at the same row.  dst_rows / dst_tok: device arrays
  * of G pointers.  pos [T*k] (or NULL) gets the send-layout row, as hm_permute would.
+ * dst_delta == NULL: slot_base is an HM_LAYOUT_EP_EXPERT layout (rows of every destination's
+ * expert-major buffer, no send layout), and the token index stored is (me << 24) | (t*k + j) so
+ * the receiver's FFN2 can route each row home (hm_grouped_gemm_remote with out_split == NULL).
  */
 HM_API int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
                             const int32_t* S, const int32_t* slot_base, const int32_t* dst_delta, int tokens, int me,
@@ -280,7 +286,8 @@ HM_API int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_
  * hm_grouped_gemm whose output rows go to other ranks (FFN2 + the return all_to_all): the rows
  * of a segment starting at receive row r0 belong to source g with out_split[g] <= r0 <
  * out_split[g+1], and land in out_ptrs[g] (device array of n_out peer pointers) at row
- * row_map[r].  2-CTA kernel only.
+ * row_map[r].  out_split == NULL (expert-major receive buffer): row r lands in
+ * out_ptrs[row_map[r] >> 24] at row row_map[r] & 0xFFFFFF.  2-CTA kernel only.
  */
 HM_API int hm_grouped_gemm_remote(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                                   const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix,

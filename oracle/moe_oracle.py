@@ -247,6 +247,30 @@ def ep_recv_segments(S, home, me: int):
     return segs
 
 
+def ep_expert_layout(S, home, me: int, cache_slots: int = 0):
+    """HM_LAYOUT_EP_EXPERT (one-sided p2p dispatch): every rank d's receive buffer is
+    [expert (ascending)][source][rank].  Returns slot_base [G,E,G] (row of bucket (g,e,d) in d's
+    buffer) and rank me's segments (row_start, nrows, wslot, expert), one per expert in plan
+    order (residents first, then fetched experts; engine.py:233-234)."""
+    S = np.asarray(S, dtype=np.int64)
+    G, E, _ = S.shape
+    home = np.asarray(home)
+    n = S.sum(axis=0).T  # [d, e]
+    off = _excl_cumsum(n, axis=1)  # [d, e]
+    slot_base = off.T[None, :, :] + _excl_cumsum(S, axis=0)  # [g, e, d]
+    resident = (home == me).astype(np.int32)
+    order = plan_order(n[me], resident)
+    n_home = int(resident.sum())
+    hslot = np.cumsum(resident) - resident
+    n_res_work = int(sum(1 for e in order if resident[e]))
+    segs = []
+    for o, e in enumerate(order):
+        fi = o - n_res_work
+        wslot = int(hslot[e]) if resident[e] else n_home + (fi % cache_slots if cache_slots > 0 else fi)
+        segs.append((int(off[me, e]), int(n[me, e]), wslot, int(e)))
+    return slot_base, segs
+
+
 # --------------------------------------------------------------------------------------------
 # bf16 helpers (numpy has no bf16): values carried as uint16 bit patterns
 # --------------------------------------------------------------------------------------------

@@ -13,7 +13,7 @@ import os
 
 HM_OK, HM_EINVAL, HM_ECUDA, HM_ENCCL, HM_ENOSPC = 0, 1, 2, 3, 4
 HM_EPI_STORE, HM_EPI_RELU, HM_EPI_SWIGLU = 0, 1, 2
-HM_LAYOUT_LOCAL, HM_LAYOUT_EP = 0, 1
+HM_LAYOUT_LOCAL, HM_LAYOUT_EP, HM_LAYOUT_EP_EXPERT = 0, 1, 2
 HM_POLICY_NONE, HM_POLICY_REBALANCE, HM_POLICY_EVEN_SPLIT = 0, 1, 2
 
 # HM_LIB_PATH: load a variant build of the same C ABI (kernel A/B experiments, tools/build_variant.sh)

@@ -778,18 +778,27 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       const int upoff = hf ? kBN / 4 : kBN / 2;  // SwiGLU: TMEM column distance gate -> up
       const bool valid = r_in_tile < rows;
       int64_t row = (int64_t)seg.x + m * 2 * kBM + rank * cta_rows + r_in_tile;
-      if (row_map != nullptr && valid) row = __ldg(row_map + row);
-      const int64_t obase = row * ldo + (int64_t)nb * kOutCols + ocol0;
-      const int nvalid = max(0, min(32, rows - (r_in_tile - lane)));
-      // remote output (EP over peer memory): the segment's rows belong to source rank g, the
-      // one whose receive range [out_split[g], out_split[g+1]) holds the segment; its rows are
-      // stored straight into that rank's token-major output over NVLink
+      // remote output (EP over peer memory): rows go straight into their source rank's token-major
+      // output over NVLink - per segment (source-major receive buffer: the source g whose range
+      // [out_split[g], out_split[g+1]) holds the segment) or per row (expert-major receive buffer,
+      // out_split == NULL: row_map carries (source << 24) | token-major row)
       __nv_bfloat16* obuf = out;
-      if (out_ptrs != nullptr) {
+      if (out_ptrs != nullptr && out_split != nullptr) {
         int g = 0;
         while (g + 1 < n_out && __ldg(out_split + g + 1) <= seg.x) ++g;
         obuf = reinterpret_cast<__nv_bfloat16*>(__ldg(out_ptrs + g));
       }
+      if (row_map != nullptr && valid) {
+        row = __ldg(row_map + row);
+        if (out_ptrs != nullptr && out_split == nullptr) {
+          obuf = reinterpret_cast<__nv_bfloat16*>(__ldg(out_ptrs + ((uint32_t)row >> 24)));
+          row &= 0xFFFFFF;
+        }
+      }
+      // per-row output address (rows of one warp may belong to different ranks' buffers)
+      const unsigned long long obase = reinterpret_cast<unsigned long long>(
+          obuf + (row * ldo + (int64_t)nb * kOutCols + ocol0));
+      const int nvalid = max(0, min(32, rows - (r_in_tile - lane)));
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
       tc_fence_after();
@@ -820,10 +829,10 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + (lane >> 2);
           const int piece = lane & 3;
-          const int64_t ob = __shfl_sync(0xffffffffu, obase, rr);
+          const unsigned long long ob = __shfl_sync(0xffffffffu, obase, rr);
           if (rr < nvalid) {
             const uint4 v = ld_shared_v4(stg + rr * kStgPitch + piece * 16);
-            st_global_v4(obuf + ob + c0 + piece * 8, v.x, v.y, v.z, v.w);
+            st_global_v4(reinterpret_cast<__nv_bfloat16*>(ob) + c0 + piece * 8, v.x, v.y, v.z, v.w);
           }
         }
         __syncwarp();
@@ -935,8 +944,8 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
   if (a_gather != nullptr && a_gather_div < 1) return set_error(HM_EINVAL, "grouped_gemm: a_gather_div must be >= 1");
-  if (out_ptrs != nullptr && (out_split == nullptr || n_out < 1))
-    return set_error(HM_EINVAL, "grouped_gemm: remote output needs out_split and n_out >= 1");
+  if (out_ptrs != nullptr && (n_out < 1 || n_out > 256 || (out_split == nullptr && row_map == nullptr)))
+    return set_error(HM_EINVAL, "grouped_gemm: remote output needs n_out in [1, 256] and out_split or a tagged row_map");
   if (out_ptrs != nullptr && !use_2cta())
     return set_error(HM_EINVAL, "grouped_gemm: remote output needs the 2-CTA kernel (unset HM_GEMM_1CTA)");
   if (slot_done != nullptr && !use_2cta())

@@ -102,11 +102,16 @@ __global__ void __launch_bounds__(kPushWarps * 32)
       if (c + s > r) break;
       c += s;
     }
-    const int p = __ldg(slot_base + ((int64_t)me * E + e) * G + d) + (r - c);  // send layout
-    qj = p + __ldg(dst_delta + d);                                              // d's receive row
+    const int p = __ldg(slot_base + ((int64_t)me * E + e) * G + d) + (r - c);
+    if (dst_delta != nullptr) {  // HM_LAYOUT_EP: p is the send-layout row, shifted into d's buffer
+      qj = p + __ldg(dst_delta + d);
+      reinterpret_cast<int32_t*>(__ldg(dst_tok + d))[qj] = (int32_t)(t * k + j);
+    } else {  // HM_LAYOUT_EP_EXPERT: p is already the row in d's buffer; tag the row with its source
+      qj = p;
+      reinterpret_cast<int32_t*>(__ldg(dst_tok + d))[qj] = (int32_t)(((uint32_t)me << 24) | (uint32_t)(t * k + j));
+    }
     dj = d;
     if (pos != nullptr) pos[t * k + j] = p;
-    reinterpret_cast<int32_t*>(__ldg(dst_tok + d))[qj] = (int32_t)(t * k + j);
   }
   for (int j = 0; j < k; ++j) {
     const int64_t q = __shfl_sync(0xffffffffu, qj, j);
@@ -190,6 +195,8 @@ int launch_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* 
   if (d % 8 != 0) return set_error(HM_EINVAL, "dispatch_push: d must be a multiple of 8");
   if (G < 1 || G > 32 || me < 0 || me >= G || k < 1 || k > 32)
     return set_error(HM_EINVAL, "dispatch_push: bad G/me/k");
+  if (dst_delta == nullptr && (int64_t)tokens * k > (1 << 24))
+    return set_error(HM_EINVAL, "dispatch_push: tagged rows need tokens * k <= 2^24");
   if (tokens <= 0) return HM_OK;
   const int n16 = d / 8;
   const int blocks = (tokens + kPushWarps - 1) / kPushWarps;

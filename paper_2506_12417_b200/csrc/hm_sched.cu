@@ -497,6 +497,75 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
     return;
   }
 
+  if (mode == HM_LAYOUT_EP_EXPERT) {
+    // ---- EP, expert-major receive buffers (one-sided p2p dispatch): rank d's buffer holds rows
+    // [expert (ascending id)][source][rank]; every sender derives its rows from the replicated S:
+    // slot_base[g,e,d] = sum_{e'<e} n_d(e') + sum_{g'<g} S[g',e,d] (the LOCAL layout with each
+    // destination starting at row 0).  Rank me's GEMM work list: ONE segment per expert (all its
+    // sources' rows contiguous) in plan order, wslot / fetch list as in HM_LAYOUT_EP.
+    for (int i = tid; i < GE; i += nt) {
+      const int d = i / E, e = i - (i / E) * E;
+      int sum = 0;
+      for (int g = 0; g < G; ++g) sum += S[(g * E + e) * G + d];
+      s_n[i] = sum;
+      s_off[i] = sum;
+    }
+    __syncthreads();
+    if (w < G) warp_exclusive_scan(s_off + w * E, E, lane);
+    if (tid == 0) {
+      s_scal[0] = 0;  // residents with work
+      s_scal[1] = 0;  // home experts
+      s_scal[2] = 0;  // experts with work
+    }
+    __syncthreads();
+    for (int i = tid; i < E * G; i += nt) {
+      const int e = i / G, d = i - (i / G) * G;
+      int run = s_off[d * E + e];
+      for (int g = 0; g < G; ++g) {
+        o.slot_base[(g * E + e) * G + d] = run;
+        run += S[(g * E + e) * G + d];
+      }
+    }
+    for (int e = tid; e < E; e += nt) {
+      const int ne = s_n[me * E + e];
+      const bool re = home[e] == me;
+      s_key[e] = plan_key(re, ne, e);
+      if (re) atomicAdd(&s_scal[1], 1);
+      if (ne > 0) {
+        atomicAdd(&s_scal[2], 1);
+        if (re) atomicAdd(&s_scal[0], 1);
+      }
+    }
+    __syncthreads();
+    const int n_res_work = s_scal[0], n_home = s_scal[1], n_work = s_scal[2];
+    for (int e = w; e < E; e += nt / 32) {
+      const unsigned long long key = s_key[e];
+      if (key == ~0ull) continue;  // warp-uniform
+      const int oo = warp_rank(s_key, E, key, lane);
+      if (lane == 0) {
+        int wslot;
+        if (home[e] == me) {
+          wslot = 0;
+          for (int e2 = 0; e2 < e; ++e2) wslot += (home[e2] == me);
+        } else {
+          const int fi = oo - n_res_work;
+          wslot = n_home + (o.cache_slots > 0 ? fi % o.cache_slots : fi);
+          o.fetch[fi] = e;
+        }
+        const int ne = s_n[me * E + e];
+        o.segs[oo] = make_int4(s_off[me * E + e], ne, wslot, e);
+        s_cnt[oo] = (ne + 127) / 128;
+      }
+    }
+    if (tid == 0) {
+      *o.n_seg = n_work;
+      *o.n_fetch = n_work - n_res_work;
+    }
+    __syncthreads();
+    block_scan_to(s_cnt, n_work, o.mprefix, s_tmp);
+    return;
+  }
+
   // ---------------- EP mode: this process is rank `me` ----------------
   for (int i = tid; i < GE; i += nt) {
     const int g = i / E, e = i - (i / E) * E;
@@ -796,8 +865,9 @@ int launch_rebalance(int32_t* S, int G, int E, int q, int32_t* iters, int32_t* l
 static int check_layout_args(int G, int E, int mode, int me) {
   if (G < 1 || G > 32 || E < 1 || E > 1024 || G * E > kLayMaxGE)
     return set_error(HM_EINVAL, "dispatch_layout: need G <= 32, E <= 1024, G*E <= 8192");
-  if (mode != HM_LAYOUT_LOCAL && mode != HM_LAYOUT_EP) return set_error(HM_EINVAL, "dispatch_layout: bad mode");
-  if (mode == HM_LAYOUT_EP && (me < 0 || me >= G)) return set_error(HM_EINVAL, "dispatch_layout: bad rank");
+  if (mode != HM_LAYOUT_LOCAL && mode != HM_LAYOUT_EP && mode != HM_LAYOUT_EP_EXPERT)
+    return set_error(HM_EINVAL, "dispatch_layout: bad mode");
+  if (mode != HM_LAYOUT_LOCAL && (me < 0 || me >= G)) return set_error(HM_EINVAL, "dispatch_layout: bad rank");
   return HM_OK;
 }
 

@@ -187,8 +187,8 @@ class EPHarMoEnyBlock:
         self.stats = BlockStats()
         if cfg.transport == "p2p":
             self._setup_p2p()
-            # ours: router, hist_scan, plan, ep_offsets, dispatch_push, fetch, gemm1, gemm2, combine
-            self.KERNELS_PER_FORWARD = 9
+            # ours: router, hist_scan, plan, dispatch_push, fetch, gemm1, gemm2, combine
+            self.KERNELS_PER_FORWARD = 8
 
     FETCH_PAIRS = 2  # CTA pairs of each GEMM launch that run the bounded-cache K6 channel
 
@@ -353,8 +353,6 @@ class EPHarMoEnyBlock:
         self.mall_row_addrs = [b + lay["m_all"] + me * E * 4 for b in bases]
         base0 = self.arena.data_ptr() + lay["flags"]
         self.local_flag_addrs = [[base0 + (c * G + g) * 4 for g in range(G)] for c in range(3)]
-        self.dst_delta = torch.empty(G, dtype=torch.int32, device=self.device)
-        self.recv_split = torch.empty(G + 1, dtype=torch.int32, device=self.device)
         dist.barrier(group=self.group)  # every arena zeroed and mapped before anyone signals
 
     def _p2p_stages(self, st, s):
@@ -381,12 +379,14 @@ class EPHarMoEnyBlock:
             ops.stream_signal(self.meta_addrs, 1, s)
             ops.stream_wait(self.flags[0], 1, s)
             ops.stream_signal(self.local_flag_addrs[0], 0, s)
-            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP, me, m_all=self.m_all_buf,
+            # expert-major receive buffers: every sender places its rows from the replicated S, and
+            # this rank's GEMMs see one segment per expert (all sources' rows contiguous)
+            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP_EXPERT, me,
+                         m_all=self.m_all_buf,
                          cache_slots=self.n_cache if self.bounded else 0, stream=s)
             m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
-            ops.ep_offsets(p.S, me, self.dst_delta, self.recv_split, stream=s)
             pos = torch.empty((Tg, k), dtype=torch.int32, device=self.device)
-            ops.dispatch_push(x, idx, lrank, tile_off, p.S, p.layout.slot_base, self.dst_delta, me, self.p2p_rows,
+            ops.dispatch_push(x, idx, lrank, tile_off, p.S, p.layout.slot_base, None, me, self.p2p_rows,
                               self.p2p_tok, pos=pos, stream=s)
             ops.stream_signal(self.tok_addrs, 1, s)
             ops.stream_wait(self.flags[1], 1, s)
@@ -420,7 +420,7 @@ class EPHarMoEnyBlock:
             lay = st["plan"].layout
             kw = dict(slot_done=self.done_out, fetch=self._fetch_plan(lay, 2, 1)) if self.bounded else {}
             ops.grouped_gemm_remote(self.h_buf, self.w_out.view(-1, cfg.d_ff), d, lay, ops.HM_EPI_STORE,
-                                    self.p2p_out, self.recv_split, self.recv_tok, slot_ready=self.ready_out,
+                                    self.p2p_out, None, self.recv_tok, slot_ready=self.ready_out,
                                     ready_from_slot=self.n_home, epoch=1, stream=s, **kw)
             if self.n_cache > 0:
                 self.ready_in.zero_()

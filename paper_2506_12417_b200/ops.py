@@ -14,6 +14,7 @@ from ._lib import (  # noqa: F401
     HM_EPI_STORE,
     HM_EPI_SWIGLU,
     HM_LAYOUT_EP,
+    HM_LAYOUT_EP_EXPERT,
     HM_LAYOUT_LOCAL,
     HM_POLICY_EVEN_SPLIT,
     HM_POLICY_NONE,
@@ -309,7 +310,9 @@ def ep_offsets(S, me: int, dst_delta=None, recv_split=None, stream=None):
 def dispatch_push(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, me: int, dst_rows, dst_tok, pos=None,
                   stream=None):
     """Fused scatter + dispatch: rows land in the destination ranks' receive buffers.
-    dst_rows / dst_tok: uint64 (int64) device tensors of G peer pointers."""
+    dst_rows / dst_tok: uint64 (int64) device tensors of G peer pointers.  dst_delta=None:
+    slot_base is an HM_LAYOUT_EP_EXPERT layout and the stored token index is tagged with the
+    source rank ((me << 24) | t*k + j)."""
     _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, dst_rows, dst_tok, pos)
     T, d = x.shape
     k = topk_idx.shape[1]
@@ -321,7 +324,8 @@ def dispatch_push(x, topk_idx, lrank, tile_off, S, slot_base, dst_delta, me: int
 def grouped_gemm_remote(A, W, N: int, layout: "Layout", epilogue: int, out_ptrs, out_split, row_map, slot_ready=None,
                         ready_from_slot: int = 0, epoch: int = 0, a_rows: int | None = None, slot_done=None,
                         fetch=None, stream=None):
-    """K5 with the rows of each segment stored into the owning source rank's buffer (peer pointer)."""
+    """K5 with the rows of each segment stored into the owning source rank's buffer (peer pointer):
+    per segment via out_split, or (out_split=None) per row via the source tag in row_map."""
     _require_cuda(A, W, out_ptrs, out_split, row_map, slot_ready, slot_done)
     rows = A.shape[0] if a_rows is None else int(a_rows)
     K = A.shape[1]

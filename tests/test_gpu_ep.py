@@ -67,6 +67,30 @@ def test_layout_ep_matches_oracle(G, E, me):
     assert fetched == [int(e) for e in order if not resident[e]]  # plan order, one channel
 
 
+@pytest.mark.parametrize("G,E,me,cache", [(2, 16, 0, 0), (2, 16, 1, 0), (8, 128, 3, 0), (4, 10, 2, 0),
+                                           (8, 128, 5, 2), (4, 32, 1, 1)])
+def test_layout_ep_expert_matches_oracle(G, E, me, cache):
+    """Expert-major receive layout of the one-sided p2p dispatch: every bucket's row in its
+    destination's buffer, one GEMM segment per expert in plan order, bounded-cache slots."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    m, home, S = _rand_S(G, E, 256 * G, 2, 1.5, G + E + me, "blocked")
+    St = torch.from_numpy(S.astype(np.int32)).to(dev)
+    ht = torch.from_numpy(home.astype(np.int32)).to(dev)
+    lay = ops.dispatch_layout(St, ht, ops.HM_LAYOUT_EP_EXPERT, me, cache_slots=cache)
+    torch.cuda.synchronize()
+    sb_ref, segs_ref = orc.ep_expert_layout(S, home, me, cache)
+    assert np.array_equal(lay.slot_base.cpu().numpy(), sb_ref)
+    n_seg = int(lay.n_seg.item())
+    assert [tuple(r) for r in lay.segs[:n_seg].cpu().numpy().tolist()] == segs_ref
+    mp = lay.mtile_prefix[: n_seg + 1].cpu().numpy()
+    assert np.array_equal(mp, np.concatenate([[0], np.cumsum([(sg[1] + 127) // 128 for sg in segs_ref])]))
+    resident = (home == me).astype(np.int32)
+    order = orc.plan_order(S[:, :, me].sum(axis=0), resident)
+    assert lay.fetch[: int(lay.n_fetch.item())].cpu().numpy().tolist() == [int(e) for e in order if not resident[e]]
+
+
 def test_permute_positions_ep_match_oracle():
     """EP send layout: positions of every assignment = oracle ep_send_positions."""
     from paper_2506_12417_b200 import ops

@@ -6,8 +6,9 @@ alone (CUDA-graph replay, L2 flushed before each call, CUDA events):
   router      hm_router_topk on the rank's T/G tokens
   plan        hm_plan (EP layout of rank `me`) on the m_all the metadata exchange delivers
   dispatch    hm_dispatch_push of the rank's tokens (the G destination buffers are local here)
-  ffn1/ffn2   the grouped GEMMs over rank `me`'s receive buffer: one segment per (expert, source)
-              with the EP weight slots (home experts, then the fetched experts in plan order)
+  ffn1/ffn2   the grouped GEMMs over rank `me`'s expert-major receive buffer (the p2p transport's
+              HM_LAYOUT_EP_EXPERT: one segment per expert) with the EP weight slots (home experts,
+              then the fetched experts in plan order)
   combine     hm_combine of the rank's T/G tokens
 
 What one GPU cannot measure is modelled explicitly and reported separately: NVLink transfer
@@ -87,7 +88,8 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
     # rank-independent kernels
     xr = x[:Tg].contiguous()
     out["router_us"] = _graph_time_us(lambda: ops.router_topk(xr, wgp, bias, 1, Tg, k, k > 1, E=E), flush)
-    plan0 = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, ops.HM_LAYOUT_EP, 0, m_all=m_all)
+    mode = ops.HM_LAYOUT_EP_EXPERT  # the p2p transport's expert-major receive buffers
+    plan0 = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, mode, 0, m_all=m_all)
     torch.cuda.synchronize()
     S = plan0.S.cpu().numpy().astype(np.int64)
     loads = S.sum(axis=(0, 1))
@@ -100,9 +102,9 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
     expert_bytes = (n_in * d + d * f) * 2
     for me in ranks:
         r = {}
-        r["plan_us"] = _graph_time_us(lambda: ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, ops.HM_LAYOUT_EP, me,
+        r["plan_us"] = _graph_time_us(lambda: ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, mode, me,
                                                        m_all=m_all), flush)
-        p = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, ops.HM_LAYOUT_EP, me, m_all=m_all)
+        p = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, mode, me, m_all=m_all)
         lay = p.layout
         n_seg = int(lay.n_seg.item())
         n_fetch = int(lay.n_fetch.item())
@@ -111,7 +113,6 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
         rows = int(segs[:, 1].sum()) if n_seg else 0
         r.update(recv_rows=rows, fetched_experts=n_fetch, segments=n_seg)
         # dispatch push of my tokens into G local stand-ins for the destination buffers
-        dst_delta, recv_split = ops.ep_offsets(p.S, me)
         cap = int(loads.max()) + 1
         bufs = [torch.empty((cap, d), dtype=torch.bfloat16, device=dev) for _ in range(G)]
         toks = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(G)]
@@ -123,7 +124,7 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
         toff_me = tile_off[me * tiles:(me + 1) * tiles].contiguous()
         x_me = x[sl].contiguous()
         r["dispatch_local_us"] = _graph_time_us(
-            lambda: ops.dispatch_push(x_me, idx_me, lrank_me, toff_me, p.S, lay.slot_base, dst_delta, me, dst_rows,
+            lambda: ops.dispatch_push(x_me, idx_me, lrank_me, toff_me, p.S, lay.slot_base, None, me, dst_rows,
                                       dst_tok), flush)
         flows = S.sum(axis=1)
         sent = int(flows[me].sum() - flows[me, me])
