@@ -254,11 +254,17 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
     if (rebalance != HM_POLICY_REBALANCE) rebalance = HM_POLICY_NONE;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < G * G; i += blockDim.x) {
-    const int g = i / G, d = i - (i / G) * G;
-    long long f = 0;
-    for (int e = 0; e < E; ++e) f += S[(g * E + e) * G + d];
-    F[g * 32 + d] = f;
+  // flows F[g][d] = sum_e S[g,e,d]: one warp per (g, d) pair, lanes stride the experts
+  {
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x >> 5; i < G * G; i += nw) {
+      const int g = i / G, d = i - (i / G) * G;
+      long long f = 0;
+      for (int e = lane; e < E; e += 32) f += S[(g * E + e) * G + d];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) f += __shfl_xor_sync(0xffffffffu, f, off);
+      if (lane == 0) F[g * 32 + d] = f;
+    }
   }
   if (St != nullptr && rebalance)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
