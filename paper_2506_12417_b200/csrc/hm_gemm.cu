@@ -418,6 +418,9 @@ __device__ void fetch_block(uint8_t* dst, const uint8_t* src, long long bytes, u
     mbar_arrive_expect_tx(&bars[st], len);
     bulk_g2s(ring + st * kFetchChunk, src + c * kFetchChunk, len, &bars[st]);
   };
+  // stage of chunk i is refilled (with chunk i + kFetchStages) kLag chunks later, once at most kLag
+  // newer stores are still reading shared memory: loads and stores both stay in flight
+  constexpr int kLag = 2;
   for (long long i = 0; i < min((long long)kFetchStages, m); ++i) issue(i);
   for (long long i = 0; i < m; ++i) {
     const int st = (int)(i % kFetchStages);
@@ -426,11 +429,17 @@ __device__ void fetch_block(uint8_t* dst, const uint8_t* src, long long bytes, u
     const long long c = fc + i * nf;
     const uint32_t len = (uint32_t)min((long long)kFetchChunk, bytes - c * kFetchChunk);
     bulk_s2g(dst + c * kFetchChunk, ring + st * kFetchChunk, len);
-    if (i + kFetchStages < m) {
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // stage st is free again
-      issue(i + kFetchStages);
+    const long long j = i - kLag;  // chunk whose stage is refilled now
+    if (j >= 0 && j + kFetchStages < m) {
+      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kLag) : "memory");
+      issue(j + kFetchStages);
     }
   }
+  for (long long j = max(0ll, m - kLag); j < m; ++j)  // refills the loop above did not reach
+    if (j + kFetchStages < m) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      issue(j + kFetchStages);
+    }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   asm volatile("fence.proxy.async.global;" ::: "memory");  // bulk writes before the generic release
 }

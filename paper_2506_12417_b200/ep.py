@@ -190,7 +190,9 @@ class EPHarMoEnyBlock:
             # ours: router, hist_scan, plan, dispatch_push, fetch, gemm1, gemm2, combine
             self.KERNELS_PER_FORWARD = 8
 
-    FETCH_PAIRS = 2  # CTA pairs of each GEMM launch that run the bounded-cache K6 channel
+    # CTA pairs of each GEMM launch that run the bounded-cache K6 channel: TMA bulk copies reach
+    # ~90 GB/s per pair HBM->HBM on B200 (tools/dbg/fetch_bw.py: 1 / 2 / 4 pairs = 94 / 177 / 317 GB/s)
+    FETCH_PAIRS = 4
 
     def _fetch_sources(self):
         """Device tables of every expert's weight blocks at its home rank (NVLink, CUDA IPC) or
