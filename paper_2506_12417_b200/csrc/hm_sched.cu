@@ -266,11 +266,13 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
       if (lane == 0) F[g * 32 + d] = f;
     }
   }
-  if (St != nullptr && rebalance)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int g = i / (G * E), r = i - g * (G * E), d = r / E, e = r - d * E;
-      St[i] = S[(g * E + e) * G + d];
+  if (St != nullptr && rebalance) {  // St[g][d][e]: one warp per (g, d) row, lanes stride the experts
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int row = threadIdx.x >> 5; row < G * G; row += nw) {
+      const int g = row / G, d = row - g * G;
+      for (int e = lane; e < E; e += 32) St[row * E + e] = S[(g * E + e) * G + d];
     }
+  }
   __syncthreads();
 
   if (threadIdx.x < 32) {
@@ -483,18 +485,20 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       s_key[i] = plan_key(home[e] == d, s_n[i], e);
     }
     __syncthreads();
-    // one warp per (dest, expert): rank = number of smaller plan keys of that dest
-    for (int p = w; p < GE; p += nt / 32) {
+    // one thread per (dest, expert): rank = number of smaller plan keys of that dest (the dest's
+    // keys are read as shared-memory broadcasts: a warp's 32 entries share d when E >= 32)
+    for (int p = tid; p < GE; p += nt) {
       const unsigned long long key = s_key[p];
-      if (key == ~0ull) continue;  // warp-uniform
-      const int d = p / E, e = p - (p / E) * E;
-      const int pos = warp_rank(s_key + d * E, E, key, lane);
-      if (lane == 0) {
-        const int ne = s_n[p];
-        const int sidx = s_nnz[d] + pos;
-        o.segs[sidx] = make_int4(s_base[d] + s_off[p], ne, e, e);
-        s_cnt[sidx] = (ne + 127) / 128;
-      }
+      if (key == ~0ull) continue;
+      const int d = p / E, e = p - d * E;
+      const unsigned long long* kd = s_key + d * E;
+      int pos = 0;
+#pragma unroll 4
+      for (int j = 0; j < E; ++j) pos += kd[j] < key;
+      const int ne = s_n[p];
+      const int sidx = s_nnz[d] + pos;
+      o.segs[sidx] = make_int4(s_base[d] + s_off[p], ne, e, e);
+      s_cnt[sidx] = (ne + 127) / 128;
     }
     __syncthreads();
     if (tid == 0) g_phase_ns[5] = globaltimer_ns();
@@ -807,6 +811,9 @@ __global__ void __launch_bounds__(kPlanThreads)
   int* s_scr = s_S + GE * G;      // layout scratch [3*G*E + 1 + 3*E]
   int* s_St = s_scr + layout_scratch_ints(G, E);  // [G*G*E] transposed S for the fast rebalance loop
   if (threadIdx.x == 0) g_phase_ns[0] = globaltimer_ns();
+#ifdef HM_PLAN_CLOCK
+  const long long c0 = clock64();
+#endif
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_home[i] = home_g[i];
   if (kHist) {
     dev_hist_reduce(tile_hist, G, tpr, E, s_m, m_out, tile_off, s_part);
@@ -820,6 +827,9 @@ __global__ void __launch_bounds__(kPlanThreads)
   for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
   dev_layout(s_S, s_home, G, E, mode, me, o, s_scr);
   if (threadIdx.x == 0) g_phase_ns[3] = globaltimer_ns();
+#ifdef HM_PLAN_CLOCK
+  if (threadIdx.x == 0) g_phase_ns[7] = (unsigned long long)(clock64() - c0);
+#endif
 }
 
 // ------------------------------------------------------------------------------------------
