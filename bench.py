@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true",
-                    help="N=1: skip the other BASELINE configs (C1/C3/C4/C5) and the sustained-power loop")
+                    help="N=1: skip the other BASELINE configs (C1/C3/C4/C5) and the G=8 projection")
     ap.add_argument("--sustained-steps", type=int, default=300,
                     help="N=1: back-to-back steps of the sustained-power measurement (0 = skip)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -736,7 +736,7 @@ def run_ours(args, rank, world, local_rank):
     # ---- sustained: the same step back to back long enough for the 1 kW power cap to engage
     # (the default timed loop above is a short burst); reported beside the headline ----
     sustained = None
-    if world == 1 and not args.no_extras and args.sustained_steps > 0:
+    if world == 1 and args.sustained_steps > 0:
         ns = args.sustained_steps
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sampler2 = ClockSampler(local_rank, enabled=not args.no_clocks)
