@@ -191,7 +191,7 @@ class EPHarMoEnyBlock:
             self.KERNELS_PER_FORWARD = 8
 
     # CTA pairs of each GEMM launch that run the bounded-cache K6 channel: TMA bulk copies reach
-    # ~90 GB/s per pair HBM->HBM on B200 (tools/dbg/fetch_bw.py: 1 / 2 / 4 pairs = 94 / 177 / 317 GB/s)
+    # ~90 GB/s per pair HBM->HBM on B200 (tools/fetch_pairs_bw.py: 1 / 2 / 4 pairs = 94 / 177 / 317 GB/s)
     FETCH_PAIRS = 4
 
     def _fetch_sources(self):
