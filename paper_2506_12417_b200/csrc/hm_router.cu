@@ -757,7 +757,7 @@ __global__ void __launch_bounds__(kR2Threads)
   }
 }
 
-// HM_ROUTER_V2=1: the split-K cluster kernel above (opt-in experiment, profiles/r2_router_split.txt:
+// HM_ROUTER_V2=1: the split-K cluster kernel above (opt-in experiment, profiles/r2_experiments.txt:
 // correct and bit-exact on the router tests, but slower than the one-CTA-per-tile kernel at
 // 16k tokens - 49-113 us vs 37-43 us cold for C = 2..8 - because launching thousands of
 // cluster CTAs and three cluster barriers per tile cost more than the split saves; it wins
