@@ -14,10 +14,19 @@ Alg. 1 across ranks, every step a kernel or a collective:
                                 GEMM's producer waits on a per-slot ready flag
   6 gather                      all_to_all_single back + hm_combine
 
-The split sizes of the all_to_all are host arguments in NCCL, so S is copied to
-the host once per layer (32 KB at G=8, E=128).  Host-side plumbing lives in
-plain functions (``ep_counts``, ``exchange_*``) that are exercised with the
-gloo backend on CPU by tests/test_ep_gloo.py.
+That is transport "nccl".  The split sizes of the all_to_all are host arguments in NCCL, so S is
+copied to the host once per layer (32 KB at G=8, E=128).  Host-side plumbing lives in plain
+functions (``ep_counts``, ``exchange_*``) that are exercised with the gloo backend on CPU by
+tests/test_ep_gloo.py.
+
+Transport "p2p" (the default of bench.py) has no collective and no host round trip: every rank
+maps every peer's arena through CUDA IPC once; step 2 pushes the histogram row into every peer's
+m_all and raises a stream flag; step 4 is hm_dispatch_push writing each token row straight into
+its destination's EXPERT-MAJOR receive buffer (HM_LAYOUT_EP_EXPERT: rows placed from the
+replicated S, one GEMM segment per expert); step 6 is FFN2's epilogue storing every row into its
+source rank's token-major output (the source rides in the pushed token index), then the combine.
+A bounded expert cache (expert_cache_size below the fetchable experts) runs K6 as fetch pairs
+inside the GEMM launches (hm_fetch_plan).
 """
 
 from __future__ import annotations
