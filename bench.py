@@ -543,11 +543,11 @@ def extra_workloads(args, dev, peaks3):
         sys.path.insert(0, os.path.join(REPO, "tools"))
         from ep_projection import project
 
-        for pl in ("round_robin", "blocked"):
-            pr = project(G=8, q=32, placement=pl, zipf_s=1.0, peak_tflops=tc)
+        for G_, pl in ((2, "round_robin"), (4, "round_robin"), (8, "round_robin"), (8, "blocked")):
+            pr = project(G=G_, q=32, placement=pl, zipf_s=1.0, peak_tflops=tc)
             crit = pr["per_rank"][pr["critical_rank"]]
-            out[f"C2_ep8_projection_{pl}"] = {
-                "config": f"BASELINE configs[1] at G=8 (expert-parallel, {pl} placement, q=32): the critical "
+            out[f"C2_ep{G_}_projection_{pl}"] = {
+                "config": f"BASELINE configs[1] at G={G_} (expert-parallel, {pl} placement, q=32): the critical "
                           f"rank's kernels measured at per-rank size on one B200, NVLink at 900 GB/s and "
                           f"{pr['config']['handshake_us']} us per cross-rank handshake modelled",
                 "projected_step_us": pr["projected_step_us"], "projected_tokens_per_s": pr["projected_tokens_per_s"],
@@ -558,7 +558,7 @@ def extra_workloads(args, dev, peaks3):
                 "critical_rank_recv_rows": crit["recv_rows"], "critical_rank_fetches": crit["fetched_experts"]}
             torch.cuda.empty_cache()
     except Exception as e:  # noqa: BLE001
-        out["C2_ep8_projection"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
+        out["C2_ep_projection"] = {"error": f"{type(e).__name__}: {str(e)[:200]}"}
     # C5: skew sweep uniform -> Zipf 1.5, max/mean per-GPU load with rebalancing off / on at
     # G = 2/4/8 (blocked placement: hot experts homed together), plus the one-GPU block rate
     try:
