@@ -360,6 +360,9 @@ struct PairCursor {
 // scatter (K4) is never written.  Loader warps fence the generic-proxy writes for the
 // tensor core (fence.proxy.async) and arrive on the leader's full barrier, which then
 // counts 1 (B expect_tx) + 8 (4 loader warps x 2 CTAs) arrivals.
+#ifndef HM_GEMM_ONCE_FIRST
+#define HM_GEMM_ONCE_FIRST 1
+#endif
 #ifndef HM_ALOAD_WARPS
 #define HM_ALOAD_WARPS 4
 #endif
@@ -511,6 +514,20 @@ __device__ void fetch_pair_role(const hm_fetch_plan& fp, uint8_t* smem, int fc, 
   }
 }
 
+// work unit t of the persistent walk -> pair tile + column slice (-1: the whole 256 columns)
+struct TailSplit {
+  int t_split;  // first split tile
+  int units;    // walk length
+  __device__ __forceinline__ int tile(int t, int& slice) const {
+    if (t < t_split) {
+      slice = -1;
+      return t;
+    }
+    slice = (t - t_split) & 1;
+    return t_split + ((t - t_split) >> 1);
+  }
+};
+
 template <int kEpi, bool kGather>
 __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kGemmThreads, 1)
     grouped_gemm_2cta_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -522,7 +539,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
                              int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
                              const int* __restrict__ a_gather, int a_gather_div, int a_src_rows,
                              const unsigned long long* __restrict__ out_ptrs, const int* __restrict__ out_split,
-                             int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan) {
+                             int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan, int tail_split) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   if (fplan.pairs > 0 && (int)(blockIdx.x >> 1) >= (int)(gridDim.x >> 1) - fplan.pairs) {
@@ -583,30 +600,45 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
   for (int i = lane; i < n_seg; i += 32) total += (mp[i + 1] - mp[i] + 1) >> 1;
   total = (int)__reduce_add_sync(0xffffffffu, (unsigned)total) * NB;
   const int KB = K / kBK;
+  // Tail split: when the last wave is at most half full (rem = total % npairs <= npairs / 2,
+  // e.g. Switch FFN2: 393 pair tiles on 74 pairs), its tiles run as two 128-column units on
+  // twice as many pairs (N = 128 MMAs, 64 weight rows per CTA).  Every output element is still
+  // one full-K accumulation in the same order: results are bit-identical to the unsplit walk.
+  TailSplit ts{total, total};
+  if (kEpi != kEpiSwiGLU && tail_split && slot_done == nullptr) {
+    const int rem = total % npairs;
+    if (rem > 0 && 2 * rem <= npairs) ts = TailSplit{total - rem, total + rem};
+  }
+  const int units = ts.units;
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs) =====
       const uint64_t pol_a = l2_policy_evict_normal();
-      const uint64_t pol_b = l2_policy_evict_last();
+      const uint64_t pol_w = l2_policy_evict_last();
+      // weights of a segment with a single pair m-tile are read once: streamed evict_first
+      // (measured TMA read ceiling 6.0 vs 5.6 TB/s under evict_last, tools/stream_bench)
+      const uint64_t pol_w1 = HM_GEMM_ONCE_FIRST ? l2_policy_evict_first() : pol_w;
       const uint32_t full_leader = mapa_shared(full, 0);
       PairCursor cur{segs, mp, NB};
       cur.half_tiles = (half_tiles & 1) != 0;
       cur.gm = max(1, half_tiles >> 1);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < total; t += npairs) {
+      for (int t = pair; t < units; t += npairs) {
         int4 seg;
-        int m, nb;
+        int m, nb, slice;
         bool hf;
-        cur.seek(t, seg, m, nb, hf);
+        cur.seek(ts.tile(t, slice), seg, m, nb, hf);
         const int row0 = seg.x + m * 2 * kBM + (int)rank * (hf ? kBM / 2 : kBM);
         const int brow0 = seg.z * N + nb * kBN;
-        const int brow = brow0 + (int)rank * (kBN / 2);
+        // split unit: 128 columns, 64 weight rows per CTA (tmap_b64: 64-row boxes)
+        const int brow = slice < 0 ? brow0 + (int)rank * (kBN / 2) : brow0 + slice * (kBN / 2) + (int)rank * (kBN / 4);
         // half tile: A is 64 rows per CTA; SwiGLU B is re-paired so CTA r holds gate rows
         // [64r, 64r+64) then the matching up rows -> every TMEM lane holds gate and up
         const bool b_split = hf && kEpi == kEpiSwiGLU;
-        const uint32_t tx = (kGather ? 0u : (hf ? k2Half / 2 : k2Half)) + k2Half;
+        const uint32_t tx = (kGather ? 0u : (hf ? k2Half / 2 : k2Half)) + (slice < 0 ? k2Half : k2Half / 2);
+        const uint64_t pol_b = cur.pair_tiles(cur.s) == 1 ? pol_w1 : pol_w;
         if (slot_ready != nullptr && seg.z >= ready_from_slot) {
           // watchdog: a fetch that never lands is a bug upstream; fail the launch instead of
           // hanging the device (~10 s)
@@ -637,7 +669,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
             tma_load_2d_2cta(sa + k2Half + k2Half / 2, &tmap_b64, full_leader + stage * 8, kb * kBK,
                              brow0 + kBN / 2 + (int)rank * 64, pol_b);
           } else {
-            tma_load_2d_2cta(sa + k2Half, &tmap_b, full_leader + stage * 8, kb * kBK, brow, pol_b);
+            tma_load_2d_2cta(sa + k2Half, slice < 0 ? &tmap_b : &tmap_b64, full_leader + stage * 8, kb * kBK, brow,
+                             pol_b);
           }
           if (++stage == k2Stages) {
             stage = 0;
@@ -651,18 +684,21 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       // ===== MMA issuer (leader CTA) =====
       constexpr uint32_t idesc_full = make_idesc_bf16(2 * kBM, kBN);
       constexpr uint32_t idesc_half = make_idesc_bf16(kBM, kBN);  // 64 rows per CTA, "2x2" TMEM layout
+      constexpr uint32_t idesc_full_n128 = make_idesc_bf16(2 * kBM, kBN / 2);  // tail-split units
+      constexpr uint32_t idesc_half_n128 = make_idesc_bf16(kBM, kBN / 2);
       PairCursor cur{segs, mp, NB};
       cur.half_tiles = (half_tiles & 1) != 0;
       cur.gm = max(1, half_tiles >> 1);
       int stage = 0;
       uint32_t phase = 0;
       int i = 0;
-      for (int t = pair; t < total; t += npairs, ++i) {
+      for (int t = pair; t < units; t += npairs, ++i) {
         int4 seg;
-        int m, nb;
+        int m, nb, slice;
         bool hf;
-        cur.seek(t, seg, m, nb, hf);
-        const uint32_t idesc = hf ? idesc_half : idesc_full;
+        cur.seek(ts.tile(t, slice), seg, m, nb, hf);
+        const uint32_t idesc =
+            slice < 0 ? (hf ? idesc_half : idesc_full) : (hf ? idesc_half_n128 : idesc_full_n128);
         const int acc = i & 1;
         mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -698,11 +734,11 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     cur.gm = max(1, half_tiles >> 1);
     // the gather indices of a tile are loaded one tile ahead (software pipelined), so the
     // dependent index -> row address chain never stalls the first k-block of a tile
-    auto tile_rows = [&](int tt, int& cta_rows, int (&gidx)[kARowsPerLane]) {
+    auto tile_rows = [&](int tu, int& cta_rows, int (&gidx)[kARowsPerLane]) {
       int4 sg;
-      int mm, nbb;
+      int mm, nbb, sl;
       bool hff;
-      cur.seek(tt, sg, mm, nbb, hff);
+      cur.seek(ts.tile(tu, sl), sg, mm, nbb, hff);
       cta_rows = hff ? kBM / 2 : kBM;
       const int rows = max(0, min(cta_rows, sg.y - mm * 2 * kBM - (int)rank * cta_rows));
       const int rbase = sg.x + mm * 2 * kBM + (int)rank * cta_rows;
@@ -715,8 +751,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     int stage = 0, sig_stage = 0, pending = 0;
     uint32_t phase = 0;
     int cta_rows_nx = 0, gidx_nx[kARowsPerLane];
-    if (pair < total) tile_rows(pair, cta_rows_nx, gidx_nx);
-    for (int t = pair; t < total; t += npairs) {
+    if (pair < units) tile_rows(pair, cta_rows_nx, gidx_nx);
+    for (int t = pair; t < units; t += npairs) {
       const int cta_rows = cta_rows_nx;
       const char* src[kARowsPerLane];
 #pragma unroll
@@ -724,7 +760,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         const int src_row = min(gidx_nx[i] / a_gather_div, a_src_rows - 1);
         src[i] = reinterpret_cast<const char*>(a_src + (int64_t)src_row * K) + c * 16;
       }
-      if (t + npairs < total) tile_rows(t + npairs, cta_rows_nx, gidx_nx);
+      if (t + npairs < units) tile_rows(t + npairs, cta_rows_nx, gidx_nx);
       for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t dst = smem_u32(smem + stage * 2 * k2Half);
@@ -769,11 +805,11 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     cur.half_tiles = (half_tiles & 1) != 0;
       cur.gm = max(1, half_tiles >> 1);
     int i = 0;
-    for (int t = pair; t < total; t += npairs, ++i) {
+    for (int t = pair; t < units; t += npairs, ++i) {
       int4 seg;
-      int m, nb;
+      int m, nb, slice;
       bool hf;
-      cur.seek(t, seg, m, nb, hf);
+      cur.seek(ts.tile(t, slice), seg, m, nb, hf);
       // Full tile: lane = row (128 per CTA), columns [0, 256).  Half tile (M=128 "2x2" layout):
       // row r < 64 of this CTA sits in lanes r (columns [0,128) of the MMA's N) and 64 + r
       // (columns [128,256)), both at TMEM columns [0,128).  SwiGLU half tiles were loaded
@@ -781,9 +817,11 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       const int cta_rows = hf ? kBM / 2 : kBM;
       const int rows = max(0, min(cta_rows, seg.y - m * 2 * kBM - (int)rank * cta_rows));  // valid rows
       const int r_in_tile = (hf ? (q & 1) : q) * 32 + lane;
-      const int ncols = hf ? kHalfCols / 2 : kHalfCols;  // output columns of this warp
-      const int tcol0 = half * ncols;                    // its first TMEM column
-      const int ocol0 = (hf ? (q >> 1) * kHalfCols : 0) + half * ncols;
+      // a split unit (never SwiGLU) is a 128-column tile: same layout at half the width
+      const int hcols = slice < 0 ? kHalfCols : kHalfCols / 2;
+      const int ncols = hf ? hcols / 2 : hcols;  // output columns of this warp
+      const int tcol0 = half * ncols;            // its first TMEM column
+      const int ocol0 = (slice < 0 ? 0 : slice * (kOutCols / 2)) + (hf ? (q >> 1) * hcols : 0) + half * ncols;
       const int upoff = hf ? kBN / 4 : kBN / 2;  // SwiGLU: TMEM column distance gate -> up
       const bool valid = r_in_tile < rows;
       int64_t row = (int64_t)seg.x + m * 2 * kBM + rank * cta_rows + r_in_tile;
@@ -874,6 +912,12 @@ static bool use_half_tiles() {
     v = (e != nullptr && e[0] == '1') ? 0 : 1;
   }
   return v == 1;
+}
+
+// tail split of a half-empty last wave into 128-column units (HM_GEMM_TAIL_SPLIT=0 disables)
+static bool use_tail_split() {
+  const char* e = getenv("HM_GEMM_TAIL_SPLIT");  // read per launch: tests compare both walks
+  return !(e != nullptr && e[0] == '0');
 }
 
 // m-tile group of the pair-tile walk: 1 when a segment's weights (N x K bf16) fit easily
@@ -994,10 +1038,10 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
       rc = make_tmap_2d_bf16(&ta64, A, (uint64_t)a_rows, (uint64_t)K, kBM / 2, kBK);
       if (rc) return rc;
     }
-    if ((half_tiles & 1) && epilogue == kEpiSwiGLU) {
-      rc = make_tmap_2d_bf16(&tb64, W, (uint64_t)w_rows, (uint64_t)K, kBN / 4, kBK);
-      if (rc) return rc;
-    }
+    // 64-row weight boxes: SwiGLU half tiles, and the 128-column units of the tail split
+    rc = make_tmap_2d_bf16(&tb64, W, (uint64_t)w_rows, (uint64_t)K, kBN / 4, kBK);
+    if (rc) return rc;
+    const int tail_split = (epilogue != kEpiSwiGLU && slot_done == nullptr && use_tail_split()) ? 1 : 0;
     const bool gather = a_gather != nullptr;
     // every pair resident at once (static tile walk; the fetch pairs and the compute pairs wait
     // on each other); fetch pairs come out of the same budget
@@ -1024,7 +1068,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, ta64, tb64, half_tiles, s4,          \
                            mtile_prefix, n_seg, o, N, K,                                                          \
                            ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
-                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan);                            \
+                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan, tail_split);                \
   } while (0)
     switch (epilogue * 2 + (gather ? 1 : 0)) {
       case kEpiStore * 2: HM_GEMM2(kEpiStore, false); break;

@@ -274,6 +274,45 @@ def test_grouped_gemm(epi, N, K, counts):
     assert_close(out.float().cpu().numpy(), ref, f"gemm {epi} N={N} K={K}")
 
 
+@pytest.mark.parametrize("epi", ["store", "relu"])
+@pytest.mark.parametrize("N,K,n_seg", [(768, 3072, 5), (768, 3072, 13), (768, 768, 30), (768, 768, 40),
+                                       (3072, 768, 80), (256, 512, 77), (512, 256, 150)])
+def test_grouped_gemm_tail_split_bit_identical(epi, N, K, n_seg, monkeypatch):
+    """The tail split (a last wave at most half full runs as 128-column units, N = 128 MMAs) gives
+    bit-identical outputs to the unsplit walk: same full-K accumulation per element.  The segment
+    mix (32-row Switch-like experts, an odd full + half m-tile expert) gives pair-tile totals on
+    both sides of the split condition for any resident pair count."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    g = torch.Generator(device=dev).manual_seed(N * 7 + n_seg)
+    counts = [int(c) for c in torch.randint(1, 64, (n_seg,), generator=torch.Generator().manual_seed(n_seg))]
+    counts[n_seg // 2] = 300  # one expert with a full + a half pair tile
+    wslots = [i % 7 for i in range(n_seg)]
+    lay, rows = _segs_from_counts(counts, wslots, dev)
+    A = torch.randn((rows, K), device=dev, generator=g).to(torch.bfloat16)
+    W = (torch.randn((7 * N, K), device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    code = dict(store=ops.HM_EPI_STORE, relu=ops.HM_EPI_RELU)[epi]
+    perm = torch.randperm(rows, device=dev, generator=g).to(torch.int32)
+    src = torch.randn((97, K), device=dev, generator=g).to(torch.bfloat16)
+    gidx = torch.randint(0, 97, (rows,), device=dev, generator=g).to(torch.int32)
+    outs = {}
+    for split in ("0", "1"):
+        monkeypatch.setenv("HM_GEMM_TAIL_SPLIT", split)
+        outs[split] = (ops.grouped_gemm(A, W, N, lay, code), ops.grouped_gemm(A, W, N, lay, code, row_map=perm),
+                       ops.grouped_gemm(src, W, N, lay, code, a_gather=gidx))
+    torch.cuda.synchronize()
+    for a, b in zip(outs["0"], outs["1"]):
+        assert torch.equal(a, b)
+    ref, r0 = [], 0
+    for n, s in zip(counts, wslots):
+        acc = A[r0:r0 + n].float() @ W[s * N:(s + 1) * N].float().T
+        ref.append(torch.relu(acc) if epi == "relu" else acc)
+        r0 += n
+    ref = torch.cat(ref).to(torch.bfloat16).float().cpu().numpy()
+    assert_close(outs["1"][0].float().cpu().numpy(), ref, f"tail split {epi} N={N} K={K} segments={n_seg}")
+
+
 # ------------------------------------------------------------------------------------------
 # full block (LOCAL layout) vs the oracle
 # ------------------------------------------------------------------------------------------
