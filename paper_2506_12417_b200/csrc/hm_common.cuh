@@ -26,6 +26,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-byte aligned view of the dynamic shared memory: pointer arithmetic on the __shared__ array
+// itself (not an integer round trip) so the compiler keeps the shared address space and emits
+// LDS/STS instead of generic LD/ST for everything derived from it
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const int* __restrict__ row_map, const int* __restrict__ a_gather, int a_gather_div,
                         int a_gather_rows, const int* __restrict__ slot_ready, int ready_from_slot, int epoch) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kABytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_b + kStages * kBBytes);
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
                              const unsigned long long* __restrict__ out_ptrs, const int* __restrict__ out_split,
                              int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan, int tail_split) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   if (fplan.pairs > 0 && (int)(blockIdx.x >> 1) >= (int)(gridDim.x >> 1) - fplan.pairs) {
     // K6 fetch pair: both CTAs of the cluster leave before any TMEM / cluster barrier
     const int fc = (int)blockIdx.x - ((int)gridDim.x - 2 * fplan.pairs);

@@ -21,6 +21,19 @@
 
 namespace hm {
 
+#ifdef HM_ROUTER_STAMPS
+// diagnostics build only (tools/router_stamps.py): per-tile %globaltimer stamps of the phases
+__device__ unsigned long long g_rstamp[4096][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define HM_RSTAMP(i) do { if (blockIdx.x < 4096) g_rstamp[blockIdx.x][i] = gtimer(); } while (0)
+#else
+#define HM_RSTAMP(i) do { } while (0)
+#endif
+
 namespace {
 // descending compare-exchange on packed keys
 __device__ __forceinline__ void ce_desc(unsigned long long& x, unsigned long long& y) {
@@ -72,14 +85,110 @@ __device__ __forceinline__ void router_sort8(unsigned long long (&k)[8]) {
   ce_desc(k[1], k[2]); ce_desc(k[3], k[4]); ce_desc(k[5], k[6]);
 }
 
+// 32-bit compare-exchange / sorts for the truncated keys (2 instructions per comparator)
+__device__ __forceinline__ void ce_u32(uint32_t& x, uint32_t& y) {
+  const uint32_t hi = max(x, y), lo = min(x, y);
+  x = hi;
+  y = lo;
+}
+__device__ __forceinline__ void sort8_u32(uint32_t* k) {
+  ce_u32(k[0], k[2]); ce_u32(k[1], k[3]); ce_u32(k[4], k[6]); ce_u32(k[5], k[7]);
+  ce_u32(k[0], k[4]); ce_u32(k[1], k[5]); ce_u32(k[2], k[6]); ce_u32(k[3], k[7]);
+  ce_u32(k[0], k[1]); ce_u32(k[2], k[3]); ce_u32(k[4], k[5]); ce_u32(k[6], k[7]);
+  ce_u32(k[2], k[4]); ce_u32(k[3], k[5]);
+  ce_u32(k[1], k[4]); ce_u32(k[3], k[6]);
+  ce_u32(k[1], k[2]); ce_u32(k[3], k[4]); ce_u32(k[5], k[6]);
+}
+// A (sorted descending; na = the 9th largest of A's set, 0 if none) <- top-8 of A u B, na <- 9th
+// largest of the union: the elementwise max of A and reversed B is a bitonic top-8, the
+// elementwise min holds the bottom 8, whose maximum is the 9th
+__device__ __forceinline__ void merge8_u32(uint32_t* A, uint32_t& na, const uint32_t* B, uint32_t nb) {
+  uint32_t lo = max(na, nb);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t b = B[7 - i];
+    lo = max(lo, min(A[i], b));
+    A[i] = max(A[i], b);
+  }
+#pragma unroll
+  for (int s2 = 4; s2 > 0; s2 >>= 1)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if ((i & s2) == 0) ce_u32(A[i], A[i + s2]);
+  na = lo;
+}
+// key[0..8) <- the 8 largest of key[0..32), descending; ninth <- the 9th largest
+__device__ __forceinline__ void top8_of_32_u32(uint32_t (&key)[32], uint32_t& ninth) {
+#pragma unroll
+  for (int g = 0; g < 32; g += 8) sort8_u32(key + g);
+  uint32_t n0 = 0u, n2 = 0u;
+  merge8_u32(key, n0, key + 8, 0u);
+  merge8_u32(key + 16, n2, key + 24, 0u);
+  merge8_u32(key, n0, key + 16, n2);
+  ninth = n0;
+}
+// float -> order-preserving uint32 (-0 folded into +0, as the float compare treats them)
+__device__ __forceinline__ uint32_t ord_u32(float v) {
+  const uint32_t u = __float_as_uint(__fadd_rn(v, 0.0f));
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unord_u32(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
+// One 32-expert chunk of a row (2 < k <= 8 path): logits + bias, running (max, sum-exp) of the
+// part, exact order-preserving keys (left in a[] for the shared-memory copy) and the truncated
+// selection keys.  kGuard: the chunk extends past E (columns >= E are masked to -inf / key 0).
+template <bool kGuard>
+__device__ __forceinline__ void router_chunk(uint32_t (&a)[32], const float* __restrict__ sb, int nval,
+                                             uint32_t kbase, float& pmx, float& psum, uint32_t (&key)[32]) {
+  float cmx = -INFINITY;
+  const float4* b4 = reinterpret_cast<const float4*>(sb);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 b = b4[i];
+    const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int jj = 4 * i + h;
+      float v = __fadd_rn(__uint_as_float(a[jj]), bb[h]);
+      if (kGuard && jj >= nval) v = -INFINITY;
+      a[jj] = __float_as_uint(v);
+      cmx = fmaxf(cmx, v);
+    }
+  }
+  const float nmx = fmaxf(pmx, cmx);  // finite: the chunk has at least one expert < E
+  const float nb = -nmx * kLog2e;
+  float cs = (pmx == -INFINITY) ? 0.0f : __fmul_rn(psum, ex2_ftz(__fmaf_rn(pmx, kLog2e, nb)));
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) cs = __fadd_rn(cs, ex2_ftz(__fmaf_rn(__uint_as_float(a[jj]), kLog2e, nb)));  // -inf -> 0
+  pmx = nmx;
+  psum = cs;
+#pragma unroll
+  for (int jj = 0; jj < 32; ++jj) {
+    uint32_t u = __float_as_uint(__fadd_rn(__uint_as_float(a[jj]), 0.0f));  // -0 -> +0
+    u ^= static_cast<uint32_t>(static_cast<int32_t>(u) >> 31) | 0x80000000u;  // order-preserving
+    a[jj] = u;
+    key[jj] = (kGuard && jj >= nval) ? 0u : ((u & 0xFFFFFF00u) | (kbase - (uint32_t)jj));
+  }
+}
+
 constexpr int kRBM = 128;
 constexpr int kRBK = 64;
+constexpr uint32_t kRPartBytes = 24 * 1024;  // epilogue partials (4 parts x 11 fields x 128 rows x 4 B)
 constexpr int kRMaxStages = 8;
 constexpr uint32_t kRA = kRBM * kRBK * 2;  // 16 KB
 constexpr int kREpiWarps = 16;
 constexpr int kRThreads = 64 + kREpiWarps * 32;
 constexpr int kRKmax = 16;
-constexpr size_t kREpiSmem = 2 * kRBM * kRKmax * sizeof(int) + 4 * 256 * sizeof(int);
+constexpr size_t kREpiSmem = 2 * kRBM * kRKmax * sizeof(int) + 4 * 256 * sizeof(int) + 256 * sizeof(float);
 constexpr size_t kRSmemMax = 227 * 1024;
 // stages in flight: as many (A + Wg) k-blocks as fit (6 at E=128, 4 at E=256, 8 at E<=48)
 inline int router_stages(int E_pad) {
@@ -90,13 +199,13 @@ inline int router_stages(int E_pad) {
 }  // namespace
 
 template <int KMAX>
-__global__ void __maxnreg__(104)
+__global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K registers
     router_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                   const float* __restrict__ bias, int tokens_per_rank, int tiles_per_rank, int d, int E, int E_pad,
                   int k, int renorm, int32_t* __restrict__ topk_idx, float* __restrict__ topk_w,
                   int32_t* __restrict__ tile_hist, int32_t* __restrict__ lrank, int kRStages) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const uint32_t kRBmax = (uint32_t)E_pad * kRBK * 2;  // B stage stride (multiple of 2 KB)
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kRStages * kRA;
@@ -107,6 +216,7 @@ __global__ void __maxnreg__(104)
   int* s_idx = reinterpret_cast<int*>(smem_b + kRStages * kRBmax + 256);
   int* s_rank = s_idx + kRBM * kRKmax;
   int* s_cnt = s_rank + kRBM * kRKmax;  // [4][E_pad]
+  float* s_bias = reinterpret_cast<float*>(s_cnt + 4 * 256);  // [E_pad]: bias (0 without one)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -117,6 +227,7 @@ __global__ void __maxnreg__(104)
   const int rows = min(kRBM, tokens_per_rank - mt * kRBM);
   const int KB = d / kRBK;
   const uint32_t b_bytes = (uint32_t)E_pad * kRBK * 2;
+  if (threadIdx.x == 0) HM_RSTAMP(0);
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kRStages; ++s) {
@@ -142,10 +253,12 @@ __global__ void __maxnreg__(104)
       // TMA loads below then hit L2 instead of exposing DRAM latency per stage
       // fixed K order for every tile: a token's logits do not depend on its position in
       // the batch (chunked / micro-batched forwards route identically)
-      for (int kb = kRStages; kb < KB; ++kb) tma_prefetch_l2_2d(&tmap_x, kb * kRBK, row0);
+      // (issued after the first ring's loads, which would otherwise queue behind the prefetches)
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = 0; kb < KB; ++kb) {
+        if (kb == kRStages)
+          for (int kp = kRStages; kp < KB; ++kp) tma_prefetch_l2_2d(&tmap_x, kp * kRBK, row0);
         mbar_wait(&empty[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full[stage], kRA + b_bytes);
         tma_load_2d(smem_a + stage * kRA, &tmap_x, &full[stage], kb * kRBK, row0, pol_x);
@@ -163,6 +276,7 @@ __global__ void __maxnreg__(104)
       uint32_t phase = 0;
       for (int kb = 0; kb < KB; ++kb) {
         mbar_wait(&full[stage], phase);
+        if (kb == 0) HM_RSTAMP(1);
         tc_fence_after();
         const uint64_t a0 = make_sdesc_sw128(smem_u32(smem_a + stage * kRA));
         const uint64_t b0 = make_sdesc_sw128(smem_u32(smem_b + stage * kRBmax));
@@ -175,6 +289,7 @@ __global__ void __maxnreg__(104)
           phase ^= 1;
         }
       }
+      HM_RSTAMP(7);
       umma_commit(&tfull[0]);
     }
   } else {
@@ -190,8 +305,13 @@ __global__ void __maxnreg__(104)
     const bool valid = r < rows;
     const int64_t t = (int64_t)row0 + r;
     for (int i = etid; i < 4 * E_pad; i += kREpiWarps * 32) s_cnt[i] = 0;
+    // bias staged in shared memory: per-logit global loads behind per-element branches were
+    // serialised round trips (the part phase's largest cost)
+    for (int i = etid; i < E_pad; i += kREpiWarps * 32) s_bias[i] = (bias != nullptr && i < E) ? __ldg(bias + i) : 0.0f;
+    named_bar_sync(2, kREpiWarps * 32);
 
     mbar_wait(&tfull[0], 0);
+    if (etid == 0) HM_RSTAMP(2);
     tc_fence_after();
     const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16);
 
@@ -203,6 +323,247 @@ __global__ void __maxnreg__(104)
       ti[j] = 0x7fffffff;
     }
     const int nchunk = (E + 31) / 32;
+    float mx = -INFINITY, sum = 0.0f;
+    if constexpr (KMAX == 4 || KMAX == 8) {
+      // ---- 2 < k <= 8: selection on truncated 32-bit keys, made exact in the merge ----
+      // key = (order-preserving value bits & ~0xFF) | (255 - expert): a comparator is 2 instructions
+      // instead of 6 for the exact 64-bit (value, ~expert) key.  The truncation only matters for
+      // distinct logits that agree in their upper 24 bits (within 2^-16 relative): the merge
+      // re-sorts the selected experts by their exact keys and recomputes a row exactly when the
+      // k-th and (k+1)-th truncated keys share a value bucket (so the selected SET could differ).
+      // [128][32 * nchunk + 4] exact keys (every chunk stores all of its 32 columns)
+      uint32_t* s_u = reinterpret_cast<uint32_t*>(smem + kRPartBytes);
+      const int upitch = nchunk * 32 + 4;
+      uint32_t lst[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) lst[j] = 0u;
+      uint32_t ninth = 0u;
+      float pmx = -INFINITY, psum = 0.0f;
+      for (int c = part; c < nchunk; c += 4) {
+        uint32_t a[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, a);
+        tmem_ld_wait();
+        uint32_t key[32];
+        if (c * 32 + 32 <= E)
+          router_chunk<false>(a, s_bias + c * 32, 32, 255u - (uint32_t)(c * 32), pmx, psum, key);
+        else
+          router_chunk<true>(a, s_bias + c * 32, E - c * 32, 255u - (uint32_t)(c * 32), pmx, psum, key);
+        uint4* dst = reinterpret_cast<uint4*>(s_u + r * upitch + c * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = make_uint4(a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
+        uint32_t cn;
+        top8_of_32_u32(key, cn);
+        if (c == part) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) lst[j] = key[j];
+          ninth = cn;
+        } else {
+          merge8_u32(lst, ninth, key, cn);
+        }
+      }
+      // partials -> smem (aliases the drained pipeline stages): [part][field][row], fields
+      // 0 max, 1 sum-exp, 2..9 sorted truncated keys, 10 the 9th key
+      uint32_t* pu = reinterpret_cast<uint32_t*>(smem);
+      {
+        const int b = part * 11 * kRBM;
+        pu[b + r] = __float_as_uint(pmx);
+        pu[b + kRBM + r] = __float_as_uint(psum);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pu[b + (2 + j) * kRBM + r] = lst[j];
+        pu[b + 10 * kRBM + r] = ninth;
+      }
+      named_bar_sync(2, kREpiWarps * 32);
+      if (etid == 0) HM_RSTAMP(3);
+      // ---- merge, outputs and ranks on all 16 warps: 4 adjacent lanes per row ----
+      // (the partials are in shared memory, so rows no longer follow the TMEM lane quarters)
+      {
+        const int mr = etid >> 2;  // row of the tile
+        const int sub = etid & 3;  // part list it loads / output slots it writes
+        const bool mvalid = mr < rows;
+        uint32_t A[8], na;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) A[j] = pu[sub * 11 * kRBM + (2 + j) * kRBM + mr];
+        na = pu[sub * 11 * kRBM + 10 * kRBM + mr];
+        const float pm = __uint_as_float(pu[sub * 11 * kRBM + mr]);
+        const float ps = __uint_as_float(pu[sub * 11 * kRBM + kRBM + mr]);
+        // butterfly over the 4 lanes: every lane ends with the row's top-8 and 9th (merge8 is
+        // symmetric in its operands) and the row max
+        float m4 = pm;
+#pragma unroll
+        for (int sh = 1; sh <= 2; sh <<= 1) {
+          uint32_t B[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) B[j] = __shfl_xor_sync(0xffffffffu, A[j], sh);
+          const uint32_t nb = __shfl_xor_sync(0xffffffffu, na, sh);
+          merge8_u32(A, na, B, nb);
+          m4 = fmaxf(m4, __shfl_xor_sync(0xffffffffu, m4, sh));
+        }
+        mx = m4;
+        // sum-exp: every lane rescales its part's partial, pairwise butterfly adds (commutative,
+        // so all 4 lanes hold the bit-identical sum)
+        float sm = (pm == -INFINITY) ? 0.0f : __fmul_rn(ps, __expf(__fsub_rn(pm, mx)));
+#pragma unroll
+        for (int sh = 1; sh <= 2; sh <<= 1) sm = __fadd_rn(sm, __shfl_xor_sync(0xffffffffu, sm, sh));
+        sum = sm;
+        // the k-th and (k+1)-th truncated keys
+        uint32_t kth = 0u, nxt = na;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j == k - 1) kth = A[j];
+          if (j == k) nxt = A[j];
+        }
+        const uint32_t* urow = s_u + mr * upitch;
+        unsigned long long K[8];
+        if (nxt == 0u || (kth >> 8) != (nxt >> 8)) {
+          // every unselected expert is in a lower value bucket: the set is exact; exact keys
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            K[j] = 0ull;
+            if (j < k) {
+              const uint32_t id = 255u - (A[j] & 0xFFu);
+              K[j] = (static_cast<unsigned long long>(urow[id]) << 32) | (0xFFFFFFFFu - id);
+            }
+          }
+        } else {
+          // ambiguous bucket at the boundary: exact top-k over the experts whose value bucket is at
+          // least the k-th's (the selected higher buckets plus that bucket's members); the row's 4
+          // lanes each scan a quarter of it, then two 64-bit top-8 butterfly merges
+          const uint32_t bucket = kth >> 8;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) K[j] = 0ull;
+          const int q4 = (E + 15) / 16 * 4;  // quarter length, a multiple of 4
+          const int e_lo = sub * q4, e_hi = min(E, e_lo + q4);
+          for (int e4 = e_lo; e4 < e_hi; e4 += 4) {
+            const uint4 u4 = *reinterpret_cast<const uint4*>(urow + e4);
+            const uint32_t uu[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (e4 + i < e_hi && (uu[i] >> 8) >= bucket) {
+                unsigned long long cv =
+                    (static_cast<unsigned long long>(uu[i]) << 32) | (0xFFFFFFFFu - (uint32_t)(e4 + i));
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  if (cv > K[j]) {
+                    const unsigned long long tk = K[j];
+                    K[j] = cv;
+                    cv = tk;
+                  }
+                }
+              }
+            }
+          }
+          // all 4 lanes of the row take this branch together (their condition is the row's)
+#pragma unroll
+          for (int sh = 1; sh <= 2; sh <<= 1) {
+            unsigned long long O[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) O[j] = __shfl_xor_sync(0xFu << (lane & ~3), K[j], sh);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) K[j] = K[j] > O[7 - j] ? K[j] : O[7 - j];
+#pragma unroll
+            for (int s2 = 4; s2 > 0; s2 >>= 1)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if ((j & s2) == 0) ce_desc(K[j], K[j + s2]);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j >= k) K[j] = 0ull;
+        }
+        // lane sub owns selected entries j = sub, sub + 4: its exact slot is its rank among the k
+        // exact keys (order: value desc, expert asc)
+        float pw[2] = {0.0f, 0.0f};
+        int slot[2] = {0, 0}, sid[2] = {-1, -1};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = sub + 4 * h;
+          unsigned long long kj = 0ull;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i == j) kj = K[i];
+          int rk = 0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) rk += (K[i] > kj) ? 1 : 0;
+          if (j < k) {
+            slot[h] = rk;
+            sid[h] = static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(kj));
+            pw[h] = __fdiv_rn(__expf(__fsub_rn(unord_u32(static_cast<uint32_t>(kj >> 32)), mx)), sum);
+          }
+        }
+        if (renorm) {
+          // sum of the k probabilities in slot order (fixed order; the 4 lanes exchange them)
+          float ps_all = 0.0f;
+#pragma unroll
+          for (int sl = 0; sl < 8; ++sl) {
+            float v = 0.0f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (sid[h] >= 0 && slot[h] == sl) v = pw[h];
+            // exactly one lane of the row holds slot sl: a max-free OR of the 4 lanes' values
+            const uint32_t b = __float_as_uint(v);
+            const uint32_t b1 = b | __shfl_xor_sync(0xffffffffu, b, 1);
+            const uint32_t b2 = b1 | __shfl_xor_sync(0xffffffffu, b1, 2);
+            if (sl < k) ps_all = __fadd_rn(ps_all, __uint_as_float(b2));
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (sid[h] >= 0) pw[h] = __fdiv_rn(pw[h], ps_all);
+        }
+        const int64_t tm = (int64_t)row0 + mr;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (sid[h] >= 0) {
+            if (mvalid) {
+              topk_idx[tm * k + slot[h]] = sid[h];
+              topk_w[tm * k + slot[h]] = pw[h];
+            }
+            s_idx[mr * k + slot[h]] = mvalid ? sid[h] : -1;
+          }
+        }
+      }
+      // per-warp expert counts for the (token, slot)-order ranks: [16][E_pad] after s_u
+      int* s_c16 = reinterpret_cast<int*>(smem + kRPartBytes + (size_t)kRBM * upitch * 4);
+      for (int i = etid; i < kREpiWarps * E_pad; i += kREpiWarps * 32) s_c16[i] = 0;
+      named_bar_sync(2, kREpiWarps * 32);
+      if (etid == 0) HM_RSTAMP(4);
+      // rank pass: warp ew walks the assignments of rows 8ew..8ew+7 in (token, slot) order
+      const int abase = ew * 8 * k;
+      int lr[2] = {0, 0}, le[2] = {-1, -1};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c * 32 < 8 * k) {
+          const int a = c * 32 + lane;
+          const int e = (a < 8 * k) ? s_idx[abase + a] : -1;
+          const uint32_t mask = __match_any_sync(0xffffffffu, e);
+          const int cnt0 = (e >= 0) ? s_c16[ew * E_pad + e] : 0;
+          __syncwarp();
+          if (e >= 0 && lane == 31 - __clz(mask)) s_c16[ew * E_pad + e] = cnt0 + __popc(mask);
+          lr[c] = cnt0 + __popc(mask & lanemask_lt());
+          le[c] = e;
+          __syncwarp();
+        }
+      }
+      named_bar_sync(2, kREpiWarps * 32);
+      // exclusive prefix of the 16 warps' counts per expert; the tile histogram
+      for (int e = etid; e < E_pad; e += kREpiWarps * 32) {
+        int run = 0;
+#pragma unroll
+        for (int g = 0; g < kREpiWarps; ++g) {
+          const int v = s_c16[g * E_pad + e];
+          s_c16[g * E_pad + e] = run;
+          run += v;
+        }
+        if (e < E) tile_hist[(int64_t)tile * E + e] = run;
+      }
+      named_bar_sync(2, kREpiWarps * 32);
+      if (etid == 0) HM_RSTAMP(5);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int a = c * 32 + lane;
+        if (c * 32 < 8 * k && a < 8 * k && le[c] >= 0)
+          lrank[(int64_t)row0 * k + abase + a] = lr[c] + s_c16[ew * E_pad + le[c]];
+      }
+    } else {
     float vals[32];
     float lsum = 0.0f;
     // single pass per chunk: logits stay in registers for the partial sum-exp
@@ -224,8 +585,7 @@ __global__ void __maxnreg__(104)
         const int e = c * 32 + jj;
         float v = -INFINITY;
         if (e < E) {
-          v = __uint_as_float(a[jj]);
-          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
+          v = __fadd_rn(__uint_as_float(a[jj]), s_bias[e]);
         }
         a[jj] = __float_as_uint(v);
         mx = fmaxf(mx, v);
@@ -264,8 +624,7 @@ __global__ void __maxnreg__(104)
         const int e = c * 32 + jj;
         float v = -INFINITY;
         if (e < E) {
-          v = __uint_as_float(a[jj]);
-          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
+          v = __fadd_rn(__uint_as_float(a[jj]), s_bias[e]);
           float cv = v;
           int ci = e;
           bool ins = false;
@@ -303,8 +662,7 @@ __global__ void __maxnreg__(104)
         const int e = c * 32 + jj;
         float v = -INFINITY;
         if (e < E) {
-          v = __uint_as_float(a[jj]);
-          if (bias != nullptr) v = __fadd_rn(v, __ldg(bias + e));
+          v = __fadd_rn(__uint_as_float(a[jj]), s_bias[e]);
           float cv = v;
           int ci = e;
           bool ins = false;
@@ -345,12 +703,11 @@ __global__ void __maxnreg__(104)
       }
     }
     named_bar_sync(2, kREpiWarps * 32);
+    if (etid == 0) HM_RSTAMP(3);
     if (part == 0) {
     // merge: global max / sum-exp, and a 4-way merge of the sorted partial lists
-    float mx = -INFINITY;
 #pragma unroll
     for (int pp = 0; pp < 4; ++pp) mx = fmaxf(mx, pf[pp * nf * kRBM + r]);
-    float sum = 0.0f;
 #pragma unroll
     for (int pp = 0; pp < 4; ++pp) {
       const float pm = pf[pp * nf * kRBM + r];
@@ -382,6 +739,8 @@ __global__ void __maxnreg__(104)
         }
       }
     }
+    }  // part == 0 (merge)
+    if (part == 0) {
     float p[KMAX];
     float psum = 0.0f;
 #pragma unroll
@@ -403,6 +762,7 @@ __global__ void __maxnreg__(104)
       }
     }
     named_bar_sync(1, 128);
+    if (etid == 0) HM_RSTAMP(4);
 
     // rank pass: warp q walks its 32 rows' assignments in (token, slot) order
     const int base_a = q * 32 * k;
@@ -418,6 +778,7 @@ __global__ void __maxnreg__(104)
       __syncwarp();
     }
     named_bar_sync(1, 128);
+    if (etid == 0) HM_RSTAMP(5);
     if (valid) {
 #pragma unroll
       for (int j = 0; j < KMAX; ++j) {
@@ -433,10 +794,12 @@ __global__ void __maxnreg__(104)
       tile_hist[(int64_t)tile * E + e] =
           s_cnt[e] + s_cnt[E_pad + e] + s_cnt[2 * E_pad + e] + s_cnt[3 * E_pad + e];
     }  // part == 0
+    }  // k <= 2 or k > 8
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) HM_RSTAMP(6);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<256>(tmem_base);
@@ -498,7 +861,7 @@ __global__ void __launch_bounds__(kR2Threads)
   constexpr int RR = R < 32 ? 32 : R;
   constexpr int NG = (R + 31) / 32;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = align_smem_1024(smem_raw);
   const R2Layout L = r2_layout(C, E, E_pad, k, stages);
   const uint32_t stage_b = (uint32_t)E_pad * kRBK * 2;
   uint8_t* smem_a = smem;
@@ -840,6 +1203,10 @@ int launch_router(const void* x, const void* wg, const float* bias, int n_ranks,
 #undef HM_R2
   }
   const int stages = router_stages(E_pad);
+  // the 2 < k <= 8 epilogue reuses the drained ring for its partials and exact keys
+  if ((size_t)stages * (kRA + (size_t)E_pad * kRBK * 2) <
+      kRPartBytes + (size_t)kRBM * ((E + 31) / 32 * 32 + 4) * 4 + (size_t)kREpiWarps * E_pad * 4)
+    return set_error(HM_EINVAL, "router: pipeline ring too small for the epilogue scratch (E_pad %d)", E_pad);
   const size_t smem = 1024 + (size_t)stages * (kRA + (size_t)E_pad * kRBK * 2) + 256 + kREpiSmem;
 #define HM_LAUNCH_ROUTER(KM)                                                                                 \
   do {                                                                                                       \
@@ -858,3 +1225,17 @@ int launch_router(const void* x, const void* wg, const float* bias, int n_ranks,
 }
 
 }  // namespace hm
+
+#ifdef HM_ROUTER_STAMPS
+namespace hm {
+__global__ void debug_stamp_kernel(int slot) { g_rstamp[4095][slot] = gtimer(); }
+}  // namespace hm
+// one-thread kernel writing %globaltimer into g_rstamp[4095][slot] (launch-gap measurements)
+extern "C" __attribute__((visibility("default"))) int hm_debug_stamp(int slot, void* stream) {
+  hm::debug_stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(slot);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+extern "C" __attribute__((visibility("default"))) int hm_debug_router_stamps(void* out, int n_tiles) {
+  return cudaMemcpyFromSymbol(out, hm::g_rstamp, (size_t)n_tiles * 8 * sizeof(unsigned long long)) == cudaSuccess ? 0 : 1;
+}
+#endif
