@@ -326,6 +326,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K reg
     float mx = -INFINITY, sum = 0.0f;
     if constexpr (KMAX == 4 || KMAX == 8) {
       // ---- 2 < k <= 8: selection on truncated 32-bit keys, made exact in the merge ----
+      // (k <= 2 keeps the per-thread insertion below: measured faster for top-1/top-2)
       // key = (order-preserving value bits & ~0xFF) | (255 - expert): a comparator is 2 instructions
       // instead of 6 for the exact 64-bit (value, ~expert) key.  The truncation only matters for
       // distinct logits that agree in their upper 24 bits (within 2^-16 relative): the merge
@@ -593,7 +594,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K reg
       float cs = 0.0f;
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj)
-        if (c * 32 + jj < E) cs = __fadd_rn(cs, expf(__fsub_rn(__uint_as_float(a[jj]), mx)));
+        if (c * 32 + jj < E) cs = __fadd_rn(cs, ex2_ftz(__fmul_rn(__fsub_rn(__uint_as_float(a[jj]), mx), kLog2e)));
       lsum = cs;
       unsigned long long key[32];
 #pragma unroll
@@ -648,7 +649,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K reg
       float cs = 0.0f;
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj)
-        if (c * 32 + jj < E) cs = __fadd_rn(cs, expf(__fsub_rn(vals[jj], m)));
+        if (c * 32 + jj < E) cs = __fadd_rn(cs, ex2_ftz(__fmul_rn(__fsub_rn(vals[jj], m), kLog2e)));
       lsum = cs;
     }
     for (int c = part + 4; c < nchunk; c += 4) {
@@ -682,10 +683,10 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K reg
         vals[jj] = v;
       }
       const float m = tv[0];
-      float cs = (m_old == -INFINITY) ? 0.0f : __fmul_rn(lsum, expf(__fsub_rn(m_old, m)));
+      float cs = (m_old == -INFINITY) ? 0.0f : __fmul_rn(lsum, ex2_ftz(__fmul_rn(__fsub_rn(m_old, m), kLog2e)));
 #pragma unroll
       for (int jj = 0; jj < 32; ++jj)
-        if (c * 32 + jj < E) cs = __fadd_rn(cs, expf(__fsub_rn(vals[jj], m)));
+        if (c * 32 + jj < E) cs = __fadd_rn(cs, ex2_ftz(__fmul_rn(__fsub_rn(vals[jj], m), kLog2e)));
       lsum = cs;
     }
     // partials -> smem (aliases the drained pipeline stages): [part][field][row]
@@ -711,7 +712,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K reg
 #pragma unroll
     for (int pp = 0; pp < 4; ++pp) {
       const float pm = pf[pp * nf * kRBM + r];
-      if (pm != -INFINITY) sum = __fadd_rn(sum, __fmul_rn(pf[pp * nf * kRBM + kRBM + r], expf(__fsub_rn(pm, mx))));
+      if (pm != -INFINITY) sum = __fadd_rn(sum, __fmul_rn(pf[pp * nf * kRBM + kRBM + r], ex2_ftz(__fmul_rn(__fsub_rn(pm, mx), kLog2e))));
     }
     {
       int head[4] = {0, 0, 0, 0};
@@ -746,7 +747,7 @@ __global__ void __maxnreg__(96)  // 18 warps: 5 on one SMSP x 96 x 32 <= 16K reg
 #pragma unroll
     for (int j = 0; j < KMAX; ++j) {
       if (j < k) {
-        p[j] = __fdiv_rn(expf(__fsub_rn(tv[j], mx)), sum);
+        p[j] = __fdiv_rn(ex2_ftz(__fmul_rn(__fsub_rn(tv[j], mx), kLog2e)), sum);
         psum = __fadd_rn(psum, p[j]);
       }
     }

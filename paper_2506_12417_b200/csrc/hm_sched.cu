@@ -431,8 +431,10 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
   int* s_ne = s_cnt + GE + 1; // [E]
   int* s_nsrc = s_ne + E;     // [E]
   int* s_ord = s_nsrc + E;    // [E]
-  unsigned long long* s_key =  // [GE] plan-order keys (8-byte aligned)
-      reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_ord + E) + 7) & ~uintptr_t(7));
+  // [GE] plan-order keys, 8-byte aligned by pointer arithmetic on the shared array (an integer
+  // round trip would drop the shared address space: generic loads in the rank loops)
+  unsigned long long* s_key =
+      reinterpret_cast<unsigned long long*>(s_ord + E + ((smem_u32(s_ord + E) & 4u) ? 1 : 0));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
 
   if (mode == HM_LAYOUT_LOCAL) {
@@ -756,8 +758,8 @@ __global__ void __launch_bounds__(kPlanThreads)
   int* s_m = s_dyn;                 // [E]
   int* s_base = s_m + E;            // [E + 1] expert-major row starts
   int* s_cnt = s_base + E + 1;      // [E + 1] 128-row tiles per segment, plan order
-  unsigned long long* s_key =       // [E] plan-order keys (8-byte aligned)
-      reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_cnt + E + 1) + 7) & ~uintptr_t(7));
+  unsigned long long* s_key =       // [E] plan-order keys (8-byte aligned, shared address space kept)
+      reinterpret_cast<unsigned long long*>(s_cnt + E + 1 + ((smem_u32(s_cnt + E + 1) & 4u) ? 1 : 0));
   const int tid = threadIdx.x;
   if (tid == 0) g_phase_ns[0] = globaltimer_ns();
   dev_hist_reduce(tile_hist, 1, tpr, E, s_m, m_out, tile_off, s_part);
