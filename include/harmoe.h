@@ -29,6 +29,7 @@
  *                       model engine.py:128-132)
  *   hm_fetch_expert(s)  async expert fetch (engine.py:253-265)
  *   hm_combine          Alg.1 step 6 gather + reconstruct
+ *   hm_grouped_gemm_combine  steps 5 (FFN2) + 6 fused: the combine runs in the FFN2 epilogue
  *   hm_ep_offsets, hm_dispatch_push, hm_grouped_gemm_remote, hm_stream_signal/wait,
  *   hm_ipc_*            expert parallelism over NVSwitch peer memory: the metadata exchange
  *                       and the scatter / gather all-to-alls of engine.py:328-375
@@ -227,6 +228,20 @@ HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t
                     const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue, void* out, const int32_t* row_map,
                     const int32_t* a_gather, int a_gather_div, const int32_t* slot_ready, int ready_from_slot,
                     int epoch, int32_t* slot_done, const hm_fetch_plan* fetch, void* stream);
+
+/*
+ * FFN2 with the weighted combine (K7) fused into its epilogue (LOCAL layout, Alg. 1 steps 5-6,
+ * PAPER.md:613-616): the STORE epilogue scatters expert row r to Y row row_map[r] = t*k + j as
+ * hm_grouped_gemm does, and the k-th arriving row of every (token t, 64-column chunk) computes
+ *   y[t, chunk] = (residual[t, chunk] +) sum_{j<k} topk_w[t, j] * Y[t*k + j, chunk]
+ * in fp32 in slot order - bit-identical to hm_combine(Y, NULL, topk_w, ...) after hm_grouped_gemm.
+ *   counters [T * N/64] uint32, zero before the first call; every call leaves them zero again.
+ *   residual [T, N] bf16 or NULL; y [T, N] bf16.  Requires 1 <= k <= 32.
+ */
+HM_API int hm_grouped_gemm_combine(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                                   const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, void* Y,
+                                   const int32_t* row_map, const float* topk_w, int k, const void* residual, void* y,
+                                   uint32_t* counters, void* stream);
 
 /*
  * Async expert fetch (K6): copy `bytes` from src (peer HBM through UVA/NVLink, or pinned host

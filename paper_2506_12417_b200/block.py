@@ -68,6 +68,13 @@ class MoEConfig:
     # of it (False: the synchronous-loading ablation, engine.py:266-269)
     async_fetch: bool = True
     residual: bool = False  # decoder-layer residual y = x + MoE(x), fused into the combine kernel
+    # LOCAL mode: run the weighted combine inside the FFN2 epilogue (hm_grouped_gemm_combine:
+    # the k-th arriving row of each token chunk combines it; bit-identical output) instead of
+    # a separate combine kernel.  Off by default: measured 820 us for the fused FFN2 vs 351 + 98 us
+    # separately at Qwen-128 (the epilogue waits on its arrival atomics, fences and the other
+    # rows' DRAM reads every tile, which stalls the MMA pipeline; profiles/r2_experiments.txt).
+    # HM_FUSED_COMBINE=0/1 overrides.
+    fused_combine: bool = False
     # EP mode: "nccl" (all_to_all_single; split sizes need S on the host once per layer) or "p2p"
     # (one-sided pushes into peers' buffers over NVLink/NVSwitch, no host round trip)
     transport: str = "nccl"
@@ -406,19 +413,41 @@ class HarMoEnyBlock:
                 st["h"] = ops.grouped_gemm(st["xs"], self.w_in, self.n_in, st["plan"].layout, self.epi_in,
                                            stream=s)
 
+        fuse_comb = self.uses_fused_combine()
+
         def gemm2():
             # FFN2 scatters its rows token-major (row_map = inverse permutation) so the
             # combine reads each token's k expert outputs as one contiguous block
-            st["ys"] = ops.grouped_gemm(st["h"], self.w_out, cfg.d_model, st["plan"].layout, ops.HM_EPI_STORE,
-                                        row_map=st["inv"], stream=s)
+            if fuse_comb:
+                st["ys"], st["y"] = ops.grouped_gemm_combine(
+                    st["h"], self.w_out, cfg.d_model, st["plan"].layout, st["inv"], st["w"],
+                    self._combine_counters(T), residual=st["x"] if cfg.residual else None, stream=s)
+            else:
+                st["ys"] = ops.grouped_gemm(st["h"], self.w_out, cfg.d_model, st["plan"].layout, ops.HM_EPI_STORE,
+                                            row_map=st["inv"], stream=s)
 
         def combine():
-            st["y"] = ops.combine(st["ys"], None, st["w"], residual=st["x"] if cfg.residual else None, stream=s)
+            if not fuse_comb:  # (fused: the FFN2 epilogue already wrote y)
+                st["y"] = ops.combine(st["ys"], None, st["w"], residual=st["x"] if cfg.residual else None, stream=s)
 
         return [("router", router), ("schedule", plan), ("permute", permute), ("gemm1", gemm1),
                 ("gemm2", gemm2), ("combine", combine)]
 
-    KERNELS_PER_FORWARD = 6  # router, plan, permute, gemm1, gemm2, combine
+    @property
+    def KERNELS_PER_FORWARD(self) -> int:  # router, plan, permute, gemm1, gemm2 (+ combine unless fused)
+        return 5 if self.uses_fused_combine() else 6
+
+    def uses_fused_combine(self) -> bool:
+        env = os.environ.get("HM_FUSED_COMBINE")
+        return (env == "1") if env is not None else self.cfg.fused_combine
+
+    def _combine_counters(self, T: int) -> torch.Tensor:
+        """Arrival counters of the fused combine, [T * d/64] int32; they return to zero after every
+        forward, so one zeroed allocation (grown with the largest batch) serves every call."""
+        n = T * (self.cfg.d_model // 64)
+        if getattr(self, "_comb_ctr", None) is None or self._comb_ctr.numel() < n:
+            self._comb_ctr = torch.zeros(n, dtype=torch.int32, device=self.device)
+        return self._comb_ctr
 
     def capture(self, num_tokens: int, groups=(("router", "schedule", "permute"), ("gemm1",), ("gemm2",),
                                                ("combine",)), x_static: torch.Tensor | None = None,

@@ -539,7 +539,8 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
                              int ready_from_slot, int epoch, const __nv_bfloat16* __restrict__ a_src,
                              const int* __restrict__ a_gather, int a_gather_div, int a_src_rows,
                              const unsigned long long* __restrict__ out_ptrs, const int* __restrict__ out_split,
-                             int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan, int tail_split) {
+                             int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan, int tail_split,
+                             const CombineFuse cf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   if (fplan.pairs > 0 && (int)(blockIdx.x >> 1) >= (int)(gridDim.x >> 1) - fplan.pairs) {
@@ -884,6 +885,82 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         }
         __syncwarp();
       }
+      if (kEpi == kEpiStore && cf.y != nullptr) {
+        // fused combine: this warp's rows are stored for columns [nb*256 + ocol0, + ncols); each
+        // (token, 64-column chunk) counts its k expert rows and the k-th arrival combines the
+        // chunk in slot order - the arithmetic of combine_dense_kernel, so the output is
+        // bit-identical to the separate combine.  Stores -> fence -> count (the last arriver
+        // fences again before reading the other rows through L2).
+        __threadfence();
+        __syncwarp();
+        const int kk = cf.k;
+        const int nchk = ldo / 64;
+        const int c64_0 = (nb * kOutCols + ocol0) / 64;
+        const int tok = valid ? (int)(row / kk) : 0;
+        for (int ch = 0; ch < ncols / 64; ++ch) {
+          bool lastarr = false;
+          if (valid)
+            lastarr = atomicInc(cf.counters + (int64_t)tok * nchk + c64_0 + ch, (unsigned)(kk - 1)) ==
+                      (unsigned)(kk - 1);
+          uint32_t m = __ballot_sync(0xffffffffu, lastarr);
+          if (m != 0u) __threadfence();
+          while (m != 0u) {
+            // up to 4 finished chunks per round, 8 lanes x 16 B per 64-column chunk
+            uint32_t mm = m;
+            int src = -1;
+            for (int g = 0; g <= (lane >> 3); ++g) {
+              src = (mm != 0u) ? __ffs(mm) - 1 : -1;
+              mm &= mm - 1u;
+            }
+#pragma unroll
+            for (int g = 0; g < 4; ++g) m &= m - 1u;
+            const int t_c = __shfl_sync(0xffffffffu, tok, src < 0 ? 0 : src);
+            if (src >= 0) {
+              const int col = (c64_0 + ch) * 64 + (lane & 7) * 8;
+              const __nv_bfloat16* yb = out + (int64_t)t_c * kk * ldo + col;
+              float acc[8];
+              if (cf.residual != nullptr) {
+                const uint4 rv = ld_global_nc_v4(reinterpret_cast<const __nv_bfloat16*>(cf.residual) +
+                                                 (int64_t)t_c * ldo + col);
+                const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  acc[2 * h] = bf16lo(rr[h]);
+                  acc[2 * h + 1] = bf16hi(rr[h]);
+                }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 8; ++h) acc[h] = 0.0f;
+              }
+              for (int j0 = 0; j0 < kk; j0 += 4) {
+                uint4 u4[4];
+                float wj[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  if (j0 + jj < kk) {
+                    u4[jj] = ld_global_cg_v4(yb + (int64_t)(j0 + jj) * ldo);
+                    wj[jj] = __ldg(cf.w + (int64_t)t_c * kk + j0 + jj);
+                  }
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  if (j0 + jj < kk) {
+                    const uint32_t uu[4] = {u4[jj].x, u4[jj].y, u4[jj].z, u4[jj].w};
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                      acc[2 * h] = __fadd_rn(acc[2 * h], __fmul_rn(wj[jj], bf16lo(uu[h])));
+                      acc[2 * h + 1] = __fadd_rn(acc[2 * h + 1], __fmul_rn(wj[jj], bf16hi(uu[h])));
+                    }
+                  }
+                }
+              }
+              st_global_v4(reinterpret_cast<__nv_bfloat16*>(cf.y) + (int64_t)t_c * ldo + col,
+                           pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                           pack_bf16x2(acc[6], acc[7]));
+            }
+          }
+        }
+      }
       // K6 slot reuse: this warp is done with the tile, so its weight loads (TMA, consumed by
       // the MMAs before tfull fired) are complete; a fetch may overwrite a fetched expert's
       // cache slot once all 16 epilogue warps of all its tiles have counted here
@@ -992,7 +1069,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
                         const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
                         const unsigned long long* out_ptrs, const int32_t* out_split, int n_out, int32_t* slot_done,
-                        const hm_fetch_plan* fetch) {
+                        const hm_fetch_plan* fetch, const CombineFuse* combine) {
   if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
     return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
@@ -1015,6 +1092,14 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
       return set_error(HM_EINVAL, "grouped_gemm: incomplete fetch plan");
     const cudaError_t me = cudaMemsetAsync(fplan.counters, 0, sizeof(int32_t) * fplan.n_counters, stream);
     if (me != cudaSuccess) return set_error(HM_ECUDA, "grouped_gemm fetch counters: %s", cudaGetErrorString(me));
+  }
+  CombineFuse cf = {};
+  if (combine != nullptr && combine->y != nullptr) {
+    cf = *combine;
+    if (epilogue != kEpiStore || row_map == nullptr || out_ptrs != nullptr || out == nullptr || !use_2cta() ||
+        cf.w == nullptr || cf.counters == nullptr || cf.k < 1 || cf.k > 32 || N % 64 != 0)
+      return set_error(HM_EINVAL, "grouped_gemm: the fused combine needs the STORE epilogue with a token-major "
+                                  "row map, local output, weights, counters and 1 <= k <= 32");
   }
   if (a_rows <= 0) return HM_OK;
   CUtensorMap ta, tb;
@@ -1041,7 +1126,9 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     // 64-row weight boxes: SwiGLU half tiles, and the 128-column units of the tail split
     rc = make_tmap_2d_bf16(&tb64, W, (uint64_t)w_rows, (uint64_t)K, kBN / 4, kBK);
     if (rc) return rc;
-    const int tail_split = (epilogue != kEpiSwiGLU && slot_done == nullptr && use_tail_split()) ? 1 : 0;
+    // (not with the fused combine: its 64-column chunk counters assume >= 64-column warp spans)
+    const int tail_split =
+        (epilogue != kEpiSwiGLU && slot_done == nullptr && cf.y == nullptr && use_tail_split()) ? 1 : 0;
     const bool gather = a_gather != nullptr;
     // every pair resident at once (static tile walk; the fetch pairs and the compute pairs wait
     // on each other); fetch pairs come out of the same budget
@@ -1068,7 +1155,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, ta64, tb64, half_tiles, s4,          \
                            mtile_prefix, n_seg, o, N, K,                                                          \
                            ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
-                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan, tail_split);                \
+                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan, tail_split, cf);            \
   } while (0)
     switch (epilogue * 2 + (gather ? 1 : 0)) {
       case kEpiStore * 2: HM_GEMM2(kEpiStore, false); break;
@@ -1083,6 +1170,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     if (e != cudaSuccess) return set_error(HM_ECUDA, "grouped_gemm (2-CTA) launch: %s", cudaGetErrorString(e));
     return check_launch("grouped_gemm_2cta");
   }
+  if (cf.y != nullptr) return set_error(HM_EINVAL, "grouped_gemm: the fused combine needs the 2-CTA kernel");
 #define HM_GEMM(EPI)                                                                                         \
   do {                                                                                                       \
     cudaFuncSetAttribute(grouped_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem); \

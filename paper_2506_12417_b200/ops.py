@@ -252,6 +252,29 @@ def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=
     return out
 
 
+def grouped_gemm_combine(H, W, N: int, layout: "Layout", row_map, topk_w, counters, Y=None, y=None, residual=None,
+                         stream=None):
+    """K5 (FFN2, STORE epilogue, token-major scatter through row_map) with K7 fused into the
+    epilogue: returns (Y [T*k, N], y [T, N]) where y = (residual +) sum_j w[t,j] Y[t*k+j] is
+    bit-identical to combine(Y, None, topk_w, residual=residual).  counters: int32 [T * N/64],
+    zero before the first call (every call leaves them zero)."""
+    _require_cuda(H, W, row_map, topk_w, counters, residual, Y, y)
+    _require_dtype(torch.bfloat16, H, W, Y, y, residual, what="grouped_gemm_combine operands")
+    _require_dtype(torch.float32, topk_w, what="combine weights")
+    _require_dtype(torch.int32, row_map, counters, what="grouped_gemm_combine index tensors")
+    T, k = topk_w.shape
+    if counters.numel() < T * (N // 64):
+        raise ValueError("grouped_gemm_combine: counters must hold T * N/64 entries")
+    if Y is None:
+        Y = torch.empty((max(T * k, 1), N), dtype=torch.bfloat16, device=H.device)
+    if y is None:
+        y = torch.empty((T, N), dtype=torch.bfloat16, device=H.device)
+    _lib.call("hm_grouped_gemm_combine", _ptr(H), H.shape[0], _ptr(W), W.shape[0], N, H.shape[1], _ptr(layout.segs),
+              _ptr(layout.n_seg), _ptr(layout.mtile_prefix), _ptr(Y), _ptr(row_map), _ptr(topk_w), k,
+              _ptr(residual), _ptr(y), _ptr(counters), _stream(stream))
+    return Y, y
+
+
 def fetch_plan(fetch, n_fetch, src_in, src_out, dst_in, dst_out, in_bytes: int, out_bytes: int, first_slot: int,
                n_slots: int, ready_in, ready_out, counters, value: int, phase: int, pairs: int = 2):
     """hm_fetch_plan for the K6 fetch pairs of a grouped-GEMM launch (bounded expert cache):

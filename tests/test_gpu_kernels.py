@@ -517,3 +517,38 @@ def test_config_rejects_untileable_shapes():
         MoEConfig(d_model=256, d_ff=128, num_experts=8, top_k=1, activation="relu")
     with pytest.raises(ValueError, match="top_k"):
         MoEConfig(d_model=256, d_ff=256, num_experts=4, top_k=5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,f,E,k,act,T,G,residual", [
+    (256, 256, 32, 4, "swiglu", 256, 2, False),
+    (512, 256, 16, 8, "swiglu", 1000, 1, True),    # ragged segments, half tiles, residual
+    (768, 512, 64, 1, "relu", 640, 4, False),     # top-1 (every row is the last arrival)
+    (512, 256, 8, 2, "swiglu", 2048, 2, True),    # top-2, few large experts
+    (2048, 768, 128, 8, "swiglu", 4096, 1, False),  # Qwen-128 shape
+])
+def test_fused_combine_bit_identical(d, f, E, k, act, T, G, residual):
+    """hm_grouped_gemm_combine: the combine run by the k-th arriving row of each (token,
+    64-column chunk) in the FFN2 epilogue gives the same bits as FFN2 + the separate combine
+    kernel, and leaves its arrival counters at zero (two forwards in a row agree too)."""
+    import os
+
+    from paper_2506_12417_b200.block import HarMoEnyBlock, MoEConfig
+
+    dev = _cuda()
+    cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, logical_ranks=G, eq_tokens=4,
+                    residual=residual, placement="blocked", fused_combine=True)
+    blk = HarMoEnyBlock.random(cfg, seed=7, device=dev, zipf_s=1.0, std=0.05)
+    x = torch.randn((T, d), device=dev, generator=torch.Generator(device=dev).manual_seed(3)).to(torch.bfloat16)
+    os.environ["HM_FUSED_COMBINE"] = "0"
+    try:
+        y_ref = blk(x).clone()
+    finally:
+        os.environ.pop("HM_FUSED_COMBINE", None)
+    assert blk.uses_fused_combine() and blk.KERNELS_PER_FORWARD == 5
+    y1 = blk(x).clone()
+    y2 = blk(x).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(y1.view(torch.int16), y_ref.view(torch.int16))
+    assert torch.equal(y2.view(torch.int16), y_ref.view(torch.int16))
+    assert int(blk._comb_ctr.abs().sum().item()) == 0
