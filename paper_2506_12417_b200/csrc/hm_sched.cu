@@ -47,6 +47,23 @@ int read_plan_phases(long long* out8) {
   return HM_OK;
 }
 
+// diagnostics build only (-DHM_PLAN_STAMPS, tools/plan_clocks.py): clock64 at block-wide barriers
+#ifdef HM_PLAN_STAMPS
+__device__ long long g_pclk[16];
+#define HM_PSTAMP(i)                                   \
+  do {                                                 \
+    __syncthreads();                                   \
+    if (threadIdx.x == 0) g_pclk[i] = clock64();       \
+  } while (0)
+extern "C" __attribute__((visibility("default"))) int hm_debug_plan_clocks(long long* out16) {
+  return cudaMemcpyFromSymbol(out16, g_pclk, sizeof(long long) * 16) == cudaSuccess ? 0 : 1;
+}
+#else
+#define HM_PSTAMP(i) \
+  do {               \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void warp_argmax_ll(long long& v, int& i) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -274,6 +291,7 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
     }
   }
   __syncthreads();
+  HM_PSTAMP(2);
 
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -332,6 +350,7 @@ __device__ void dev_schedule(int* S, bool init_from_m, const int* m_all, const i
     if (loads_out != nullptr && lane < G) loads_out[lane] = (int)t;
   }
   __syncthreads();
+  HM_PSTAMP(3);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -436,6 +455,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
   unsigned long long* s_key =
       reinterpret_cast<unsigned long long*>(s_ord + E + ((smem_u32(s_ord + E) & 4u) ? 1 : 0));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nt = blockDim.x;
+  HM_PSTAMP(4);
 
   if (mode == HM_LAYOUT_LOCAL) {
     for (int i = tid; i < GE; i += nt) {
@@ -474,6 +494,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
     }
     __syncthreads();
     if (tid == 0) g_phase_ns[4] = globaltimer_ns();
+    HM_PSTAMP(5);
     for (int i = tid; i < E * G; i += nt) {
       const int e = i / G, d = i - (i / G) * G;
       int run = s_base[d] + s_off[d * E + e];
@@ -487,6 +508,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       s_key[i] = plan_key(home[e] == d, s_n[i], e);
     }
     __syncthreads();
+    HM_PSTAMP(6);
     // one thread per (dest, expert): rank = number of smaller plan keys of that dest (the dest's
     // keys are read as shared-memory broadcasts: a warp's 32 entries share d when E >= 32)
     for (int p = tid; p < GE; p += nt) {
@@ -504,8 +526,10 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
     }
     __syncthreads();
     if (tid == 0) g_phase_ns[5] = globaltimer_ns();
+    HM_PSTAMP(7);
     block_scan_to(s_cnt, s_nnz[G], o.mprefix, s_tmp);
     if (tid == 0) g_phase_ns[6] = globaltimer_ns();
+    HM_PSTAMP(8);
     return;
   }
 
@@ -523,6 +547,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       s_off[i] = sum;
     }
     __syncthreads();
+    HM_PSTAMP(5);
     if (w < G) warp_exclusive_scan(s_off + w * E, E, lane);
     if (tid == 0) {
       s_scal[0] = 0;  // residents with work
@@ -549,6 +574,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       }
     }
     __syncthreads();
+    HM_PSTAMP(6);
     const int n_res_work = s_scal[0], n_home = s_scal[1], n_work = s_scal[2];
     for (int e = w; e < E; e += nt / 32) {
       const unsigned long long key = s_key[e];
@@ -574,7 +600,9 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       *o.n_fetch = n_work - n_res_work;
     }
     __syncthreads();
+    HM_PSTAMP(7);
     block_scan_to(s_cnt, n_work, o.mprefix, s_tmp);
+    HM_PSTAMP(8);
     return;
   }
 
@@ -705,6 +733,294 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
 }
 
 // ------------------------------------------------------------------------------------------
+// fast planner path (plan_kernel): every count < 2^21, policy harmony / none, LOCAL or EP_EXPERT
+// layout.  S is kept only transposed, St[g][d][e] (experts on consecutive words), built straight
+// from m_all and home; flows and loads are 32-bit.  Same decisions and outputs as dev_schedule +
+// dev_layout (bit-exact on the same fixtures): measured with clock64 stamps, the S[g][e][d]
+// reads of the general path (G-way bank conflicts: lanes stride G words), its S zero-fill and the
+// per-expert serial home-slot count were most of the planner's time.
+// ------------------------------------------------------------------------------------------
+// rebalance on St / F32 (F32[g*32+d] = sum_e St[g][d][e]); kNch = E/32 chunks per lane, 0 = any E
+template <int kNch>
+__device__ int rebalance_t(int* St, int* F, int G, int E, int Ep, int q, int lane, int& t_lane, int t_avg) {
+  int t = t_lane;
+  int iters = 0;
+  for (;;) {
+    if (__ballot_sync(0xffffffffu, lane < G && t > t_avg) == 0u) break;
+    // argmin t does not depend on the rest of the iteration: reduce it alongside argmax t
+    const unsigned kmin = __reduce_min_sync(0xffffffffu, lane < G ? ((unsigned)t << 5) | lane : 0xffffffffu);
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, lane < G ? ((unsigned)t << 5) | (31u - lane) : 0u);
+    const int g_max = 31 - (int)(kmax & 31u);
+    const unsigned kf =
+        __reduce_max_sync(0xffffffffu, lane < G ? ((unsigned)F[lane * 32 + g_max] << 5) | (31u - lane) : 0u);
+    const int g_from = 31 - (int)(kf & 31u);
+    const int* col = St + (g_from * G + g_max) * Ep;
+    unsigned kb = 0u;
+    if (kNch > 0) {
+#pragma unroll
+      for (int c = 0; c < kNch; ++c) {
+        const int e = c * 32 + lane;
+        kb = max(kb, ((unsigned)col[e] << 10) | (1023u - e));
+      }
+    } else {
+      for (int e = lane; e < E; e += 32) kb = max(kb, ((unsigned)col[e] << 10) | (1023u - e));
+    }
+    kb = __reduce_max_sync(0xffffffffu, kb);
+    const int t_move = (int)(kb >> 10);
+    const int e_max = 1023 - (int)(kb & 1023u);
+    if (t_move < q) break;
+    const int g_min = (int)(kmin & 31u);
+    const int vmin = (int)(kmin >> 5);
+    if (g_min == g_max || (long long)vmin + q > t_avg) break;
+    const int t_s = min(t_move, t_avg - vmin);
+    if (lane == 0) {
+      St[(g_from * G + g_max) * Ep + e_max] -= t_s;
+      St[(g_from * G + g_min) * Ep + e_max] += t_s;
+      F[g_from * 32 + g_max] -= t_s;
+      F[g_from * 32 + g_min] += t_s;
+    }
+    if (lane == g_max) t -= t_s;
+    if (lane == g_min) t += t_s;
+    __syncwarp();
+    ++iters;
+  }
+  t_lane = t;
+  return iters;
+}
+
+// Thread mapping of the fast path's per-(dest, expert) passes: G is a power of two dividing the
+// block, so thread t owns dest d = t % G for the whole kernel and strides the experts by
+// blockDim / G - no integer divisions, [g][e][d]-ordered global stores are coalesced, and with
+// every [.][e] row padded to Ep = E + 32/G words a warp's (e, d) reads hit 32 distinct banks.
+struct DestLanes {
+  int d, e0, step;
+};
+__device__ __forceinline__ DestLanes dest_lanes(int G) {
+  const int lg = 31 - __clz(G);
+  return DestLanes{(int)(threadIdx.x & (G - 1)), (int)(threadIdx.x >> lg), (int)(blockDim.x >> lg)};
+}
+
+// initial_assign + rebalance into St[g][d][e] (rows of Ep words); S_out[g][e][d] written from St
+__device__ void dev_schedule_t(int* St, int Ep, int* F, const int* m, const int* home, int G, int E, int q,
+                               int rebalance, int32_t* __restrict__ S_out, int32_t* iters_out, int32_t* loads_out) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = blockDim.x >> 5;
+  // initial_assign (policies.py:109-117): bucket (g, e) starts on home[e]; flows F[g][d] on the fly
+  for (int row = w; row < G * G; row += nw) {
+    const int g = row >> (31 - __clz(G)), d = row & (G - 1);
+    int f = 0;
+    for (int e = lane; e < E; e += 32) {
+      const int v = (home[e] == d) ? m[g * E + e] : 0;
+      St[row * Ep + e] = v;
+      f += v;
+    }
+    f = (int)__reduce_add_sync(0xffffffffu, (unsigned)f);
+    if (lane == 0) F[g * 32 + d] = f;
+  }
+  __syncthreads();
+  HM_PSTAMP(2);
+  if (w == 0) {
+    int t = 0;
+    if (lane < G)
+      for (int g = 0; g < G; ++g) t += F[g * 32 + lane];
+    const int total = (int)__reduce_add_sync(0xffffffffu, (unsigned)t);  // lanes >= G hold 0
+    const int t_avg = total / G;
+    int iters = 0;
+    if (rebalance == HM_POLICY_REBALANCE) {
+      if (E == 128)
+        iters = rebalance_t<4>(St, F, G, E, Ep, q, lane, t, t_avg);
+      else if (E == 64)
+        iters = rebalance_t<2>(St, F, G, E, Ep, q, lane, t, t_avg);
+      else if (E == 256)
+        iters = rebalance_t<8>(St, F, G, E, Ep, q, lane, t, t_avg);
+      else
+        iters = rebalance_t<0>(St, F, G, E, Ep, q, lane, t, t_avg);
+    }
+    if (lane == 0 && iters_out != nullptr) *iters_out = iters;
+    if (loads_out != nullptr && lane < G) loads_out[lane] = t;
+  }
+  __syncthreads();
+  HM_PSTAMP(3);
+  const DestLanes L = dest_lanes(G);
+  for (int g = 0; g < G; ++g) {
+    const int* row = St + (g * G + L.d) * Ep;
+    for (int e = L.e0; e < E; e += L.step) S_out[(g * E + e) * G + L.d] = row[e];
+  }
+}
+
+// plan-order key in 32 bits (counts < 2^21, E <= 1024): residents first, then more tokens, then
+// lower expert id (engine.py:233-234); experts without work sort last.  Same order as plan_key.
+__device__ __forceinline__ unsigned plan_key32(bool resident, int n, int e) {
+  if (n <= 0) return 0xffffffffu;
+  return ((resident ? 0u : 1u) << 31) | ((unsigned)((1 << 21) - 1 - n) << 10) | (unsigned)e;
+}
+
+// fast-path layout scratch (ints): s_n, s_off [G][Ep], s_cnt [G*E + 1], s_key [G][Ep] (+3 for
+// 16-byte alignment), s_hr [E]
+constexpr int fast_layout_scratch_ints(int G, int E) { return 3 * G * (E + 32 / G) + G * E + 1 + 3 + E; }
+constexpr int plan_scratch_ints(int G, int E) {
+  return layout_scratch_ints(G, E) > fast_layout_scratch_ints(G, E) ? layout_scratch_ints(G, E)
+                                                                     : fast_layout_scratch_ints(G, E);
+}
+
+// LOCAL / EP_EXPERT layouts from St (same outputs as dev_layout)
+__device__ void dev_layout_t(const int* St, int Ep, const int* home, int G, int E, int mode, int me, LayoutOut o,
+                             int* scratch) {
+  __shared__ int s_base[33];
+  __shared__ int s_nnz[33];
+  __shared__ int s_tmp[32];
+  __shared__ int s_scal[4];
+  const int GE = G * E;
+  int* s_n = scratch;            // n[d][e] = rows of expert e on dest d (rows of Ep)
+  int* s_off = s_n + G * Ep;     // exclusive scan of n[d][.] over experts (rows of Ep)
+  int* s_cnt = s_off + G * Ep;   // [GE + 1] 128-row tiles per segment (plan order)
+  // [G][Ep] plan-order keys, 16-byte aligned for the vector rank loads (pointer arithmetic on the
+  // shared array keeps the shared address space)
+  int* key_base = s_cnt + GE + 1;
+  unsigned* s_key = reinterpret_cast<unsigned*>(key_base + ((4u - ((smem_u32(key_base) >> 2) & 3u)) & 3u));
+  int* s_hr = reinterpret_cast<int*>(s_key + G * Ep);  // [E] EP: home-slot rank
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const DestLanes L = dest_lanes(G);
+  const bool local = mode == HM_LAYOUT_LOCAL;
+  HM_PSTAMP(4);
+  for (int e = L.e0; e < E; e += L.step) {
+    int sum = 0;
+    for (int g = 0; g < G; ++g) sum += St[(g * G + L.d) * Ep + e];
+    s_n[L.d * Ep + e] = sum;
+    s_off[L.d * Ep + e] = sum;
+    if (local) s_key[L.d * Ep + e] = plan_key32(home[e] == L.d, sum, e);
+  }
+  if (!local) {  // home-slot rank of every expert: ballots over warp chunks
+    for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+      const int e = e0 + tid;
+      const bool mine = e < E && home[e] == me;
+      const unsigned mask = __ballot_sync(0xffffffffu, mine);
+      if (lane == 0) s_tmp[w] = __popc(mask);
+      __syncthreads();
+      if (e < E) {
+        int r = e0 > 0 ? s_hr[e0 - 1] + (home[e0 - 1] == me) : 0;
+        for (int w2 = 0; w2 < w; ++w2) r += s_tmp[w2];
+        s_hr[e] = r + __popc(mask & ((1u << lane) - 1u));
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  HM_PSTAMP(5);
+  if (w < G) {
+    const int total = warp_exclusive_scan(s_off + w * Ep, E, lane);
+    int nz = 0;
+    for (int e = lane; e < E; e += 32) nz += (s_n[w * Ep + e] > 0);
+    nz = (int)__reduce_add_sync(0xffffffffu, (unsigned)nz);
+    if (lane == 0) {
+      s_base[w] = total;
+      s_nnz[w] = nz;
+    }
+  }
+  if (tid == 0) {
+    s_scal[0] = 0;  // residents with work (EP)
+    s_scal[1] = 0;  // home experts (EP)
+    s_scal[2] = 0;  // experts with work (EP)
+  }
+  if (!local) {
+    for (int e = tid; e < E; e += blockDim.x) s_key[e] = plan_key32(home[e] == me, s_n[me * Ep + e], e);
+  }
+  __syncthreads();
+  if (local && tid == 0) {
+    int run = 0, runz = 0;
+    for (int d = 0; d < G; ++d) {
+      const int a = s_base[d], z = s_nnz[d];
+      s_base[d] = run;
+      s_nnz[d] = runz;
+      run += a;
+      runz += z;
+    }
+    s_base[G] = run;
+    s_nnz[G] = runz;
+    *o.n_seg = runz;
+    *o.n_fetch = 0;
+  }
+  if (!local) {
+    for (int e = tid; e < E; e += blockDim.x) {
+      const bool re = home[e] == me;
+      if (re) atomicAdd(&s_scal[1], 1);
+      if (s_n[me * Ep + e] > 0) {
+        atomicAdd(&s_scal[2], 1);
+        if (re) atomicAdd(&s_scal[0], 1);
+      }
+    }
+  }
+  __syncthreads();
+  // slot_base[g,e,d] = base(d) + off[d][e] + sum_{g'<g} S[g',e,d] (EP_EXPERT: base(d) = 0)
+  for (int e = L.e0; e < E; e += L.step) {
+    int run = (local ? s_base[L.d] : 0) + s_off[L.d * Ep + e];
+    for (int g = 0; g < G; ++g) {
+      o.slot_base[(g * E + e) * G + L.d] = run;
+      run += St[(g * G + L.d) * Ep + e];
+    }
+  }
+  HM_PSTAMP(6);
+  if (local) {
+    // one thread per (dest, expert): rank among the dest's keys (keys are distinct: the expert id
+    // is part of the key); 128-bit loads of the dest's key row
+    const bool vec = ((E | Ep) & 3) == 0;
+    for (int e = L.e0; e < E; e += L.step) {
+      const int d = L.d;
+      const unsigned key = s_key[d * Ep + e];
+      if (key == 0xffffffffu) continue;
+      const unsigned* kd = s_key + d * Ep;
+      int pos = 0;
+      if (vec) {
+        const uint4* kd4 = reinterpret_cast<const uint4*>(kd);
+#pragma unroll 4
+        for (int j = 0; j < E / 4; ++j) {
+          const uint4 v = kd4[j];
+          pos += (v.x < key) + (v.y < key) + (v.z < key) + (v.w < key);
+        }
+      } else {
+        for (int j = 0; j < E; ++j) pos += kd[j] < key;
+      }
+      const int ne = s_n[d * Ep + e];
+      const int sidx = s_nnz[d] + pos;
+      o.segs[sidx] = make_int4(s_base[d] + s_off[d * Ep + e], ne, e, e);
+      s_cnt[sidx] = (ne + 127) / 128;
+    }
+    __syncthreads();
+    HM_PSTAMP(7);
+    block_scan_to(s_cnt, s_nnz[G], o.mprefix, s_tmp);
+    HM_PSTAMP(8);
+    return;
+  }
+  const int n_res_work = s_scal[0], n_home = s_scal[1], n_work = s_scal[2];
+  for (int e = tid; e < E; e += blockDim.x) {
+    const unsigned key = s_key[e];
+    if (key == 0xffffffffu) continue;
+    int oo = 0;
+    for (int j = 0; j < E; ++j) oo += s_key[j] < key;
+    int wslot;
+    if (home[e] == me) {
+      wslot = s_hr[e];
+    } else {
+      // bounded cache: fetch i reuses the slot of fetch i - cache_slots, the one whose occupant
+      // finishes first (fetched experts compute in plan order; engine.py:239-257)
+      const int fi = oo - n_res_work;
+      wslot = n_home + (o.cache_slots > 0 ? fi % o.cache_slots : fi);
+      o.fetch[fi] = e;
+    }
+    const int ne = s_n[me * Ep + e];
+    o.segs[oo] = make_int4(s_off[me * Ep + e], ne, wslot, e);
+    s_cnt[oo] = (ne + 127) / 128;
+  }
+  if (tid == 0) {
+    *o.n_seg = n_work;
+    *o.n_fetch = n_work - n_res_work;
+  }
+  __syncthreads();
+  HM_PSTAMP(7);
+  block_scan_to(s_cnt, n_work, o.mprefix, s_tmp);
+  HM_PSTAMP(8);
+}
+
+// ------------------------------------------------------------------------------------------
 // kernels
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) hist_scan_kernel(const int32_t* __restrict__ tile_hist, int n_ranks, int tpr,
@@ -802,7 +1118,7 @@ __global__ void __launch_bounds__(kPlanThreads)
     plan_kernel(const int32_t* __restrict__ tile_hist, int tpr, const int32_t* __restrict__ m_in,
                 const int32_t* __restrict__ home_g, int G, int E, int q, int rebalance, int mode, int me,
                 int32_t* __restrict__ m_out, int32_t* __restrict__ tile_off, int32_t* __restrict__ S_out,
-                int32_t* __restrict__ iters_out, int32_t* __restrict__ loads_out, LayoutOut o) {
+                int32_t* __restrict__ iters_out, int32_t* __restrict__ loads_out, LayoutOut o, int fast) {
   extern __shared__ int s_dyn[];
   __shared__ long long F[32 * 32];
   __shared__ int s_part[8 * 128];
@@ -811,8 +1127,13 @@ __global__ void __launch_bounds__(kPlanThreads)
   int* s_m = s_home + E;          // [G*E]
   int* s_S = s_m + GE;            // [G*E*G]
   int* s_scr = s_S + GE * G;      // layout scratch [3*G*E + 1 + 3*E]
-  int* s_St = s_scr + layout_scratch_ints(G, E);  // [G*G*E] transposed S for the fast rebalance loop
+  int* s_St = s_scr + plan_scratch_ints(G, E);  // [G*G*E] transposed S (fast path: [G*G][E + 32/G])
+#ifdef HM_PLAN_TWICE  // diagnostics: run the whole plan twice, the stamps keep the second (warm icache) pass
+  for (int rep = 0; rep < 2; ++rep) {
+  __syncthreads();
+#endif
   if (threadIdx.x == 0) g_phase_ns[0] = globaltimer_ns();
+  HM_PSTAMP(0);
 #ifdef HM_PLAN_CLOCK
   const long long c0 = clock64();
 #endif
@@ -824,13 +1145,39 @@ __global__ void __launch_bounds__(kPlanThreads)
   }
   __syncthreads();
   if (threadIdx.x == 0) g_phase_ns[1] = globaltimer_ns();
-  dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F, s_St);
-  if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
-  for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
-  dev_layout(s_S, s_home, G, E, mode, me, o, s_scr);
+  HM_PSTAMP(1);
+  // fast path: every count < 2^21 (32-bit packed keys), harmony / static policy, LOCAL or
+  // EP_EXPERT layout (HM_PLAN_FAST=0 forces the general path: A/B and tests)
+  __shared__ unsigned long long s_total;
+  if (threadIdx.x == 0) s_total = 0ull;
+  __syncthreads();
+  {
+    unsigned long long part = 0ull;
+    for (int i = threadIdx.x; i < GE; i += blockDim.x) part += (unsigned)s_m[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+    if ((threadIdx.x & 31) == 0 && part != 0ull) atomicAdd(&s_total, part);
+  }
+  __syncthreads();
+  if (fast && s_total < (1ull << 21) && rebalance != HM_POLICY_EVEN_SPLIT && mode != HM_LAYOUT_EP &&
+      (G & (G - 1)) == 0) {
+    const int Ep = E + 32 / G;
+    dev_schedule_t(s_St, Ep, reinterpret_cast<int*>(F), s_m, s_home, G, E, q, rebalance, S_out, iters_out,
+                   loads_out);
+    if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
+    dev_layout_t(s_St, Ep, s_home, G, E, mode, me, o, s_scr);
+  } else {
+    dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F, s_St);
+    if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
+    for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
+    dev_layout(s_S, s_home, G, E, mode, me, o, s_scr);
+  }
   if (threadIdx.x == 0) g_phase_ns[3] = globaltimer_ns();
 #ifdef HM_PLAN_CLOCK
   if (threadIdx.x == 0) g_phase_ns[7] = (unsigned long long)(clock64() - c0);
+#endif
+#ifdef HM_PLAN_TWICE
+  }
 #endif
 }
 
@@ -911,6 +1258,15 @@ static bool use_plan_g1() {  // HM_PLAN_G1=0: the general planner at G = 1 too (
   return v == 1;
 }
 
+static int plan_fast() {  // HM_PLAN_FAST=0: the general (S-layout, 64-bit) planner path everywhere
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HM_PLAN_FAST");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_in, const int32_t* home, int G, int E,
                 int q, int rebalance, int mode, int me, int32_t* m_out, int32_t* tile_off, int32_t* S, int32_t* iters,
                 int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix,
@@ -924,7 +1280,7 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   const bool hist = tile_hist != nullptr;
   if (hist && mode != HM_LAYOUT_LOCAL) return set_error(HM_EINVAL, "plan: tile histograms imply the LOCAL layout");
   if (!hist && m_in == nullptr) return set_error(HM_EINVAL, "plan: need tile_hist or m_all");
-  const size_t smem = (size_t)(E + G * E + 2 * G * E * G + layout_scratch_ints(G, E)) * sizeof(int);
+  const size_t smem = (size_t)(E + G * E + 2 * G * E * G + 32 * G + plan_scratch_ints(G, E)) * sizeof(int);
   if (smem > 200 * 1024) return set_error(HM_EINVAL, "plan: G*E*G too large for the fused planner; use hm_schedule");
   LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch, cache_slots};
   if (hist && G == 1 && use_plan_g1()) {
@@ -935,11 +1291,11 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   } else if (hist) {
     cudaFuncSetAttribute(plan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     plan_kernel<true><<<1, kPlanThreads, smem, stream>>>(tile_hist, tiles_per_rank, nullptr, home, G, E, q, rebalance,
-                                                         mode, me, m_out, tile_off, S, iters, loads, o);
+                                                         mode, me, m_out, tile_off, S, iters, loads, o, plan_fast());
   } else {
     cudaFuncSetAttribute(plan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     plan_kernel<false><<<1, kPlanThreads, smem, stream>>>(nullptr, 0, m_in, home, G, E, q, rebalance, mode, me,
-                                                          m_out, tile_off, S, iters, loads, o);
+                                                          m_out, tile_off, S, iters, loads, o, plan_fast());
   }
   return check_launch("plan");
 }

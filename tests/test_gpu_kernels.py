@@ -81,6 +81,45 @@ def test_fused_planner_wide_totals_bit_exact(golden):
     assert n >= 20
 
 
+@pytest.mark.parametrize("pack", ["fig4", "acceptance_c2", "baseline_shapes"])
+def test_fused_planner_bit_exact(golden, pack):
+    """The fused planner's fast path (hm_plan: St-only schedule, 32-bit keys) equals moesim's
+    S / iterations / loads on the fixtures, and its LOCAL and EP_EXPERT layouts equal the
+    standalone layout kernel's (pinned to the oracle by test_gpu_ep) on the same S."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    n = 0
+    for inst in iter_packed(golden(pack)):
+        G, E = inst["m"].shape
+        if 2 * G * E * G * 4 > 180 * 1024 or G * E > 8192:
+            continue
+        m = torch.from_numpy(inst["m"].astype(np.int32)).to(dev)
+        home = torch.from_numpy(inst["home"].astype(np.int32)).to(dev)
+        for mode, me in ((ops.HM_LAYOUT_LOCAL, 0), (ops.HM_LAYOUT_EP_EXPERT, n % G)):
+            try:
+                p = ops.plan(home, G, E, inst["q"], True, mode, me, m_all=m, cache_slots=(n % 3) if mode else 0)
+            except ValueError:  # beyond the fused planner's shared memory (hm_schedule covers it)
+                break
+            assert np.array_equal(p.S.cpu().numpy(), inst["S"]), f"{pack} instance {inst['i']}"
+            assert int(p.iters.item()) == inst["iters"], f"{pack} instance {inst['i']}"
+            assert np.array_equal(p.loads.cpu().numpy(), inst["S"].sum(axis=(0, 1)))
+            lay = ops.dispatch_layout(p.S, home, mode, me, cache_slots=(n % 3) if mode else 0)
+            ns = int(lay.n_seg.item())
+            assert int(p.layout.n_seg.item()) == ns
+            assert np.array_equal(p.layout.segs[:ns].cpu().numpy(), lay.segs[:ns].cpu().numpy())
+            assert np.array_equal(p.layout.mtile_prefix[: ns + 1].cpu().numpy(),
+                                  lay.mtile_prefix[: ns + 1].cpu().numpy())
+            assert np.array_equal(p.layout.slot_base.cpu().numpy(), lay.slot_base.cpu().numpy())
+            nf = int(lay.n_fetch.item())
+            assert int(p.layout.n_fetch.item()) == nf
+            assert np.array_equal(p.layout.fetch[:nf].cpu().numpy(), lay.fetch[:nf].cpu().numpy())
+        n += 1
+        if n >= 400:
+            break
+    assert n >= (1 if pack == "fig4" else 100)
+
+
 def test_even_split_kernel_bit_exact(golden):
     """HM_POLICY_EVEN_SPLIT == the reference's even_split_assign (policies.py:174-203)."""
     from paper_2506_12417_b200 import RoutingMatrix, even_split_assign, ops
