@@ -298,6 +298,43 @@ HM_API int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_
                             int32_t* pos, void* stream);
 
 /*
+ * Expert-ordered dispatch (EP p2p, overlapped with FFN1).  hm_plan_dispatch is hm_plan with
+ * m_all_in and the HM_LAYOUT_EP_EXPERT layout of rank `me`, plus this rank's push work list:
+ *   push_items [G*E, 4] int32: item v = p*G + d is me's bucket of the expert at position p of
+ *     destination d's plan order (engine.py:233-234): (expert, first rank among me's assignments
+ *     to it, rows, first row in d's receive buffer); rows 0 where d has fewer than p+1 experts;
+ *   push_cprefix [G*E + 1]: exclusive prefix of 32-row units per item (-1 at [G*E] if the batch
+ *     left the planner's fast path: >= 2^21 assignments, which the push then reports by trapping);
+ *   push_ebase [E + 1]: exclusive prefix of m_all[me] over experts.
+ * Requires a power-of-two G and a harmony / static policy.
+ * hm_dispatch_push_ordered copies the rows unit by unit in that order (32 rows of one bucket per
+ * unit) into dst_rows[d] / tags dst_tok[d] as hm_dispatch_push with dst_delta == NULL does, and
+ * after each unit adds its row count to ((int32_t*)dst_arrive[d])[expert] (system-scope release).
+ * order [tokens*k] int32 scratch; pos [tokens*k] or NULL as hm_dispatch_push; sync [2] uint32
+ * scratch (zeroed by the call).  One CTA per SM with a grid barrier: launch it right before the
+ * FFN1 that consumes it, nothing else running on the device's SMs in between.
+ * hm_grouped_gemm_arrive is hm_grouped_gemm (TMA-loaded A, no row map) whose producers wait per
+ * segment until a_arrive[expert] >= the segment's rows (system-scope acquire); pdl = 1 launches
+ * it with programmatic stream serialisation so it starts while the push kernel before it in the
+ * stream still runs (it completes only after that kernel has).
+ */
+HM_API int hm_plan_dispatch(const int32_t* m_all_in, const int32_t* home, int G, int E, int q, int rebalance, int me,
+                            int32_t* S, int32_t* iters, int32_t* loads, int32_t* slot_base, int32_t* segs,
+                            int32_t* n_seg, int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch, int cache_slots,
+                            int32_t* push_items, int32_t* push_cprefix, int32_t* push_ebase, void* stream);
+HM_API int hm_dispatch_push_ordered(const void* x, const int32_t* topk_idx, const int32_t* lrank,
+                                    const int32_t* tile_off, const int32_t* S, const int32_t* slot_base,
+                                    const int32_t* push_items, const int32_t* push_cprefix, const int32_t* push_ebase,
+                                    int tokens, int me, int G, int E, int k, int d, const uint64_t* dst_rows,
+                                    const uint64_t* dst_tok, const uint64_t* dst_arrive, int32_t* order, int32_t* pos,
+                                    uint32_t* sync, void* stream);
+HM_API int hm_grouped_gemm_arrive(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                                  const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix,
+                                  int epilogue, void* out, const int32_t* slot_ready, int ready_from_slot, int epoch,
+                                  int32_t* slot_done, const hm_fetch_plan* fetch, const int32_t* a_arrive, int pdl,
+                                  void* stream);
+
+/*
  * hm_grouped_gemm whose output rows go to other ranks (FFN2 + the return all_to_all): the rows
  * of a segment starting at receive row r0 belong to source g with out_split[g] <= r0 <
  * out_split[g+1], and land in out_ptrs[g] (device array of n_out peer pointers) at row

@@ -46,6 +46,11 @@ SIGNATURES = {
     "hm_combine": [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_ep_offsets": [_vp, _i32, _i32, _i32, _vp, _vp, _vp],
     "hm_dispatch_push": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
+    "hm_plan_dispatch": [_vp, _vp, _i32, _i32, _i32, _i32, _i32] + [_vp] * 9 + [_i32, _vp, _vp, _vp, _vp],
+    "hm_dispatch_push_ordered": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp,
+                                 _vp, _vp, _vp, _vp, _vp, _vp],
+    "hm_grouped_gemm_arrive": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp,
+                               _vp, _i32, _vp],
     "hm_grouped_gemm_remote": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp, _vp, _i32,
                                _i32, _vp, _vp, _vp],
     "hm_fetch_experts": [_vp, _vp, _vp, _vp, ctypes.c_size_t, ctypes.c_size_t, _vp, _vp, _i32, _i32, _vp, _vp, _vp,

@@ -93,7 +93,11 @@ int launch_schedule_batched(const int32_t*, const int32_t*, int, int, int, int, 
 int read_plan_phases(long long*);
 int launch_plan(const int32_t*, int, const int32_t*, const int32_t*, int, int, int, int, int, int, int32_t*, int32_t*,
                 int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int32_t*, int,
-                cudaStream_t);
+                cudaStream_t, int32_t* = nullptr, int32_t* = nullptr, int32_t* = nullptr);
+int launch_dispatch_push_ordered(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*,
+                                 const int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int,
+                                 int, int, const unsigned long long*, const unsigned long long*,
+                                 const unsigned long long*, int32_t*, int32_t*, uint32_t*, cudaStream_t);
 int launch_layout(const int32_t*, const int32_t*, int, int, int, int, int32_t*, int32_t*, int32_t*, int32_t*,
                   int32_t*, int32_t*, int, cudaStream_t);
 int launch_permute(const void*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, const int32_t*, int,
@@ -162,6 +166,16 @@ int hm_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_all_i
                      as_stream(stream));
 }
 
+int hm_plan_dispatch(const int32_t* m_all_in, const int32_t* home, int G, int E, int q, int rebalance, int me,
+                     int32_t* S, int32_t* iters, int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg,
+                     int32_t* mtile_prefix, int32_t* fetch, int32_t* n_fetch, int cache_slots, int32_t* push_items,
+                     int32_t* push_cprefix, int32_t* push_ebase, void* stream) {
+  if (push_items == nullptr) return set_error(HM_EINVAL, "plan_dispatch: push_items is required");
+  return launch_plan(nullptr, 0, m_all_in, home, G, E, q, rebalance, HM_LAYOUT_EP_EXPERT, me, nullptr, nullptr, S,
+                     iters, loads, slot_base, segs, n_seg, mtile_prefix, fetch, n_fetch, cache_slots,
+                     as_stream(stream), push_items, push_cprefix, push_ebase);
+}
+
 int hm_schedule_batched(const int32_t* m_all, const int32_t* home, int B, int G, int E, int q, int rebalance,
                         int32_t* S, int32_t* iters, int32_t* loads, void* stream) {
   return launch_schedule_batched(m_all, home, B, G, E, q, rebalance, S, iters, loads, as_stream(stream));
@@ -215,6 +229,28 @@ int hm_grouped_gemm_remote(const void* A, int64_t a_rows, const void* W, int64_t
                              nullptr, 1, slot_ready, ready_from_slot, epoch, as_stream(stream),
                              reinterpret_cast<const unsigned long long*>(out_ptrs), out_split, n_out, slot_done,
                              fetch);
+}
+
+int hm_grouped_gemm_arrive(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                           const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, int epilogue,
+                           void* out, const int32_t* slot_ready, int ready_from_slot, int epoch, int32_t* slot_done,
+                           const hm_fetch_plan* fetch, const int32_t* a_arrive, int pdl, void* stream) {
+  if (a_arrive == nullptr) return set_error(HM_EINVAL, "grouped_gemm_arrive: a_arrive is required");
+  return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, epilogue, out, nullptr, nullptr, 1,
+                             slot_ready, ready_from_slot, epoch, as_stream(stream), nullptr, nullptr, 0, slot_done,
+                             fetch, nullptr, a_arrive, pdl);
+}
+
+int hm_dispatch_push_ordered(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+                             const int32_t* S, const int32_t* slot_base, const int32_t* push_items,
+                             const int32_t* push_cprefix, const int32_t* push_ebase, int tokens, int me, int G, int E,
+                             int k, int d, const uint64_t* dst_rows, const uint64_t* dst_tok,
+                             const uint64_t* dst_arrive, int32_t* order, int32_t* pos, uint32_t* sync, void* stream) {
+  return launch_dispatch_push_ordered(x, topk_idx, lrank, tile_off, S, slot_base, push_items, push_cprefix, push_ebase,
+                                      tokens, me, G, E, k, d, reinterpret_cast<const unsigned long long*>(dst_rows),
+                                      reinterpret_cast<const unsigned long long*>(dst_tok),
+                                      reinterpret_cast<const unsigned long long*>(dst_arrive), order, pos, sync,
+                                      as_stream(stream));
 }
 
 int hm_ep_offsets(const int32_t* S, int G, int E, int me, int32_t* dst_delta, int32_t* recv_split, void* stream) {

@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
                              const int* __restrict__ a_gather, int a_gather_div, int a_src_rows,
                              const unsigned long long* __restrict__ out_ptrs, const int* __restrict__ out_split,
                              int n_out, int* __restrict__ slot_done, const hm_fetch_plan fplan, int tail_split,
-                             const CombineFuse cf) {
+                             const CombineFuse cf, const int* __restrict__ a_arrive) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   if (fplan.pairs > 0 && (int)(blockIdx.x >> 1) >= (int)(gridDim.x >> 1) - fplan.pairs) {
@@ -626,6 +626,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
       cur.gm = max(1, half_tiles >> 1);
       int stage = 0;
       uint32_t phase = 0;
+      int arrived_e = -1;
       for (int t = pair; t < units; t += npairs) {
         int4 seg;
         int m, nb, slice;
@@ -657,6 +658,21 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
             }
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        if (a_arrive != nullptr && seg.w != arrived_e) {
+          // expert-ordered dispatch (hm_dispatch_push_ordered): this segment's rows land over
+          // NVLink while earlier segments compute; wait for all seg.y of them (system scope)
+          long long spins = 0;
+          while (ld_acquire_sys(a_arrive + seg.w) < seg.y) {
+            __nanosleep(64);
+            if (++spins > (1ll << 27)) {
+              printf("hm grouped_gemm: rows of expert %d never arrived (%d < %d)\n", seg.w,
+                     ld_acquire_sys(a_arrive + seg.w), seg.y);
+              __trap();
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          arrived_e = seg.w;
         }
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -980,6 +996,9 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
     tc_fence_after();
     tmem_dealloc_2cta<kTmemCols>(tmem_base);
   }
+  // launched behind the ordered dispatch push (PDL): do not complete before it has, so the
+  // stream order of later kernels covers the push too (returns at once without a dependency)
+  if (a_arrive != nullptr) griddep_wait();
 }
 
 static bool use_half_tiles() {
@@ -1069,7 +1088,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
                         void* out, const int32_t* row_map, const int32_t* a_gather, int a_gather_div,
                         const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
                         const unsigned long long* out_ptrs, const int32_t* out_split, int n_out, int32_t* slot_done,
-                        const hm_fetch_plan* fetch, const CombineFuse* combine) {
+                        const hm_fetch_plan* fetch, const CombineFuse* combine, const int32_t* a_arrive, int pdl) {
   if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
     return set_error(HM_EINVAL, "grouped_gemm: N %% 256 and K %% 64 must be 0");
   if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm: weight rows must be a multiple of N");
@@ -1101,6 +1120,8 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
       return set_error(HM_EINVAL, "grouped_gemm: the fused combine needs the STORE epilogue with a token-major "
                                   "row map, local output, weights, counters and 1 <= k <= 32");
   }
+  if (a_arrive != nullptr && (a_gather != nullptr || !use_2cta()))
+    return set_error(HM_EINVAL, "grouped_gemm: arrival waits need TMA-loaded A rows and the 2-CTA kernel");
   if (a_rows <= 0) return HM_OK;
   CUtensorMap ta, tb;
   // gathered A: 1-row boxes fetched four at a time by tile::gather4
@@ -1139,13 +1160,15 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     cfg.blockDim = dim3(kGemmThreads + (gather ? kALoadWarps * 32 : 0));
     cfg.dynamicSmemBytes = kGemm2Smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: start behind the push
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 2 : 1;
     cudaError_t e = cudaSuccess;
     const auto* a_src = reinterpret_cast<const __nv_bfloat16*>(A);
 #define HM_GEMM2(EPI, G)                                                                                          \
@@ -1155,7 +1178,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
     e = cudaLaunchKernelEx(&cfg, grouped_gemm_2cta_kernel<EPI, G>, ta, tb2, ta64, tb64, half_tiles, s4,          \
                            mtile_prefix, n_seg, o, N, K,                                                          \
                            ldo, row_map, slot_ready, ready_from_slot, epoch, a_src, a_gather, a_gather_div,       \
-                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan, tail_split, cf);            \
+                           (int)a_rows, out_ptrs, out_split, n_out, slot_done, fplan, tail_split, cf, a_arrive);  \
   } while (0)
     switch (epilogue * 2 + (gather ? 1 : 0)) {
       case kEpiStore * 2: HM_GEMM2(kEpiStore, false); break;

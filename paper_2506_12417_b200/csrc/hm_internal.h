@@ -37,7 +37,7 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
                         const int32_t* slot_ready, int ready_from_slot, int epoch, cudaStream_t stream,
                         const unsigned long long* out_ptrs = nullptr, const int32_t* out_split = nullptr,
                         int n_out = 0, int32_t* slot_done = nullptr, const hm_fetch_plan* fetch = nullptr,
-                        const CombineFuse* combine = nullptr);
+                        const CombineFuse* combine = nullptr, const int32_t* a_arrive = nullptr, int pdl = 0);
 
 int gemm_resident_pairs(int epilogue, bool gather);
 

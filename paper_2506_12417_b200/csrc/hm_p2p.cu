@@ -126,6 +126,117 @@ __global__ void __launch_bounds__(kPushWarps * 32)
 }
 
 // ------------------------------------------------------------------------------------------
+// expert-ordered dispatch push (overlapped with FFN1).  The unordered push above finishes every
+// expert's rows at about the same time (token order), so FFN1 can only start after the whole
+// all-to-all.  Here every sender walks its work list in the DESTINATIONS' plan order (item
+// p*G + d = its bucket of the p-th expert of destination d, hm_plan_dispatch), 32 rows per work
+// unit, and after each unit adds the row count to the destination's per-expert arrival counter
+// (system-scope release after the rows).  FFN1 is launched right behind this kernel with
+// programmatic dependent launch and its producer waits per segment for arrive[e] == rows of e,
+// so the first experts' tiles start while later experts are still in flight over NVLink.
+//   phase 1: order[ebase[e] + r] = t*k + j for this rank's r-th assignment to e (and pos);
+//   grid barrier (one CTA per SM, all resident: launched before its dependent GEMM);
+//   phase 2: 32-row units by a global counter, in (position, destination) order.
+// ------------------------------------------------------------------------------------------
+constexpr int kOPushThreads = 256;
+constexpr int kOPushRows = 32;
+
+template <int VEC>
+__global__ void __launch_bounds__(kOPushThreads, 4)  // <= 64 registers: co-resident with the FFN1 pairs
+    dispatch_push_ordered_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ topk_idx,
+                                 const int32_t* __restrict__ lrank, const int32_t* __restrict__ tile_off,
+                                 const int32_t* __restrict__ S, const int32_t* __restrict__ slot_base,
+                                 const int4* __restrict__ items, const int32_t* __restrict__ cprefix,
+                                 const int32_t* __restrict__ ebase, int n_items, int64_t T, int me, int G, int E,
+                                 int k, int n16, const unsigned long long* __restrict__ dst_rows,
+                                 const unsigned long long* __restrict__ dst_tok,
+                                 const unsigned long long* __restrict__ dst_arrive, int32_t* __restrict__ order,
+                                 int32_t* __restrict__ pos, unsigned* __restrict__ sync) {
+  griddep_launch_dependents();
+  __shared__ int s_unit;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // ---- phase 1: per-expert assignment order (+ pos: the row of each assignment in its
+  // destination's receive buffer, as the unordered push reports it)
+  const int64_t TK = T * k;
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < TK; a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = a / k;
+    const int e = __ldg(topk_idx + a);
+    const int r = __ldg(tile_off + (t / 128) * E + e) + __ldg(lrank + a);
+    order[__ldg(ebase + e) + r] = (int32_t)a;
+    if (pos != nullptr) {
+      const int32_t* srow = S + ((int64_t)me * E + e) * G;
+      int c = 0, d = 0;
+      for (; d < G - 1; ++d) {
+        const int sv = __ldg(srow + d);
+        if (c + sv > r) break;
+        c += sv;
+      }
+      pos[a] = __ldg(slot_base + ((int64_t)me * E + e) * G + d) + (r - c);
+    }
+  }
+  // ---- grid barrier
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(sync, 1u);
+    long long spins = 0;
+    while (ld_acquire_gpu(reinterpret_cast<const int*>(sync)) < (int)gridDim.x) {
+      __nanosleep(32);
+      if (++spins > (1ll << 26)) {
+        printf("hm dispatch_push_ordered: grid barrier timed out (CTAs not co-resident)\n");
+        __trap();
+      }
+    }
+  }
+  __syncthreads();
+  const int total = __ldcg(cprefix + n_items);
+  if (total < 0) {
+    if (threadIdx.x == 0) printf("hm dispatch_push_ordered: no push work list (planner took the general path)\n");
+    __trap();
+  }
+  // ---- phase 2: 32-row units in (position, destination) order
+  int it = 0;
+  for (;;) {
+    if (threadIdx.x == 0) s_unit = (int)atomicAdd(sync + 1, 1u);
+    __syncthreads();
+    const int u = s_unit;
+    __syncthreads();
+    if (u >= total) break;
+    while (__ldg(cprefix + it + 1) <= u) ++it;  // units only grow for this CTA: amortised O(1)
+    const int4 item = __ldg(items + it);
+    const int d = it & (G - 1);
+    const int r0 = (u - __ldg(cprefix + it)) * kOPushRows;
+    const int nr = min(kOPushRows, item.z - r0);
+    const int e = item.x;
+    const int ob = __ldg(ebase + e) + item.y + r0;
+    uint4* dst = reinterpret_cast<uint4*>(__ldg(dst_rows + d));
+    int32_t* tok = reinterpret_cast<int32_t*>(__ldg(dst_tok + d));
+    for (int rr = warp; rr < nr; rr += kOPushThreads / 32) {
+      const int a = __ldcg(order + ob + rr);
+      const uint4* src = x + (int64_t)(a / k) * n16;
+      uint4 v[VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const int c = i * 32 + lane;
+        if (c < n16) v[i] = ld_global_nc_v4(src + c);
+      }
+      uint4* drow = dst + (int64_t)(item.w + r0 + rr) * n16;
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const int c = i * 32 + lane;
+        if (c < n16) drow[c] = v[i];
+      }
+      if (lane == 0) tok[item.w + r0 + rr] = (int32_t)(((uint32_t)me << 24) | (uint32_t)a);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();  // every row of the unit (bar.sync above) before the count
+      red_release_sys_add(reinterpret_cast<int*>(__ldg(dst_arrive + d)) + e, nr);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // device-driven expert fetch (K6).  All CTAs copy fetch i's gate/up block, then its down
 // block, then move on (one logical channel in plan order, engine.py:253-265); the last CTA
 // to finish a block publishes its slot's ready flag with release semantics.
@@ -213,6 +324,42 @@ int launch_dispatch_push(const void* x, const int32_t* topk_idx, const int32_t* 
   else return set_error(HM_EINVAL, "dispatch_push: d > 4096 unsupported");
 #undef HM_PUSH
   return check_launch("dispatch_push");
+}
+
+int launch_dispatch_push_ordered(const void* x, const int32_t* topk_idx, const int32_t* lrank, const int32_t* tile_off,
+                                 const int32_t* S, const int32_t* slot_base, const int32_t* items,
+                                 const int32_t* cprefix, const int32_t* ebase, int tokens, int me, int G, int E, int k,
+                                 int d, const unsigned long long* dst_rows, const unsigned long long* dst_tok,
+                                 const unsigned long long* dst_arrive, int32_t* order, int32_t* pos, uint32_t* sync,
+                                 cudaStream_t stream) {
+  if (d % 8 != 0) return set_error(HM_EINVAL, "dispatch_push_ordered: d must be a multiple of 8");
+  if (G < 1 || G > 32 || (G & (G - 1)) != 0 || me < 0 || me >= G || k < 1 || k > 32)
+    return set_error(HM_EINVAL, "dispatch_push_ordered: bad G (power of two <= 32) / me / k");
+  if ((int64_t)tokens * k > (1 << 24))
+    return set_error(HM_EINVAL, "dispatch_push_ordered: tagged rows need tokens * k <= 2^24");
+  if (items == nullptr || cprefix == nullptr || ebase == nullptr || dst_arrive == nullptr || order == nullptr ||
+      sync == nullptr)
+    return set_error(HM_EINVAL, "dispatch_push_ordered: work list, arrival counters, order and sync are required");
+  // the grid barrier needs every CTA resident: one per SM (the kernel runs before its dependent GEMM)
+  cudaError_t ce = cudaMemsetAsync(sync, 0, 2 * sizeof(uint32_t), stream);
+  if (ce != cudaSuccess) return set_error(HM_ECUDA, "dispatch_push_ordered sync: %s", cudaGetErrorString(ce));
+  if (tokens < 0) return set_error(HM_EINVAL, "dispatch_push_ordered: tokens must be >= 0");
+  const int n16 = d / 8;
+  const int grid = num_sms();
+  const auto* xs = reinterpret_cast<const uint4*>(x);
+  const int4* it4 = reinterpret_cast<const int4*>(items);
+#define HM_OPUSH(V)                                                                                            \
+  dispatch_push_ordered_kernel<V><<<grid, kOPushThreads, 0, stream>>>(                                         \
+      xs, topk_idx, lrank, tile_off, S, slot_base, it4, cprefix, ebase, G * E, tokens, me, G, E, k, n16, dst_rows, \
+      dst_tok, dst_arrive, order, pos, sync)
+  if (n16 <= 32) HM_OPUSH(1);
+  else if (n16 <= 64) HM_OPUSH(2);
+  else if (n16 <= 128) HM_OPUSH(4);
+  else if (n16 <= 256) HM_OPUSH(8);
+  else if (n16 <= 512) HM_OPUSH(16);
+  else return set_error(HM_EINVAL, "dispatch_push_ordered: d > 4096 unsupported");
+#undef HM_OPUSH
+  return check_launch("dispatch_push_ordered");
 }
 
 int launch_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const unsigned long long* src_in,

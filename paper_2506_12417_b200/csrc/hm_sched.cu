@@ -418,6 +418,14 @@ struct LayoutOut {
   int32_t* fetch;
   int32_t* n_fetch;
   int cache_slots;  // EP: fetch cache slots (0 = one per fetched expert); fetch i -> slot n_home + i % cache_slots
+  // EP_EXPERT, optional (hm_plan_dispatch): this rank's push work list for the expert-ordered
+  // dispatch (hm_dispatch_push_ordered).  Item v = p*G + d is the bucket (me -> d) of the expert at
+  // position p of destination d's plan order: (expert, first rank c0 among me's assignments to it,
+  // rows, first row in d's receive buffer), rows 0 where d has no p-th expert;
+  // push_cprefix[v] = sum of 32-row chunks of items < v; push_ebase[e] = sum_{e'<e} m_all[me][e'].
+  int4* push_items;
+  int32_t* push_cprefix;
+  int32_t* push_ebase;
 };
 
 // plan-order sort key (ascending = execution order): residents first, then more tokens,
@@ -856,7 +864,7 @@ __device__ __forceinline__ unsigned plan_key32(bool resident, int n, int e) {
 
 // fast-path layout scratch (ints): s_n, s_off [G][Ep], s_cnt [G*E + 1], s_key [G][Ep] (+3 for
 // 16-byte alignment), s_hr [E]
-constexpr int fast_layout_scratch_ints(int G, int E) { return 3 * G * (E + 32 / G) + G * E + 1 + 3 + E; }
+constexpr int fast_layout_scratch_ints(int G, int E) { return 3 * G * (E + 32 / G) + 2 * (G * E + 1) + 3 + E; }
 constexpr int plan_scratch_ints(int G, int E) {
   return layout_scratch_ints(G, E) > fast_layout_scratch_ints(G, E) ? layout_scratch_ints(G, E)
                                                                      : fast_layout_scratch_ints(G, E);
@@ -1017,6 +1025,62 @@ __device__ void dev_layout_t(const int* St, int Ep, const int* home, int G, int 
   __syncthreads();
   HM_PSTAMP(7);
   block_scan_to(s_cnt, n_work, o.mprefix, s_tmp);
+  if (o.push_items != nullptr) {
+    // push work list for the expert-ordered dispatch: every destination's plan order (keys of
+    // all (d, e); s_key is free again), this rank's bucket of each (position, destination)
+    int* s_pc = s_hr + E;  // [GE + 1] 32-row chunks per item
+    for (int e = L.e0; e < E; e += L.step) s_key[L.d * Ep + e] = plan_key32(home[e] == L.d, s_n[L.d * Ep + e], e);
+    for (int v = tid; v < GE; v += blockDim.x) {
+      o.push_items[v] = make_int4(0, 0, 0, 0);
+      s_pc[v] = 0;
+    }
+    __syncthreads();
+    const bool vec = ((E | Ep) & 3) == 0;
+    for (int e = L.e0; e < E; e += L.step) {
+      const int d = L.d;
+      const unsigned key = s_key[d * Ep + e];
+      if (key == 0xffffffffu) continue;
+      const unsigned* kd = s_key + d * Ep;
+      int pos = 0;
+      if (vec) {
+        const uint4* kd4 = reinterpret_cast<const uint4*>(kd);
+#pragma unroll 4
+        for (int j = 0; j < E / 4; ++j) {
+          const uint4 v = kd4[j];
+          pos += (v.x < key) + (v.y < key) + (v.z < key) + (v.w < key);
+        }
+      } else {
+        for (int j = 0; j < E; ++j) pos += kd[j] < key;
+      }
+      const int cnt = St[(me * G + d) * Ep + e];
+      int c0 = 0;
+      for (int d2 = 0; d2 < d; ++d2) c0 += St[(me * G + d2) * Ep + e];
+      int row0 = s_off[d * Ep + e];
+      for (int g = 0; g < me; ++g) row0 += St[(g * G + d) * Ep + e];
+      o.push_items[pos * G + d] = make_int4(e, c0, cnt, row0);
+      s_pc[pos * G + d] = (cnt + 31) >> 5;
+    }
+    __syncthreads();
+    block_scan_to(s_pc, GE, o.push_cprefix, s_tmp);
+    if (w == 0) {  // ebase: exclusive scan of this rank's histogram row m_all[me][.]
+      int running = 0;
+      for (int base = 0; base < E; base += 32) {
+        const int e = base + lane;
+        int x = 0;
+        if (e < E)
+          for (int d = 0; d < G; ++d) x += St[(me * G + d) * Ep + e];
+        int incl = x;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        if (e < E) o.push_ebase[e] = running + incl - x;
+        running += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) o.push_ebase[E] = running;
+    }
+  }
   HM_PSTAMP(8);
 }
 
@@ -1167,6 +1231,8 @@ __global__ void __launch_bounds__(kPlanThreads)
     if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
     dev_layout_t(s_St, Ep, s_home, G, E, mode, me, o, s_scr);
   } else {
+    // the push work list exists only on the fast path: flag it invalid (the push kernel traps)
+    if (o.push_cprefix != nullptr && threadIdx.x == 0) o.push_cprefix[GE] = -1;
     dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F, s_St);
     if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
     for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
@@ -1270,7 +1336,8 @@ static int plan_fast() {  // HM_PLAN_FAST=0: the general (S-layout, 64-bit) plan
 int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_in, const int32_t* home, int G, int E,
                 int q, int rebalance, int mode, int me, int32_t* m_out, int32_t* tile_off, int32_t* S, int32_t* iters,
                 int32_t* loads, int32_t* slot_base, int32_t* segs, int32_t* n_seg, int32_t* mtile_prefix,
-                int32_t* fetch, int32_t* n_fetch, int cache_slots, cudaStream_t stream) {
+                int32_t* fetch, int32_t* n_fetch, int cache_slots, cudaStream_t stream, int32_t* push_items,
+                int32_t* push_cprefix, int32_t* push_ebase) {
   if (q < 1) return set_error(HM_EINVAL, "token threshold q must be >= 1");
   if (cache_slots < 0) return set_error(HM_EINVAL, "plan: cache_slots must be >= 0");
   int rc = check_layout_args(G, E, mode, me);
@@ -1282,7 +1349,14 @@ int launch_plan(const int32_t* tile_hist, int tiles_per_rank, const int32_t* m_i
   if (!hist && m_in == nullptr) return set_error(HM_EINVAL, "plan: need tile_hist or m_all");
   const size_t smem = (size_t)(E + G * E + 2 * G * E * G + 32 * G + plan_scratch_ints(G, E)) * sizeof(int);
   if (smem > 200 * 1024) return set_error(HM_EINVAL, "plan: G*E*G too large for the fused planner; use hm_schedule");
-  LayoutOut o{slot_base, reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch, cache_slots};
+  if (push_items != nullptr) {
+    if (mode != HM_LAYOUT_EP_EXPERT || push_cprefix == nullptr || push_ebase == nullptr)
+      return set_error(HM_EINVAL, "plan: the push work list needs the EP_EXPERT layout, cprefix and ebase");
+    if ((G & (G - 1)) != 0 || rebalance == HM_POLICY_EVEN_SPLIT || !plan_fast())
+      return set_error(HM_EINVAL, "plan: the push work list needs a power-of-two G and the fast planner path");
+  }
+  LayoutOut o{slot_base,   reinterpret_cast<int4*>(segs), n_seg, mtile_prefix, fetch, n_fetch, cache_slots,
+              reinterpret_cast<int4*>(push_items), push_cprefix, push_ebase};
   if (hist && G == 1 && use_plan_g1()) {
     const size_t smem1 = (size_t)(3 * E + 2) * sizeof(int) + 8 + (size_t)E * 8;
     cudaFuncSetAttribute(plan_g1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);

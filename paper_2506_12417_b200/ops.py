@@ -201,6 +201,68 @@ def plan(home, G: int, E: int, q: int, rebalance: bool, mode: int, me: int = 0, 
     return Plan(m_out, tile_off, S, iters, loads, lay)
 
 
+class PushList:
+    """Device-side push work list of hm_plan_dispatch (expert-ordered dispatch)."""
+
+    __slots__ = ("items", "cprefix", "ebase")
+
+    def __init__(self, items, cprefix, ebase):
+        self.items, self.cprefix, self.ebase = items, cprefix, ebase
+
+
+def plan_dispatch(home, G: int, E: int, q: int, rebalance, me: int, m_all, cache_slots: int = 0,
+                  stream=None) -> tuple[Plan, PushList]:
+    """hm_plan (EP_EXPERT layout of rank ``me`` from the all-gathered m_all) plus this rank's push
+    work list in every destination's plan order (hm_dispatch_push_ordered)."""
+    _require_cuda(home, m_all)
+    dev = home.device
+    i32 = dict(dtype=torch.int32, device=dev)
+    S = torch.empty((G, E, G), **i32)
+    iters = torch.empty(1, **i32)
+    loads = torch.empty(G, **i32)
+    cap = G * E
+    lay = Layout(torch.empty((G, E, G), **i32), torch.empty((cap, 4), **i32), torch.empty(1, **i32),
+                 torch.empty(cap + 1, **i32), torch.empty(E, **i32), torch.empty(1, **i32))
+    pl = PushList(torch.empty((cap, 4), **i32), torch.empty(cap + 1, **i32), torch.empty(E + 1, **i32))
+    _lib.call("hm_plan_dispatch", _ptr(m_all), _ptr(home), G, E, int(q), _policy(rebalance), int(me), _ptr(S),
+              _ptr(iters), _ptr(loads), _ptr(lay.slot_base), _ptr(lay.segs), _ptr(lay.n_seg), _ptr(lay.mtile_prefix),
+              _ptr(lay.fetch), _ptr(lay.n_fetch), int(cache_slots), _ptr(pl.items), _ptr(pl.cprefix), _ptr(pl.ebase),
+              _stream(stream))
+    return Plan(m_all, None, S, iters, loads, lay), pl
+
+
+def dispatch_push_ordered(x, topk_idx, lrank, tile_off, S, slot_base, push: PushList, me: int, dst_rows, dst_tok,
+                          dst_arrive, order, sync, pos=None, stream=None):
+    """Expert-ordered fused scatter + dispatch: the rows of hm_dispatch_push (EP_EXPERT layout)
+    in every destination's plan order, 32-row units, each followed by a system-scope add of its
+    row count to the destination's arrival counter dst_arrive[d][expert]."""
+    _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base, dst_rows, dst_tok, dst_arrive, order, sync, pos)
+    T, d = x.shape
+    k = topk_idx.shape[1]
+    G, E, _ = S.shape
+    _lib.call("hm_dispatch_push_ordered", _ptr(x), _ptr(topk_idx), _ptr(lrank), _ptr(tile_off), _ptr(S),
+              _ptr(slot_base), _ptr(push.items), _ptr(push.cprefix), _ptr(push.ebase), T, int(me), G, E, k, d,
+              _ptr(dst_rows), _ptr(dst_tok), _ptr(dst_arrive), _ptr(order), _ptr(pos), _ptr(sync), _stream(stream))
+
+
+def grouped_gemm_arrive(A, W, N: int, layout: "Layout", epilogue: int, a_arrive, out=None, slot_ready=None,
+                        ready_from_slot: int = 0, epoch: int = 0, slot_done=None, fetch=None, pdl: bool = True,
+                        stream=None):
+    """K5 over an expert-major receive buffer whose rows are still arriving: each segment's
+    producer waits until a_arrive[expert] >= its rows; pdl launches it behind the push kernel."""
+    _require_cuda(A, W, a_arrive, slot_ready, slot_done)
+    _require_dtype(torch.int32, a_arrive, what="arrival counters")
+    rows, K = A.shape
+    ncols = N // 2 if epilogue == HM_EPI_SWIGLU else N
+    if out is None:
+        out = torch.empty((max(rows, 1), ncols), dtype=torch.bfloat16, device=A.device)
+    _lib.call("hm_grouped_gemm_arrive", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(layout.segs),
+              _ptr(layout.n_seg), _ptr(layout.mtile_prefix), int(epilogue), _ptr(out), _ptr(slot_ready),
+              int(ready_from_slot), int(epoch), _ptr(slot_done), _fetch_ref(fetch), _ptr(a_arrive), int(bool(pdl)),
+              _stream(stream))
+    return out
+
+
 def permute(x, topk_idx, lrank, tile_off, S, slot_base, n_ranks: int, tokens_per_rank: int, src_rank_base: int,
             out_rows: int, out=None, with_inverse: bool = False, index_only: bool = False, stream=None):
     """K4.  Returns (out [out_rows, d] bf16 | None, pos [T,k] i32, inv [out_rows] i32 | None).

@@ -222,3 +222,80 @@ def test_plan_single_gpu_matches_general_kernels(E, tiles, zero_frac):
     assert torch.equal(p.layout.segs[:n], lay.segs[:n])
     assert torch.equal(p.layout.mtile_prefix[: n + 1], lay.mtile_prefix[: n + 1])
     assert torch.equal(p.layout.slot_base, lay.slot_base)
+
+
+@pytest.mark.parametrize("G,E,k,d,Tg,placement", [(2, 16, 4, 256, 384, "blocked"), (4, 32, 2, 512, 256, "round_robin"),
+                                                  (8, 128, 8, 2048, 512, "blocked"), (1, 8, 2, 256, 200, "blocked")])
+def test_ordered_push_matches_push_and_gates_ffn1(G, E, k, d, Tg, placement):
+    """Expert-ordered dispatch (hm_plan_dispatch + hm_dispatch_push_ordered): every destination's
+    receive buffer, row tags and pos equal the unordered push's, each destination's arrival counter
+    of expert e ends at the rows of e it holds, and FFN1 gated by those counters (plain and launched
+    with PDL right behind the last push) is bit-identical to the ungated FFN1."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    gen = torch.Generator(device=dev).manual_seed(G * 100 + E)
+    wg = torch.zeros((ops.e_pad(E), d), dtype=torch.bfloat16, device=dev)
+    wg[:E] = (torch.randn((E, d), device=dev, generator=gen) * 0.05).to(torch.bfloat16)
+    bias = torch.linspace(2.0, -2.0, E, device=dev)  # skewed routing: rebalancing moves buckets
+    xs, routed, hists = [], [], []
+    for g in range(G):
+        x = torch.randn((Tg, d), device=dev, generator=gen).to(torch.bfloat16)
+        idx, _, tile_hist, lrank = ops.router_topk(x, wg, bias, 1, Tg, k, True, E=E)
+        hist, tile_off = ops.hist_scan(tile_hist, 1, (Tg + 127) // 128)
+        xs.append(x)
+        routed.append((idx, lrank, tile_off))
+        hists.append(hist)
+    m_all = torch.cat(hists).contiguous()
+    home_np = orc.blocked_home(E, G) if placement == "blocked" else orc.round_robin_home(E, G)
+    home = torch.from_numpy(home_np.astype(np.int32)).to(dev)
+    cap = G * Tg * k
+    rows_a = [torch.zeros((cap, d), dtype=torch.bfloat16, device=dev) for _ in range(G)]
+    rows_b = [torch.zeros((cap, d), dtype=torch.bfloat16, device=dev) for _ in range(G)]
+    tok_a = [torch.full((cap,), -1, dtype=torch.int32, device=dev) for _ in range(G)]
+    tok_b = [torch.full((cap,), -1, dtype=torch.int32, device=dev) for _ in range(G)]
+    arrive = torch.zeros((G, E), dtype=torch.int32, device=dev)
+    ptrs = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=dev)  # noqa: E731
+    arrive_ptrs = torch.tensor([arrive[g].data_ptr() for g in range(G)], dtype=torch.int64, device=dev)
+    order = torch.empty(Tg * k, dtype=torch.int32, device=dev)
+    sync = torch.zeros(2, dtype=torch.int32, device=dev)
+    plans = []
+    for me in range(G):
+        p, pl = ops.plan_dispatch(home, G, E, 4, True, me, m_all)
+        p_ref = ops.plan(home, G, E, 4, True, ops.HM_LAYOUT_EP_EXPERT, me, m_all=m_all)
+        ns = int(p_ref.layout.n_seg.item())
+        for a, b in ((p.S, p_ref.S), (p.layout.slot_base, p_ref.layout.slot_base),
+                     (p.layout.segs[:ns], p_ref.layout.segs[:ns]), (p.layout.n_seg, p_ref.layout.n_seg),
+                     (p.layout.mtile_prefix[: ns + 1], p_ref.layout.mtile_prefix[: ns + 1])):
+            assert torch.equal(a, b)
+        idx, lrank, tile_off = routed[me]
+        pos_a = torch.empty((Tg, k), dtype=torch.int32, device=dev)
+        pos_b = torch.empty((Tg, k), dtype=torch.int32, device=dev)
+        ops.dispatch_push(xs[me], idx, lrank, tile_off, p.S, p.layout.slot_base, None, me, ptrs(rows_a), ptrs(tok_a),
+                          pos=pos_a)
+        ops.dispatch_push_ordered(xs[me], idx, lrank, tile_off, p.S, p.layout.slot_base, pl, me, ptrs(rows_b),
+                                  ptrs(tok_b), arrive_ptrs, order, sync, pos=pos_b)
+        assert torch.equal(pos_a, pos_b)
+        plans.append(p)
+    torch.cuda.synchronize()
+    S = plans[0].S.cpu().numpy()
+    for dd in range(G):
+        assert torch.equal(rows_a[dd], rows_b[dd]) and torch.equal(tok_a[dd], tok_b[dd])
+        assert np.array_equal(arrive[dd].cpu().numpy(), S[:, :, dd].sum(axis=0))
+    # FFN1 of destination G-1 gated by its arrival counters, vs ungated
+    dd = G - 1
+    lay = plans[dd].layout
+    W = (torch.randn((E * 256, d), device=dev, generator=gen) * 0.05).to(torch.bfloat16)
+    h_ref = ops.grouped_gemm(rows_a[dd], W, 256, lay, ops.HM_EPI_RELU)
+    h1 = ops.grouped_gemm_arrive(rows_b[dd], W, 256, lay, ops.HM_EPI_RELU, arrive[dd], pdl=False)
+    # overlapped: re-push every rank (counters restarted) with FFN1 launched right behind the last push
+    arrive.zero_()
+    for me in range(G):
+        p, pl = ops.plan_dispatch(home, G, E, 4, True, me, m_all)
+        idx, lrank, tile_off = routed[me]
+        ops.dispatch_push_ordered(xs[me], idx, lrank, tile_off, p.S, p.layout.slot_base, pl, me, ptrs(rows_b),
+                                  ptrs(tok_b), arrive_ptrs, order, sync)
+    h2 = ops.grouped_gemm_arrive(rows_b[dd], W, 256, lay, ops.HM_EPI_RELU, arrive[dd], pdl=True)
+    torch.cuda.synchronize()
+    n = int(S[:, :, dd].sum())  # receive rows of dd (dense, expert-major)
+    assert torch.equal(h1[:n], h_ref[:n]) and torch.equal(h2[:n], h_ref[:n])
