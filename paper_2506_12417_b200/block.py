@@ -79,6 +79,12 @@ class MoEConfig:
     # (one-sided pushes into peers' buffers over NVLink/NVSwitch, no host round trip)
     transport: str = "nccl"
     max_tokens_per_rank: int = 16384  # p2p: capacity of the peer-mapped buffers
+    # EP p2p: push the rows expert by expert in every destination's plan order with per-expert
+    # arrival counters, and start FFN1 right behind the push (programmatic dependent launch) so
+    # each expert's tiles run as soon as its rows have landed (hm_dispatch_push_ordered).  None =
+    # on where supported (power-of-two world size, harmony / static policy); HM_OVERLAP_DISPATCH=0/1
+    # overrides.  False: the unordered push, then a token flag exchange, then FFN1.
+    overlap_dispatch: bool | None = None
 
     def __post_init__(self):
         if self.eq_tokens < 1:

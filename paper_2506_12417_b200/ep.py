@@ -32,6 +32,7 @@ inside the GEMM launches (hm_fetch_plan).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -194,6 +195,15 @@ class EPHarMoEnyBlock:
         self.S_host = torch.empty((self.G, E, self.G), dtype=torch.int32, pin_memory=True)
         self.fetch_host = torch.empty(E + 1, dtype=torch.int32, pin_memory=True)
         self.stats = BlockStats()
+        # expert-ordered dispatch overlapped with FFN1 (MoEConfig.overlap_dispatch)
+        env = os.environ.get("HM_OVERLAP_DISPATCH", "")
+        want = (env == "1") if env in ("0", "1") else cfg.overlap_dispatch
+        supported = (cfg.transport == "p2p" and self.G & (self.G - 1) == 0 and
+                     cfg.policy_code != ops.HM_POLICY_EVEN_SPLIT)
+        if want and not supported:
+            raise ValueError("overlap_dispatch needs the p2p transport, a power-of-two world size and the "
+                             "harmony / static policy")
+        self.overlap = supported if want is None else bool(want)
         if cfg.transport == "p2p":
             self._setup_p2p()
             # ours: router, hist_scan, plan, dispatch_push, fetch, gemm1, gemm2, combine
@@ -339,14 +349,16 @@ class EPHarMoEnyBlock:
 
         lay = {}
         off = 0
-        for name, nbytes in (("flags", 3 * G * 4), ("m_all", G * E * 4), ("recv_tok", self.cap_recv * 4),
-                             ("x_recv", self.cap_recv * d * 2), ("y_ret", self.cap_send * d * 2)):
+        for name, nbytes in (("flags", 3 * G * 4), ("m_all", G * E * 4), ("arrive", E * 4),
+                             ("recv_tok", self.cap_recv * 4), ("x_recv", self.cap_recv * d * 2),
+                             ("y_ret", self.cap_send * d * 2)):
             lay[name] = off
             off += al(nbytes)
         self.arena = torch.zeros(off, dtype=torch.uint8, device=self.device)
         a = self.arena
         self.flags = a[lay["flags"]: lay["flags"] + 3 * G * 4].view(torch.int32).view(3, G)
         self.m_all_buf = a[lay["m_all"]: lay["m_all"] + G * E * 4].view(torch.int32).view(G, E)
+        self.arrive = a[lay["arrive"]: lay["arrive"] + E * 4].view(torch.int32)  # rows of each expert landed
         self.recv_tok = a[lay["recv_tok"]: lay["recv_tok"] + self.cap_recv * 4].view(torch.int32)
         self.x_recv = a[lay["x_recv"]: lay["x_recv"] + self.cap_recv * d * 2].view(torch.bfloat16).view(-1, d)
         self.y_ret = a[lay["y_ret"]: lay["y_ret"] + self.cap_send * d * 2].view(torch.bfloat16).view(-1, d)
@@ -357,6 +369,9 @@ class EPHarMoEnyBlock:
         self.p2p_rows = torch.tensor([b + lay["x_recv"] for b in bases], **i64)
         self.p2p_tok = torch.tensor([b + lay["recv_tok"] for b in bases], **i64)
         self.p2p_out = torch.tensor([b + lay["y_ret"] for b in bases], **i64)
+        self.p2p_arrive = torch.tensor([b + lay["arrive"] for b in bases], **i64)
+        self.push_order = torch.empty(self.cap_send, dtype=torch.int32, device=self.device)
+        self.push_sync = torch.zeros(2, dtype=torch.int32, device=self.device)
         me = self.me
         self.meta_addrs = [b + lay["flags"] + (0 * G + me) * 4 for b in bases]
         self.tok_addrs = [b + lay["flags"] + (1 * G + me) * 4 for b in bases]
@@ -392,16 +407,26 @@ class EPHarMoEnyBlock:
             ops.stream_signal(self.local_flag_addrs[0], 0, s)
             # expert-major receive buffers: every sender places its rows from the replicated S, and
             # this rank's GEMMs see one segment per expert (all sources' rows contiguous)
-            p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP_EXPERT, me,
-                         m_all=self.m_all_buf,
-                         cache_slots=self.n_cache if self.bounded else 0, stream=s)
-            m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
+            cache = self.n_cache if self.bounded else 0
             pos = torch.empty((Tg, k), dtype=torch.int32, device=self.device)
-            ops.dispatch_push(x, idx, lrank, tile_off, p.S, p.layout.slot_base, None, me, self.p2p_rows,
-                              self.p2p_tok, pos=pos, stream=s)
-            ops.stream_signal(self.tok_addrs, 1, s)
-            ops.stream_wait(self.flags[1], 1, s)
-            ops.stream_signal(self.local_flag_addrs[1], 0, s)
+            if self.overlap:
+                # rows pushed in every destination's plan order, counted per expert on arrival;
+                # FFN1 (next kernel on this stream, PDL) waits per segment instead of on a flag
+                p, pl = ops.plan_dispatch(self.home, G, E, cfg.eq_tokens, cfg.policy_code, me, self.m_all_buf,
+                                          cache_slots=cache, stream=s)
+                m_all = self.m_all_buf.clone()
+                ops.dispatch_push_ordered(x, idx, lrank, tile_off, p.S, p.layout.slot_base, pl, me, self.p2p_rows,
+                                          self.p2p_tok, self.p2p_arrive, self.push_order, self.push_sync, pos=pos,
+                                          stream=s)
+            else:
+                p = ops.plan(self.home, G, E, cfg.eq_tokens, cfg.policy_code, ops.HM_LAYOUT_EP_EXPERT, me,
+                             m_all=self.m_all_buf, cache_slots=cache, stream=s)
+                m_all = self.m_all_buf.clone()  # peers may push the next forward's rows before the host reads stats
+                ops.dispatch_push(x, idx, lrank, tile_off, p.S, p.layout.slot_base, None, me, self.p2p_rows,
+                                  self.p2p_tok, pos=pos, stream=s)
+                ops.stream_signal(self.tok_addrs, 1, s)
+                ops.stream_wait(self.flags[1], 1, s)
+                ops.stream_signal(self.local_flag_addrs[1], 0, s)
             st.update(idx=idx, w=w, plan=p, m_all=m_all, pos=pos, Tg=Tg)
             self.stats = BlockStats(m_all=m_all, schedule=p.S, iters=p.iters, loads=p.loads,
                                     extras=dict(topk_idx=idx, topk_w=w, pos=pos, layout=p.layout))
@@ -422,8 +447,13 @@ class EPHarMoEnyBlock:
                 ops.fetch_experts(lay.fetch, lay.n_fetch, self.fetch_src_in, self.fetch_src_out, self.n_in * d * 2,
                                   d * cfg.d_ff * 2, self.w_in, self.w_out, self.n_home, self.n_cache, self.ready_in,
                                   self.ready_out, self.fetch_counters, value=1, stream=fs)
-            ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
-                             slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s, **kw)
+            if self.overlap:
+                ops.grouped_gemm_arrive(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, self.arrive,
+                                        out=self.h_buf, slot_ready=self.ready_in, ready_from_slot=self.n_home,
+                                        epoch=1, pdl=True, stream=s, **kw)
+            else:
+                ops.grouped_gemm(self.x_recv, self.w_in.view(-1, d), self.n_in, lay, self.epi_in, out=self.h_buf,
+                                 slot_ready=self.ready_in, ready_from_slot=self.n_home, epoch=1, stream=s, **kw)
             if self.n_cache > 0 and fs is not s and not self.bounded:
                 s.wait_stream(fs)
 
@@ -439,6 +469,8 @@ class EPHarMoEnyBlock:
                 if self.bounded:
                     self.done_in.zero_()
                     self.done_out.zero_()
+            if self.overlap:  # every row of this forward has landed (FFN1 waited for all of them)
+                self.arrive.zero_()
             ops.stream_signal(self.y_addrs, 1, s)
             ops.stream_wait(self.flags[2], 1, s)
             ops.stream_signal(self.local_flag_addrs[2], 0, s)
