@@ -543,11 +543,13 @@ def extra_workloads(args, dev, peaks3):
         sys.path.insert(0, os.path.join(REPO, "tools"))
         from ep_projection import project
 
-        for G_, pl in ((2, "round_robin"), (4, "round_robin"), (8, "round_robin"), (8, "blocked")):
-            pr = project(G=G_, q=32, placement=pl, zipf_s=1.0, peak_tflops=tc)
+        for G_, pl, ov in ((2, "round_robin", False), (4, "round_robin", False), (8, "round_robin", False),
+                           (8, "blocked", False), (8, "round_robin", True)):
+            pr = project(G=G_, q=32, placement=pl, zipf_s=1.0, peak_tflops=tc, overlap=ov)
             crit = pr["per_rank"][pr["critical_rank"]]
-            out[f"C2_ep{G_}_projection_{pl}"] = {
-                "config": f"BASELINE configs[1] at G={G_} (expert-parallel, {pl} placement, q=32): the critical "
+            out[f"C2_ep{G_}_projection_{pl}" + ("_ordered_dispatch_overlap" if ov else "")] = {
+                "config": f"BASELINE configs[1] at G={G_} (expert-parallel, {pl} placement, q=32, "
+                          f"{pr['config']['dispatch']}): the critical "
                           f"rank's kernels measured at per-rank size on one B200, NVLink at 900 GB/s and "
                           f"{pr['config']['handshake_us']} us per cross-rank handshake modelled",
                 "projected_step_us": pr["projected_step_us"], "projected_tokens_per_s": pr["projected_tokens_per_s"],

@@ -303,12 +303,12 @@ HM_API int hm_dispatch_push(const void* x, const int32_t* topk_idx, const int32_
  *   push_items [G*E, 4] int32: item v = p*G + d is me's bucket of the expert at position p of
  *     destination d's plan order (engine.py:233-234): (expert, first rank among me's assignments
  *     to it, rows, first row in d's receive buffer); rows 0 where d has fewer than p+1 experts;
- *   push_cprefix [G*E + 1]: exclusive prefix of 32-row units per item (-1 at [G*E] if the batch
+ *   push_cprefix [G*E + 1]: exclusive prefix of 8-row units per item (-1 at [G*E] if the batch
  *     left the planner's fast path: >= 2^21 assignments, which the push then reports by trapping);
  *   push_ebase [E + 1]: exclusive prefix of m_all[me] over experts.
  * Requires a power-of-two G and a harmony / static policy.
- * hm_dispatch_push_ordered copies the rows unit by unit in that order (32 rows of one bucket per
- * unit) into dst_rows[d] / tags dst_tok[d] as hm_dispatch_push with dst_delta == NULL does, and
+ * hm_dispatch_push_ordered copies the rows unit by unit in that order (8 rows of one bucket per
+ * unit, one warp each) into dst_rows[d] / tags dst_tok[d] as hm_dispatch_push with dst_delta == NULL does, and
  * after each unit adds its row count to ((int32_t*)dst_arrive[d])[expert] (system-scope release).
  * order [tokens*k] int32 scratch; pos [tokens*k] or NULL as hm_dispatch_push; sync [2] uint32
  * scratch (zeroed by the call).  One CTA per SM with a grid barrier: launch it right before the

@@ -81,10 +81,11 @@ class MoEConfig:
     max_tokens_per_rank: int = 16384  # p2p: capacity of the peer-mapped buffers
     # EP p2p: push the rows expert by expert in every destination's plan order with per-expert
     # arrival counters, and start FFN1 right behind the push (programmatic dependent launch) so
-    # each expert's tiles run as soon as its rows have landed (hm_dispatch_push_ordered).  None =
-    # on where supported (power-of-two world size, harmony / static policy); HM_OVERLAP_DISPATCH=0/1
-    # overrides.  False: the unordered push, then a token flag exchange, then FFN1.
-    overlap_dispatch: bool | None = None
+    # each expert's tiles run as soon as its rows have landed (hm_dispatch_push_ordered; needs a
+    # power-of-two world size and the harmony / static policy).  Off by default: measured slower
+    # than the unordered push + token flags + FFN1 (profiles/r2_experiments.txt).
+    # HM_OVERLAP_DISPATCH=0/1 overrides.
+    overlap_dispatch: bool = False
 
     def __post_init__(self):
         if self.eq_tokens < 1:

@@ -129,20 +129,29 @@ __global__ void __launch_bounds__(kPushWarps * 32)
 // expert-ordered dispatch push (overlapped with FFN1).  The unordered push above finishes every
 // expert's rows at about the same time (token order), so FFN1 can only start after the whole
 // all-to-all.  Here every sender walks its work list in the DESTINATIONS' plan order (item
-// p*G + d = its bucket of the p-th expert of destination d, hm_plan_dispatch), 32 rows per work
+// p*G + d = its bucket of the p-th expert of destination d, hm_plan_dispatch), 8 rows per work
 // unit, and after each unit adds the row count to the destination's per-expert arrival counter
 // (system-scope release after the rows).  FFN1 is launched right behind this kernel with
 // programmatic dependent launch and its producer waits per segment for arrive[e] == rows of e,
 // so the first experts' tiles start while later experts are still in flight over NVLink.
 //   phase 1: order[ebase[e] + r] = t*k + j for this rank's r-th assignment to e (and pos);
-//   grid barrier (one CTA per SM, all resident: launched before its dependent GEMM);
-//   phase 2: 32-row units by a global counter, in (position, destination) order.
+//   grid barrier (all CTAs resident: launched on dedicated TPCs before its dependent GEMM);
+//   phase 2: 8-row units (one warp each) dealt round-robin in (position, destination) order.
 // ------------------------------------------------------------------------------------------
-constexpr int kOPushThreads = 256;
-constexpr int kOPushRows = 32;
+// One CTA per SM of 4 warps (one per SM sub-partition) of <= 64 registers, so that the FFN1 pair
+// CTA launched behind it with PDL fits beside it: each sub-partition has 16K registers and the
+// GEMM CTA holds 3 warps x 4,608 of them on two of its sub-partitions; the push also asks for the
+// maximal shared-memory carveout (tools/pdl_probe: the GEMM's CTAs then start ~3 us after the
+// push instead of after it).  Measured alternative: the push on 4-16 dedicated TPCs of full-SM
+// CTAs (GEMM on the others) - 93-241 us for one rank's rows, far slower.
+constexpr int kOPushThreads = 128;
+// rows per work unit (one warp, one arrival increment).  Units are dealt round-robin over the
+// grid's warps, so ~#warps units are in flight at once: small units keep the completion order
+// close to the plan order (the first experts land after ~1/4 of the push, not at its end)
+constexpr int kOPushRows = 8;
 
 template <int VEC>
-__global__ void __launch_bounds__(kOPushThreads, 4)  // <= 64 registers: co-resident with the FFN1 pairs
+__global__ void __launch_bounds__(kOPushThreads, 8)  // <= 64 registers: co-resident with the FFN1 pairs
     dispatch_push_ordered_kernel(const uint4* __restrict__ x, const int32_t* __restrict__ topk_idx,
                                  const int32_t* __restrict__ lrank, const int32_t* __restrict__ tile_off,
                                  const int32_t* __restrict__ S, const int32_t* __restrict__ slot_base,
@@ -153,7 +162,6 @@ __global__ void __launch_bounds__(kOPushThreads, 4)  // <= 64 registers: co-resi
                                  const unsigned long long* __restrict__ dst_arrive, int32_t* __restrict__ order,
                                  int32_t* __restrict__ pos, unsigned* __restrict__ sync) {
   griddep_launch_dependents();
-  __shared__ int s_unit;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // ---- phase 1: per-expert assignment order (+ pos: the row of each assignment in its
   // destination's receive buffer, as the unordered push reports it)
@@ -189,30 +197,49 @@ __global__ void __launch_bounds__(kOPushThreads, 4)  // <= 64 registers: co-resi
     }
   }
   __syncthreads();
+#ifdef HM_OPUSH_ONLY_P1  // diagnostics: phase 1 + barrier only
+  return;
+#endif
   const int total = __ldcg(cprefix + n_items);
   if (total < 0) {
     if (threadIdx.x == 0) printf("hm dispatch_push_ordered: no push work list (planner took the general path)\n");
     __trap();
   }
-  // ---- phase 2: 32-row units in (position, destination) order
-  int it = 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_unit = (int)atomicAdd(sync + 1, 1u);
-    __syncthreads();
-    const int u = s_unit;
-    __syncthreads();
-    if (u >= total) break;
-    while (__ldg(cprefix + it + 1) <= u) ++it;  // units only grow for this CTA: amortised O(1)
+  // ---- phase 2: 8-row units in (position, destination) order, one warp per unit (the release
+  // after a unit stalls only its warp), dealt round-robin over the grid's warps in order
+  const int nwarps = gridDim.x * (kOPushThreads / 32);
+  int it = 0;  // item of the warp's current unit: units only grow, so the search moves forward
+  for (int u = blockIdx.x * (kOPushThreads / 32) + warp; u < total; u += nwarps) {
+    // 32-ary search from the previous item (cprefix is non-decreasing, so the lanes whose probe
+    // is <= u are a prefix): each step narrows the range 32-fold with one coalesced probe
+    for (int span = n_items - it; span > 0;) {
+      const int step = (span + 31) >> 5;
+      const int j = it + (lane + 1) * step;
+      const unsigned b = __ballot_sync(0xffffffffu, j <= n_items && __ldg(cprefix + j) <= u);
+      const int n = __popc(b);
+      it += n * step;
+      span = (n == 32 ? span - 32 * step : step - 1);
+      if (step == 1) break;
+    }
     const int4 item = __ldg(items + it);
     const int d = it & (G - 1);
     const int r0 = (u - __ldg(cprefix + it)) * kOPushRows;
     const int nr = min(kOPushRows, item.z - r0);
     const int e = item.x;
     const int ob = __ldg(ebase + e) + item.y + r0;
-    uint4* dst = reinterpret_cast<uint4*>(__ldg(dst_rows + d));
+    uint4* dst = reinterpret_cast<uint4*>(__ldg(dst_rows + d)) + (int64_t)(item.w + r0) * n16;
     int32_t* tok = reinterpret_cast<int32_t*>(__ldg(dst_tok + d));
-    for (int rr = warp; rr < nr; rr += kOPushThreads / 32) {
-      const int a = __ldcg(order + ob + rr);
+    const int my_a = lane < nr ? __ldcg(order + ob + lane) : 0;  // the unit's assignment indices
+#ifdef HM_OPUSH_NO_ROWS  // diagnostics: work distribution + counts only
+#ifdef HM_OPUSH_GPU_SCOPE
+    if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(reinterpret_cast<int*>(__ldg(dst_arrive + d)) + e), "r"(nr) : "memory");
+#else
+    if (lane == 0) red_release_sys_add(reinterpret_cast<int*>(__ldg(dst_arrive + d)) + e, nr);
+#endif
+    continue;
+#endif
+    for (int rr = 0; rr < nr; ++rr) {  // a row's VEC 16-byte loads per lane in flight, then its stores
+      const int a = __shfl_sync(0xffffffffu, my_a, rr);
       const uint4* src = x + (int64_t)(a / k) * n16;
       uint4 v[VEC];
 #pragma unroll
@@ -220,18 +247,27 @@ __global__ void __launch_bounds__(kOPushThreads, 4)  // <= 64 registers: co-resi
         const int c = i * 32 + lane;
         if (c < n16) v[i] = ld_global_nc_v4(src + c);
       }
-      uint4* drow = dst + (int64_t)(item.w + r0 + rr) * n16;
+      uint4* drow = dst + (int64_t)rr * n16;
 #pragma unroll
       for (int i = 0; i < VEC; ++i) {
         const int c = i * 32 + lane;
         if (c < n16) drow[c] = v[i];
       }
-      if (lane == 0) tok[item.w + r0 + rr] = (int32_t)(((uint32_t)me << 24) | (uint32_t)a);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();  // every row of the unit (bar.sync above) before the count
-      red_release_sys_add(reinterpret_cast<int*>(__ldg(dst_arrive + d)) + e, nr);
+    if (lane < nr) tok[item.w + r0 + lane] = (int32_t)(((uint32_t)me << 24) | (uint32_t)my_a);
+    // every lane's rows (ordered before lane 0 by the warp barrier) before the count: the
+    // release is cumulative over them
+    __syncwarp();
+    if (lane == 0) {
+      int* cnt = reinterpret_cast<int*>(__ldg(dst_arrive + d)) + e;
+#ifdef HM_OPUSH_GPU_SCOPE
+      if (true)
+#else
+      if (d == me)  // this GPU's own buffer: device scope suffices (its FFN1 reads it)
+#endif
+        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(cnt), "r"(nr) : "memory");
+      else
+        red_release_sys_add(cnt, nr);
     }
   }
 }
@@ -348,10 +384,17 @@ int launch_dispatch_push_ordered(const void* x, const int32_t* topk_idx, const i
   const int grid = num_sms();
   const auto* xs = reinterpret_cast<const uint4*>(x);
   const int4* it4 = reinterpret_cast<const int4*>(items);
-#define HM_OPUSH(V)                                                                                            \
-  dispatch_push_ordered_kernel<V><<<grid, kOPushThreads, 0, stream>>>(                                         \
-      xs, topk_idx, lrank, tile_off, S, slot_base, it4, cprefix, ebase, G * E, tokens, me, G, E, k, n16, dst_rows, \
-      dst_tok, dst_arrive, order, pos, sync)
+  // maximal shared-memory carveout: an SM configured for this kernel's (tiny) shared memory could
+  // not take the FFN1 CTAs (~224 KB) launched behind it until the push left the SM
+  cudaError_t le = cudaSuccess;
+#define HM_OPUSH(V)                                                                                              \
+  do {                                                                                                           \
+    cudaFuncSetAttribute(dispatch_push_ordered_kernel<V>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  \
+    dispatch_push_ordered_kernel<V><<<grid, kOPushThreads, 0, stream>>>(                                         \
+        xs, topk_idx, lrank, tile_off, S, slot_base, it4, cprefix, ebase, G * E, tokens, me, G, E, k, n16,        \
+        dst_rows, dst_tok, dst_arrive, order, pos, reinterpret_cast<unsigned*>(sync));                           \
+    le = cudaGetLastError();                                                                                     \
+  } while (0)
   if (n16 <= 32) HM_OPUSH(1);
   else if (n16 <= 64) HM_OPUSH(2);
   else if (n16 <= 128) HM_OPUSH(4);
@@ -359,6 +402,7 @@ int launch_dispatch_push_ordered(const void* x, const int32_t* topk_idx, const i
   else if (n16 <= 512) HM_OPUSH(16);
   else return set_error(HM_EINVAL, "dispatch_push_ordered: d > 4096 unsupported");
 #undef HM_OPUSH
+  if (le != cudaSuccess) return set_error(HM_ECUDA, "dispatch_push_ordered launch: %s", cudaGetErrorString(le));
   return check_launch("dispatch_push_ordered");
 }
 

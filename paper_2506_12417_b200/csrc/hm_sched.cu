@@ -422,7 +422,7 @@ struct LayoutOut {
   // dispatch (hm_dispatch_push_ordered).  Item v = p*G + d is the bucket (me -> d) of the expert at
   // position p of destination d's plan order: (expert, first rank c0 among me's assignments to it,
   // rows, first row in d's receive buffer), rows 0 where d has no p-th expert;
-  // push_cprefix[v] = sum of 32-row chunks of items < v; push_ebase[e] = sum_{e'<e} m_all[me][e'].
+  // push_cprefix[v] = sum of 8-row units of items < v; push_ebase[e] = sum_{e'<e} m_all[me][e'].
   int4* push_items;
   int32_t* push_cprefix;
   int32_t* push_ebase;
@@ -1028,7 +1028,7 @@ __device__ void dev_layout_t(const int* St, int Ep, const int* home, int G, int 
   if (o.push_items != nullptr) {
     // push work list for the expert-ordered dispatch: every destination's plan order (keys of
     // all (d, e); s_key is free again), this rank's bucket of each (position, destination)
-    int* s_pc = s_hr + E;  // [GE + 1] 32-row chunks per item
+    int* s_pc = s_hr + E;  // [GE + 1] 8-row push units per item
     for (int e = L.e0; e < E; e += L.step) s_key[L.d * Ep + e] = plan_key32(home[e] == L.d, s_n[L.d * Ep + e], e);
     for (int v = tid; v < GE; v += blockDim.x) {
       o.push_items[v] = make_int4(0, 0, 0, 0);
@@ -1058,7 +1058,7 @@ __device__ void dev_layout_t(const int* St, int Ep, const int* home, int G, int 
       int row0 = s_off[d * Ep + e];
       for (int g = 0; g < me; ++g) row0 += St[(g * G + d) * Ep + e];
       o.push_items[pos * G + d] = make_int4(e, c0, cnt, row0);
-      s_pc[pos * G + d] = (cnt + 31) >> 5;
+      s_pc[pos * G + d] = (cnt + 7) >> 3;  // 8-row push units (hm_dispatch_push_ordered)
     }
     __syncthreads();
     block_scan_to(s_pc, GE, o.push_cprefix, s_tmp);

@@ -203,7 +203,7 @@ class EPHarMoEnyBlock:
         if want and not supported:
             raise ValueError("overlap_dispatch needs the p2p transport, a power-of-two world size and the "
                              "harmony / static policy")
-        self.overlap = supported if want is None else bool(want)
+        self.overlap = bool(want)
         if cfg.transport == "p2p":
             self._setup_p2p()
             # ours: router, hist_scan, plan, dispatch_push, fetch, gemm1, gemm2, combine

@@ -234,7 +234,7 @@ def plan_dispatch(home, G: int, E: int, q: int, rebalance, me: int, m_all, cache
 def dispatch_push_ordered(x, topk_idx, lrank, tile_off, S, slot_base, push: PushList, me: int, dst_rows, dst_tok,
                           dst_arrive, order, sync, pos=None, stream=None):
     """Expert-ordered fused scatter + dispatch: the rows of hm_dispatch_push (EP_EXPERT layout)
-    in every destination's plan order, 32-row units, each followed by a system-scope add of its
+    in every destination's plan order, 8-row units (one warp each), each followed by a system-scope add of its
     row count to the destination's arrival counter dst_arrive[d][expert]."""
     _require_cuda(x, topk_idx, lrank, tile_off, S, slot_base, dst_rows, dst_tok, dst_arrive, order, sync, pos)
     T, d = x.shape

@@ -44,7 +44,7 @@ def _worker(rank, world, port, fetch_source, transport, out_q, cache=0):
 
         cfg = MoEConfig(rank=rank, world_size=world, fetch_source=fetch_source, transport=transport.split("-")[0],
                         max_tokens_per_rank=T // world, async_fetch="sync" not in transport,
-                        expert_cache_size=cache, overlap_dispatch=False if "noov" in transport else None, **KW)
+                        expert_cache_size=cache, overlap_dispatch="-ov" in transport, **KW)
         blk = EPHarMoEnyBlock.random(cfg, seed=7, device="cuda", zipf_s=1.3, std=0.05)
         g = torch.Generator(device="cuda").manual_seed(99)
         x = torch.randn((T, 256), device="cuda", generator=g).to(torch.bfloat16)
@@ -69,16 +69,16 @@ def _worker(rank, world, port, fetch_source, transport, out_q, cache=0):
 @pytest.mark.parametrize("fetch_source,transport,world,cache", [
     ("peer", "nccl", 2, 0), ("host", "nccl", 2, 0), ("peer", "p2p", 2, 0), ("host", "p2p", 2, 0),
     ("peer", "p2p", 4, 0), ("peer", "p2p-graph", 2, 0), ("host", "p2p-graph", 4, 0), ("peer", "nccl-sync", 2, 0),
-    ("peer", "p2p-sync", 2, 0), ("peer", "p2p-noov", 2, 0), ("host", "p2p-graph-noov", 4, 0),
+    ("peer", "p2p-sync", 2, 0), ("peer", "p2p-ov", 2, 0), ("host", "p2p-graph-ov", 4, 0), ("peer", "p2p-ov", 4, 1),
     # bounded expert cache (engine.py:204-275 overwrite semantics): fewer slots than fetches
     ("peer", "nccl", 2, 1), ("host", "nccl", 4, 1), ("peer", "p2p", 2, 1), ("host", "p2p", 4, 1),
     ("peer", "p2p-graph", 2, 1), ("peer", "p2p-graph", 4, 1), ("peer", "nccl", 4, 1)])
 def test_ep_ranks_one_gpu_bit_identical(fetch_source, transport, world, cache):
     """transport "nccl": exchanges through the process group (gloo here, host-staged);
     transport "p2p": one-sided pushes into the other ranks' IPC-mapped buffers + stream flags,
-    no collective and no host round trip inside the forward; by default with the expert-ordered
-    dispatch overlapped with FFN1 (per-expert arrival counters, PDL), "-noov" the unordered push
-    + token flag exchange.  "-sync": the synchronous-loading
+    no collective and no host round trip inside the forward; "-ov": the expert-ordered dispatch
+    overlapped with FFN1 (per-expert arrival counters, PDL) instead of the unordered push + token
+    flag exchange.  "-sync": the synchronous-loading
     ablation (expert fetches in stream order ahead of FFN1, SimFlags.async_loading_enabled=False).
     cache > 0: expert_cache_size slots, fewer than the experts a rank fetches, so fetches reuse
     slots as the GEMMs finish their occupants; outputs stay bit-identical."""

@@ -58,8 +58,55 @@ def _graph_time_us(fn, flush, reps=10):
     return float(np.median(ts))
 
 
+def _plan_orders(S, home_np):
+    """Every destination's plan order (engine.py:233-234): residents with work by (-rows, e), then
+    the other experts with work by (-rows, e)."""
+    G, E, _ = S.shape
+    orders = []
+    for d in range(G):
+        n = S[:, :, d].sum(axis=0)
+        keys = sorted((0 if home_np[e] == d else 1, -int(n[e]), e) for e in range(E) if n[e] > 0)
+        orders.append([e for _, _, e in keys])
+    return orders
+
+
+def _arrival_times(S, home_np, me, bytes_tok, nvlink_gbs, warps=592, unit_rows=8):
+    """Expert-ordered dispatch (hm_dispatch_push_ordered): the time (us from the push start) at
+    which every row of each of rank me's experts has landed.  Every sender walks its units (8 rows of
+    one bucket) in (position, destination) order, dealt round-robin over its `warps` warps, so ~one
+    round of `warps` units is in flight at a time and completes together: a unit lands when the
+    sender's remote bytes up to the end of its round have left at nvlink_gbs.  Rank me's inbound
+    link carries nvlink_gbs too; local rows (g == me) cost no NVLink time."""
+    G, E, _ = S.shape
+    orders = _plan_orders(S, home_np)
+    P = max(len(o) for o in orders)
+    bw = nvlink_gbs * 1e3  # bytes per us
+    done = np.zeros((G, P))  # sender g: completion time of its item (p, me)
+    for g in range(G):
+        unit_bytes, last_unit = [], {}
+        for p in range(P):
+            for d in range(G):
+                if p >= len(orders[d]):
+                    continue
+                rows = int(S[g, orders[d][p], d])
+                for r0 in range(0, rows, unit_rows):
+                    unit_bytes.append(min(unit_rows, rows - r0) * bytes_tok if d != g else 0)
+                if d == me and rows:
+                    last_unit[p] = len(unit_bytes) - 1
+        cum = np.cumsum(unit_bytes) if unit_bytes else np.zeros(1)
+        for p, u in last_unit.items():
+            end = min(len(unit_bytes), (u // warps + 1) * warps) - 1
+            done[g, p] = cum[end] / bw
+    arrive = {}
+    inbound = 0.0
+    for p, e in enumerate(orders[me]):
+        inbound += sum(S[g, e, me] for g in range(G) if g != me) * bytes_tok
+        arrive[e] = max(max(done[g, p] for g in range(G) if g != me) if G > 1 else 0.0, inbound / bw)
+    return arrive, orders[me]
+
+
 def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placement="round_robin", zipf_s=1.0,
-            nvlink_gbs=900.0, handshake_us=4.0, peak_tflops=None, ranks=None, seed=0):
+            nvlink_gbs=900.0, handshake_us=4.0, peak_tflops=None, ranks=None, seed=0, overlap=False):
     dev = torch.device("cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     cfg = MoEConfig(d_model=d, d_ff=f, num_experts=E, top_k=k, activation=act, eq_tokens=q, placement=placement,
@@ -84,7 +131,9 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
     home_np = placement_home(cfg)
     bytes_tok = d * 2
     out = {"config": dict(d_model=d, d_ff=f, experts=E, top_k=k, tokens=T, G=G, q=q, placement=placement,
-                          zipf_s=zipf_s, nvlink_gbs=nvlink_gbs, handshake_us=handshake_us)}
+                          zipf_s=zipf_s, nvlink_gbs=nvlink_gbs, handshake_us=handshake_us,
+                          dispatch="expert-ordered push overlapped with FFN1" if overlap else "push, then FFN1")}
+    overlap = overlap and G & (G - 1) == 0
     # rank-independent kernels
     xr = x[:Tg].contiguous()
     out["router_us"] = _graph_time_us(lambda: ops.router_topk(xr, wgp, bias, 1, Tg, k, k > 1, E=E), flush)
@@ -102,8 +151,12 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
     expert_bytes = (n_in * d + d * f) * 2
     for me in ranks:
         r = {}
-        r["plan_us"] = _graph_time_us(lambda: ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, mode, me,
-                                                       m_all=m_all), flush)
+        if overlap:
+            r["plan_us"] = _graph_time_us(lambda: ops.plan_dispatch(home, G, E, q, ops.HM_POLICY_REBALANCE, me,
+                                                                    m_all), flush)
+        else:
+            r["plan_us"] = _graph_time_us(lambda: ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, mode, me,
+                                                           m_all=m_all), flush)
         p = ops.plan(home, G, E, q, ops.HM_POLICY_REBALANCE, mode, me, m_all=m_all)
         lay = p.layout
         n_seg = int(lay.n_seg.item())
@@ -140,6 +193,30 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
         h = torch.empty((max(rows, 1), n_in // (2 if act == "swiglu" else 1)), dtype=torch.bfloat16, device=dev)
         y = torch.empty((max(rows, 1), d), dtype=torch.bfloat16, device=dev)
         r["ffn1_us"] = _graph_time_us(lambda: ops.grouped_gemm(a, w_in, n_in, lay, epi, out=h), flush)
+        if overlap:
+            # the push of my tokens (into G local stand-ins) with my FFN1 launched right behind it
+            # (PDL), its arrival counters pre-filled with the rows the other senders deliver: what
+            # one GPU can measure of the overlap (SM / HBM sharing of push and GEMM)
+            _, pl = ops.plan_dispatch(home, G, E, q, ops.HM_POLICY_REBALANCE, me, m_all)
+            n_e = S[:, :, me].sum(axis=0)
+            pre = torch.from_numpy((n_e - S[me, :, me]).astype(np.int32)).to(dev)
+            arrive = torch.zeros((G, E), dtype=torch.int32, device=dev)
+            arrive_ptrs = torch.tensor([arrive[g_].data_ptr() for g_ in range(G)], **i64)
+            order = torch.empty(Tg * k, dtype=torch.int32, device=dev)
+            sync = torch.zeros(2, dtype=torch.int32, device=dev)
+            a_me = bufs[me]
+
+            def push():
+                ops.dispatch_push_ordered(x_me, idx_me, lrank_me, toff_me, p.S, lay.slot_base, pl, me, dst_rows,
+                                          dst_tok, arrive_ptrs, order, sync)
+
+            def push_ffn1():
+                arrive[me].copy_(pre)
+                push()
+                ops.grouped_gemm_arrive(a_me, w_in, n_in, lay, epi, arrive[me], out=h, pdl=True)
+
+            r["push_ordered_local_us"] = _graph_time_us(lambda: (arrive.zero_(), push()), flush)
+            r["push_ffn1_local_us"] = _graph_time_us(push_ffn1, flush)
         r["ffn2_us"] = _graph_time_us(lambda: ops.grouped_gemm(h, w_out, d, lay, ops.HM_EPI_STORE, out=y), flush)
         # resident experts' share of FFN1 (their segments come first in plan order)
         n_res_seg = int(sum(1 for s_ in segs if s_[2] < n_home))
@@ -163,6 +240,19 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
             t = max(t, j * t_one + t_in) + share
         r["fetch_nvlink_us"] = n_fetch * t_one
         r["ffn1_with_fetch_us"] = max(t, r["ffn1_us"])
+        if overlap:
+            # FFN1 timeline from the push start: expert e's share (its rows of FFN1, the measured
+            # co-running FFN1 time) starts once its rows have landed and, if fetched, its gate/up
+            # block (fetch channel as above, starting with the push)
+            arr, order_me = _arrival_times(S, home_np, me, bytes_tok, nvlink_gbs)
+            f1 = max(r["push_ffn1_local_us"], r["ffn1_us"])
+            fetch_ready = {e: j * t_one + t_in for j, e in enumerate(fetched)}
+            seg_rows = {int(s_[3]): int(s_[1]) for s_ in segs}
+            t = 0.0
+            for e in order_me:
+                t = max(t, arr[e], fetch_ready.get(e, 0.0)) + f1 * seg_rows.get(e, 0) / max(rows, 1)
+            r["last_arrival_us"] = max(arr.values()) if arr else 0.0
+            r["dispatch_ffn1_us"] = max(t, f1, r["dispatch_nvlink_us"])
         # FFN2 needs every down block; its rows for other ranks go back over NVLink in the epilogue
         back = rows - int(S[me, :, me].sum())
         r["return_nvlink_us"] = back * bytes_tok / (nvlink_gbs * 1e3)
@@ -170,14 +260,20 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
         # (last in plan order) after its resident share
         tail = r["ffn2_us"] * fetched_rows / max(rows, 1)
         r["ffn2_with_fetch_us"] = max(r["ffn2_us"], r["return_nvlink_us"],
-                                      n_fetch * t_one - r["ffn1_with_fetch_us"] + tail)
+                                      n_fetch * t_one - (r["dispatch_ffn1_us"] if overlap else r["ffn1_with_fetch_us"])
+                                      + tail)
         yk = torch.randn((Tg * k, d), device=dev).to(torch.bfloat16)
         w_me = w[sl].contiguous()
         r["combine_us"] = _graph_time_us(lambda: ops.combine(yk, None, w_me), flush)
-        r["handshakes_us"] = 3 * handshake_us
-        r["step_us"] = (out["router_us"] + r["handshakes_us"] + r["plan_us"] +
-                        max(r["dispatch_local_us"], r["dispatch_nvlink_us"]) + r["ffn1_with_fetch_us"] +
-                        r["ffn2_with_fetch_us"] + r["combine_us"])
+        if overlap:  # metadata and output flags; the token flag is replaced by the arrival counters
+            r["handshakes_us"] = 2 * handshake_us
+            r["step_us"] = (out["router_us"] + r["handshakes_us"] + r["plan_us"] + r["dispatch_ffn1_us"] +
+                            r["ffn2_with_fetch_us"] + r["combine_us"])
+        else:
+            r["handshakes_us"] = 3 * handshake_us
+            r["step_us"] = (out["router_us"] + r["handshakes_us"] + r["plan_us"] +
+                            max(r["dispatch_local_us"], r["dispatch_nvlink_us"]) + r["ffn1_with_fetch_us"] +
+                            r["ffn2_with_fetch_us"] + r["combine_us"])
         r["gemm_flops"] = rows * (f1_flops_per_row + f2_flops_per_row)
         per_rank[me] = r
         del bufs, toks, a, h, y, w_in, w_out
@@ -202,8 +298,9 @@ def main():
     ap.add_argument("--q", type=int, default=32)
     ap.add_argument("--zipf", type=float, default=1.0)
     ap.add_argument("--peak", type=float, default=1631.3)
+    ap.add_argument("--overlap", action="store_true", help="expert-ordered push overlapped with FFN1 (opt-in)")
     a = ap.parse_args()
-    res = project(G=a.G, q=a.q, placement=a.placement, zipf_s=a.zipf, peak_tflops=a.peak)
+    res = project(G=a.G, q=a.q, placement=a.placement, zipf_s=a.zipf, peak_tflops=a.peak, overlap=a.overlap)
     print(json.dumps(res))
 
 
