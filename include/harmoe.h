@@ -236,6 +236,8 @@ HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t
  *   y[t, chunk] = (residual[t, chunk] +) sum_{j<k} topk_w[t, j] * Y[t*k + j, chunk]
  * in fp32 in slot order - bit-identical to hm_combine(Y, NULL, topk_w, ...) after hm_grouped_gemm.
  *   counters [T * N/64] uint32, zero before the first call; every call leaves them zero again.
+ *   k == 1 (top-1, Switch): the epilogue writes y[t] = (residual[t] +) w[t] * Y_row directly (same
+ *   arithmetic, bit-identical); Y is not written and may be NULL, counters may be NULL.
  *   residual [T, N] bf16 or NULL; y [T, N] bf16.  Requires 1 <= k <= 32.
  */
 HM_API int hm_grouped_gemm_combine(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,

@@ -90,6 +90,8 @@ def load(path: str = LIB_PATH):
             )
         L = ctypes.CDLL(path)
         for name, args in SIGNATURES.items():
+            if os.environ.get("HM_LIB_PATH") and not hasattr(L, name):
+                continue  # an older variant build (A/B diagnostics) may lack newer entry points
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = _RESTYPE.get(name, ctypes.c_int)

@@ -212,7 +212,8 @@ int hm_grouped_gemm_combine(const void* A, int64_t a_rows, const void* W, int64_
                             const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, void* Y,
                             const int32_t* row_map, const float* topk_w, int k, const void* residual, void* y,
                             uint32_t* counters, void* stream) {
-  if (y == nullptr || Y == nullptr) return set_error(HM_EINVAL, "grouped_gemm_combine: Y and y are required");
+  if (y == nullptr || (Y == nullptr && k != 1))
+    return set_error(HM_EINVAL, "grouped_gemm_combine: y (and Y unless k == 1) are required");
   const CombineFuse cf{topk_w, residual, y, counters, k};
   return launch_grouped_gemm(A, a_rows, W, w_rows, N, K, segs, n_seg, mtile_prefix, 0 /* STORE */, Y, row_map,
                              nullptr, 1, nullptr, 0, 0, as_stream(stream), nullptr, nullptr, 0, nullptr, nullptr,

@@ -859,9 +859,21 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
           row &= 0xFFFFFF;
         }
       }
+      // top-1 combine in the epilogue (cf.k == 1): row -> token t, y[t] = (residual[t] +) w[t] * Y,
+      // the arithmetic of combine_dense_kernel (bit-identical), Y never written
+      const bool direct = kEpi == kEpiStore && cf.y != nullptr && cf.k == 1;
+      if (direct) obuf = reinterpret_cast<__nv_bfloat16*>(cf.y);
       // per-row output address (rows of one warp may belong to different ranks' buffers)
       const unsigned long long obase = reinterpret_cast<unsigned long long>(
           obuf + (row * ldo + (int64_t)nb * kOutCols + ocol0));
+      float w_row = 0.0f;
+      unsigned long long rbase = 0ull;
+      if (direct && valid) {
+        w_row = __ldg(cf.w + row);
+        if (cf.residual != nullptr)
+          rbase = reinterpret_cast<unsigned long long>(reinterpret_cast<const __nv_bfloat16*>(cf.residual) +
+                                                       (row * ldo + (int64_t)nb * kOutCols + ocol0));
+      }
       const int nvalid = max(0, min(32, rows - (r_in_tile - lane)));
       const int acc = i & 1;
       mbar_wait(&tfull[acc], (i >> 1) & 1);
@@ -894,6 +906,35 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
           const int rr = it * 8 + (lane >> 2);
           const int piece = lane & 3;
           const unsigned long long ob = __shfl_sync(0xffffffffu, obase, rr);
+          if (direct) {
+            const float wv = __shfl_sync(0xffffffffu, w_row, rr);
+            const unsigned long long rb = __shfl_sync(0xffffffffu, rbase, rr);
+            if (rr < nvalid) {
+              const uint4 v = ld_shared_v4(stg + rr * kStgPitch + piece * 16);
+              float acc[8];
+              if (rb != 0ull) {
+                const uint4 rv = ld_global_nc_v4(reinterpret_cast<const __nv_bfloat16*>(rb) + c0 + piece * 8);
+                const uint32_t r4[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                  acc[2 * h] = bf16lo(r4[h]);
+                  acc[2 * h + 1] = bf16hi(r4[h]);
+                }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 8; ++h) acc[h] = 0.0f;
+              }
+              const uint32_t y4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                acc[2 * h] = __fadd_rn(acc[2 * h], __fmul_rn(wv, bf16lo(y4[h])));
+                acc[2 * h + 1] = __fadd_rn(acc[2 * h + 1], __fmul_rn(wv, bf16hi(y4[h])));
+              }
+              st_global_v4(reinterpret_cast<__nv_bfloat16*>(ob) + c0 + piece * 8, pack_bf16x2(acc[0], acc[1]),
+                           pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+            }
+            continue;
+          }
           if (rr < nvalid) {
             const uint4 v = ld_shared_v4(stg + rr * kStgPitch + piece * 16);
             st_global_v4(reinterpret_cast<__nv_bfloat16*>(ob) + c0 + piece * 8, v.x, v.y, v.z, v.w);
@@ -901,7 +942,7 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
         }
         __syncwarp();
       }
-      if (kEpi == kEpiStore && cf.y != nullptr) {
+      if (kEpi == kEpiStore && cf.y != nullptr && !direct) {
         // fused combine: this warp's rows are stored for columns [nb*256 + ocol0, + ncols); each
         // (token, 64-column chunk) counts its k expert rows and the k-th arrival combines the
         // chunk in slot order - the arithmetic of combine_dense_kernel, so the output is
@@ -1115,8 +1156,8 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
   CombineFuse cf = {};
   if (combine != nullptr && combine->y != nullptr) {
     cf = *combine;
-    if (epilogue != kEpiStore || row_map == nullptr || out_ptrs != nullptr || out == nullptr || !use_2cta() ||
-        cf.w == nullptr || cf.counters == nullptr || cf.k < 1 || cf.k > 32 || N % 64 != 0)
+    if (epilogue != kEpiStore || row_map == nullptr || out_ptrs != nullptr || (out == nullptr && cf.k != 1) ||
+        !use_2cta() || cf.w == nullptr || (cf.counters == nullptr && cf.k != 1) || cf.k < 1 || cf.k > 32 || N % 64 != 0)
       return set_error(HM_EINVAL, "grouped_gemm: the fused combine needs the STORE epilogue with a token-major "
                                   "row map, local output, weights, counters and 1 <= k <= 32");
   }

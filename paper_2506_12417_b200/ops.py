@@ -319,15 +319,16 @@ def grouped_gemm_combine(H, W, N: int, layout: "Layout", row_map, topk_w, counte
     """K5 (FFN2, STORE epilogue, token-major scatter through row_map) with K7 fused into the
     epilogue: returns (Y [T*k, N], y [T, N]) where y = (residual +) sum_j w[t,j] Y[t*k+j] is
     bit-identical to combine(Y, None, topk_w, residual=residual).  counters: int32 [T * N/64],
-    zero before the first call (every call leaves them zero)."""
+    zero before the first call (every call leaves them zero).  Top-1 (k == 1): the epilogue writes
+    y directly (no counters, Y not written: returned as None)."""
     _require_cuda(H, W, row_map, topk_w, counters, residual, Y, y)
     _require_dtype(torch.bfloat16, H, W, Y, y, residual, what="grouped_gemm_combine operands")
     _require_dtype(torch.float32, topk_w, what="combine weights")
     _require_dtype(torch.int32, row_map, counters, what="grouped_gemm_combine index tensors")
     T, k = topk_w.shape
-    if counters.numel() < T * (N // 64):
+    if k != 1 and (counters is None or counters.numel() < T * (N // 64)):
         raise ValueError("grouped_gemm_combine: counters must hold T * N/64 entries")
-    if Y is None:
+    if Y is None and k != 1:
         Y = torch.empty((max(T * k, 1), N), dtype=torch.bfloat16, device=H.device)
     if y is None:
         y = torch.empty((T, N), dtype=torch.bfloat16, device=H.device)

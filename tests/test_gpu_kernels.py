@@ -562,7 +562,8 @@ def test_config_rejects_untileable_shapes():
 @pytest.mark.parametrize("d,f,E,k,act,T,G,residual", [
     (256, 256, 32, 4, "swiglu", 256, 2, False),
     (512, 256, 16, 8, "swiglu", 1000, 1, True),    # ragged segments, half tiles, residual
-    (768, 512, 64, 1, "relu", 640, 4, False),     # top-1 (every row is the last arrival)
+    (768, 512, 64, 1, "relu", 640, 4, False),     # top-1: the epilogue writes y directly
+    (768, 3072, 128, 1, "relu", 4096, 4, True),   # Switch-128 shape, top-1 with residual
     (512, 256, 8, 2, "swiglu", 2048, 2, True),    # top-2, few large experts
     (2048, 768, 128, 8, "swiglu", 4096, 1, False),  # Qwen-128 shape
 ])
@@ -590,4 +591,5 @@ def test_fused_combine_bit_identical(d, f, E, k, act, T, G, residual):
     torch.cuda.synchronize()
     assert torch.equal(y1.view(torch.int16), y_ref.view(torch.int16))
     assert torch.equal(y2.view(torch.int16), y_ref.view(torch.int16))
-    assert int(blk._comb_ctr.abs().sum().item()) == 0
+    if k > 1:
+        assert int(blk._comb_ctr.abs().sum().item()) == 0
