@@ -448,8 +448,10 @@ class HarMoEnyBlock:
         return 5 if self.uses_fused_combine() else 6
 
     def uses_fused_combine(self) -> bool:
-        """FFN2 with the combine in its epilogue: always for top-1 (the epilogue scales its row into
-        y directly - no arrival counters; Switch-128 C1 287.7 -> 283.9 us), else MoEConfig.fused_combine.
+        """FFN2 with the combine in its epilogue (bit-identical either way): always for top-1 (the
+        epilogue scales its row into y directly - no arrival counters; Switch-128 C1 287.7 ->
+        283.9 us), else MoEConfig.fused_combine (top-8 Qwen: 820 vs 450 us; top-2 Mixtral: within
+        run-to-run noise of the power-capped GEMMs, 3,091-3,240 vs 3,110-3,261 us for FFN2 + combine).
         HM_FUSED_COMBINE=0/1 overrides."""
         env = os.environ.get("HM_FUSED_COMBINE")
         return (env == "1") if env is not None else (self.cfg.fused_combine or self.cfg.top_k == 1)
