@@ -277,8 +277,18 @@ __global__ void __launch_bounds__(kOPushThreads, 8)  // <= 64 registers: co-resi
 // block, then move on (one logical channel in plan order, engine.py:253-265); the last CTA
 // to finish a block publishes its slot's ready flag with release semantics.
 // ------------------------------------------------------------------------------------------
+// One 4-warp CTA per SM, <= 64 registers, maximal shared-memory carveout: the fetch runs beside
+// FFN1 (its own stream) on every SM instead of taking SMs from the persistent GEMM's pairs (a
+// 512-thread CTA does not fit beside a GEMM pair CTA: 16K registers per SM sub-partition, 3 GEMM
+// warps x 4,608 on two of them; its SMs' pairs then waited for the whole fetch).  8 x 16 B per
+// lane in flight: ~2.4 MB per GPU, enough for NVLink's latency-bandwidth product.
+#ifdef HM_FETCH_WIDE  // A/B: the round-1 configuration (32 CTAs x 512 threads, 4 x 16 B in flight)
 constexpr int kFetchThreads = 512;
 constexpr int kFetchUnroll = 4;
+#else
+constexpr int kFetchThreads = 128;
+constexpr int kFetchUnroll = 8;
+#endif
 
 __device__ __forceinline__ void copy_block(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -305,7 +315,7 @@ __device__ __forceinline__ void block_done(int32_t* counter, int32_t* flag, int 
   }
 }
 
-__global__ void __launch_bounds__(kFetchThreads)
+__global__ void __launch_bounds__(kFetchThreads, 2048 / kFetchThreads)
     fetch_kernel(const int32_t* __restrict__ fetch, const int32_t* __restrict__ n_fetch_p,
                  const unsigned long long* __restrict__ src_in, const unsigned long long* __restrict__ src_out,
                  int64_t in16, int64_t out16, uint4* __restrict__ dst_in, uint4* __restrict__ dst_out, int first_slot,
@@ -415,7 +425,13 @@ int launch_fetch_experts(const int32_t* fetch, const int32_t* n_fetch, const uns
   if (n_counters < 2) return set_error(HM_EINVAL, "fetch_experts: counters too small");
   cudaError_t e = cudaMemsetAsync(counters, 0, sizeof(int32_t) * n_counters, stream);
   if (e != cudaSuccess) return set_error(HM_ECUDA, "fetch_experts memset: %s", cudaGetErrorString(e));
-  fetch_kernel<<<ctas > 0 ? ctas : 32, kFetchThreads, 0, stream>>>(
+#ifdef HM_FETCH_WIDE
+  const int grid = ctas > 0 ? ctas : 32;
+#else
+  cudaFuncSetAttribute(fetch_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  const int grid = ctas > 0 ? ctas : num_sms();
+#endif
+  fetch_kernel<<<grid, kFetchThreads, 0, stream>>>(
       fetch, n_fetch, src_in, src_out, (int64_t)(in_bytes / 16), (int64_t)(out_bytes / 16),
       reinterpret_cast<uint4*>(dst_in), reinterpret_cast<uint4*>(dst_out), first_slot, n_slots, ready_in, ready_out,
       counters, n_counters, value);

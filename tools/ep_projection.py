@@ -193,6 +193,28 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
         h = torch.empty((max(rows, 1), n_in // (2 if act == "swiglu" else 1)), dtype=torch.bfloat16, device=dev)
         y = torch.empty((max(rows, 1), d), dtype=torch.bfloat16, device=dev)
         r["ffn1_us"] = _graph_time_us(lambda: ops.grouped_gemm(a, w_in, n_in, lay, epi, out=h), flush)
+        if n_fetch:
+            # K6 co-running: the fetch kernel (local copies standing in for the NVLink reads) on its
+            # own stream beside FFN1, whose tiles of fetched experts wait on the ready flags - shows
+            # whether the copy takes SMs from the persistent GEMM
+            src_in = torch.tensor([w_in_all[e_].data_ptr() for e_ in range(E)], **i64)
+            src_out = torch.tensor([w_out_all[e_].data_ptr() for e_ in range(E)], **i64)
+            rdy_in = torch.zeros(E, dtype=torch.int32, device=dev)
+            rdy_out = torch.zeros(E, dtype=torch.int32, device=dev)
+            ctr = torch.zeros(2 * E, dtype=torch.int32, device=dev)
+            fs = torch.cuda.Stream()
+
+            def ffn1_fetch():
+                cur = torch.cuda.current_stream()
+                rdy_in.zero_()
+                rdy_out.zero_()
+                fs.wait_stream(cur)
+                ops.fetch_experts(lay.fetch, lay.n_fetch, src_in, src_out, n_in * d * 2, d * f * 2, w_in, w_out,
+                                  n_home, n_fetch, rdy_in, rdy_out, ctr, value=1, stream=fs)
+                ops.grouped_gemm(a, w_in, n_in, lay, epi, out=h, slot_ready=rdy_in, ready_from_slot=n_home, epoch=1)
+                cur.wait_stream(fs)
+
+            r["ffn1_fetch_corun_local_us"] = _graph_time_us(ffn1_fetch, flush)
         if overlap:
             # the push of my tokens (into G local stand-ins) with my FFN1 launched right behind it
             # (PDL), its arrival counters pre-filled with the rows the other senders deliver: what
@@ -239,7 +261,7 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
             share = (r["ffn1_us"] - r["ffn1_resident_us"]) * rows_e / max(fetched_rows, 1)
             t = max(t, j * t_one + t_in) + share
         r["fetch_nvlink_us"] = n_fetch * t_one
-        r["ffn1_with_fetch_us"] = max(t, r["ffn1_us"])
+        r["ffn1_with_fetch_us"] = max(t, r["ffn1_us"], r.get("ffn1_fetch_corun_local_us", 0.0))
         if overlap:
             # FFN1 timeline from the push start: expert e's share (its rows of FFN1, the measured
             # co-running FFN1 time) starts once its rows have landed and, if fetched, its gate/up
