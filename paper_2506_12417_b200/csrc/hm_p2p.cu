@@ -282,12 +282,15 @@ __global__ void __launch_bounds__(kOPushThreads, 8)  // <= 64 registers: co-resi
 // 512-thread CTA does not fit beside a GEMM pair CTA: 16K registers per SM sub-partition, 3 GEMM
 // warps x 4,608 on two of them; its SMs' pairs then waited for the whole fetch).  8 x 16 B per
 // lane in flight: ~2.4 MB per GPU, enough for NVLink's latency-bandwidth product.
+#ifndef HM_FETCH_UNROLL
+#define HM_FETCH_UNROLL 8
+#endif
 #ifdef HM_FETCH_WIDE  // A/B: the round-1 configuration (32 CTAs x 512 threads, 4 x 16 B in flight)
 constexpr int kFetchThreads = 512;
 constexpr int kFetchUnroll = 4;
 #else
 constexpr int kFetchThreads = 128;
-constexpr int kFetchUnroll = 8;
+constexpr int kFetchUnroll = HM_FETCH_UNROLL;
 #endif
 
 __device__ __forceinline__ void copy_block(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16) {
@@ -325,12 +328,16 @@ __global__ void __launch_bounds__(kFetchThreads, 2048 / kFetchThreads)
   // more fetches than slots (a bounded cache belongs to the in-GEMM fetch pairs, hm_gemm.cu):
   // fail the launch loudly rather than leave the GEMM waiting on (or reading) unfilled slots
   if (n_fetch > n_slots || 2 * n_fetch > n_counters) __trap();
+  // every gate/up block first (all FFN1 waits on), then the down blocks (FFN2's), each in plan order
   for (int i = 0; i < n_fetch; ++i) {
     const int e = __ldg(fetch + i);
-    const int slot = first_slot + i;
-    copy_block(dst_in + (int64_t)slot * in16, reinterpret_cast<const uint4*>(__ldg(src_in + e)), in16);
+    copy_block(dst_in + (int64_t)(first_slot + i) * in16, reinterpret_cast<const uint4*>(__ldg(src_in + e)), in16);
     block_done(counters + 2 * i, ready_in + e, value);
-    copy_block(dst_out + (int64_t)slot * out16, reinterpret_cast<const uint4*>(__ldg(src_out + e)), out16);
+  }
+  for (int i = 0; i < n_fetch; ++i) {
+    const int e = __ldg(fetch + i);
+    copy_block(dst_out + (int64_t)(first_slot + i) * out16, reinterpret_cast<const uint4*>(__ldg(src_out + e)),
+               out16);
     block_done(counters + 2 * i + 1, ready_out + e, value);
   }
 }

@@ -215,6 +215,9 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
                 cur.wait_stream(fs)
 
             r["ffn1_fetch_corun_local_us"] = _graph_time_us(ffn1_fetch, flush)
+            r["fetch_local_us"] = _graph_time_us(
+                lambda: ops.fetch_experts(lay.fetch, lay.n_fetch, src_in, src_out, n_in * d * 2, d * f * 2, w_in,
+                                          w_out, n_home, n_fetch, rdy_in, rdy_out, ctr, value=1), flush)
         if overlap:
             # the push of my tokens (into G local stand-ins) with my FFN1 launched right behind it
             # (PDL), its arrival counters pre-filled with the rows the other senders deliver: what
