@@ -253,8 +253,8 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
                                                    flush)
         else:
             r["ffn1_resident_us"] = r["ffn1_us"] if not n_fetch else 0.0
-        # fetch channel (reference semantics): one expert at a time in plan order, gate/up block
-        # first; a fetched expert's FFN1 share starts when its gate/up block has landed
+        # fetch channel: plan order, every gate/up block before the down blocks (hm_fetch_experts);
+        # a fetched expert's FFN1 share starts when its gate/up block has landed
         t_one = expert_bytes / (nvlink_gbs * 1e3)
         t_in = t_one * (n_in * d) / (n_in * d + d * f)
         t = r["ffn1_resident_us"]
@@ -262,7 +262,7 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
         for j, e in enumerate(fetched):
             rows_e = int(sum(s_[1] for s_ in segs if s_[3] == e))
             share = (r["ffn1_us"] - r["ffn1_resident_us"]) * rows_e / max(fetched_rows, 1)
-            t = max(t, j * t_one + t_in) + share
+            t = max(t, (j + 1) * t_in) + share
         r["fetch_nvlink_us"] = n_fetch * t_one
         r["ffn1_with_fetch_us"] = max(t, r["ffn1_us"], r.get("ffn1_fetch_corun_local_us", 0.0))
         if overlap:
@@ -271,7 +271,7 @@ def project(d=2048, f=768, E=128, k=8, act="swiglu", T=16384, G=8, q=32, placeme
             # block (fetch channel as above, starting with the push)
             arr, order_me = _arrival_times(S, home_np, me, bytes_tok, nvlink_gbs)
             f1 = max(r["push_ffn1_local_us"], r["ffn1_us"])
-            fetch_ready = {e: j * t_one + t_in for j, e in enumerate(fetched)}
+            fetch_ready = {e: (j + 1) * t_in for j, e in enumerate(fetched)}
             seg_rows = {int(s_[3]): int(s_[1]) for s_ in segs}
             t = 0.0
             for e in order_me:
