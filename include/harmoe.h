@@ -230,6 +230,20 @@ HM_API int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t
                     int epoch, int32_t* slot_done, const hm_fetch_plan* fetch, void* stream);
 
 /*
+ * Swap-AB grouped GEMM for weight-streaming shapes (tens of rows per expert, e.g. Switch top-1):
+ * the MMA's M is 256 weight rows and N 64 token rows, so a small expert pads to 64 token rows
+ * instead of 128-256 rows of A.  A [a_rows, K] bf16 (no gather), W [slots*N, K]; epilogue
+ * HM_EPI_RELU or HM_EPI_STORE; out [a_rows(or row_map target), N] row r (-> row_map[r]).
+ * y != NULL (STORE, top-1 combine): y[row_map[r]] = (residual +) topk_w[row_map[r]] * row, the
+ * arithmetic of hm_combine with k = 1 (bit-identical); out is then not written (may be NULL).
+ * At most 512 segments.  Same outputs as hm_grouped_gemm (fp32 accumulation over K in order).
+ */
+HM_API int hm_grouped_gemm_swap(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                                const int32_t* segs, const int32_t* n_seg, int epilogue, void* out,
+                                const int32_t* row_map, const float* topk_w, const void* residual, void* y,
+                                void* stream);
+
+/*
  * FFN2 with the weighted combine (K7) fused into its epilogue (LOCAL layout, Alg. 1 steps 5-6,
  * PAPER.md:613-616): the STORE epilogue scatters expert row r to Y row row_map[r] = t*k + j as
  * hm_grouped_gemm does, and the k-th arriving row of every (token t, 64-column chunk) computes

@@ -40,6 +40,7 @@ SIGNATURES = {
     "hm_permute": [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp],
     "hm_grouped_gemm": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _i32, _vp, _i32, _i32,
                         _vp, _vp, _vp],
+    "hm_grouped_gemm_swap": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
     "hm_grouped_gemm_combine": [_vp, _i64, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp,
                                 _vp],
     "hm_fetch_expert": [_vp, _vp, ctypes.c_size_t, _vp, _i32, _vp],

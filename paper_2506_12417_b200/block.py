@@ -412,7 +412,18 @@ class HarMoEnyBlock:
                                                          index_only=fused, stream=s)
             self.stats.extras["pos"] = st["pos"]
 
+        # HM_GEMM_SWAP=1 (opt-in): swap-AB tiles for ReLU / plain experts with the copy scatter -
+        # the weights on the MMA's M, 64 token rows on N - instead of padding each expert's few rows
+        # to 128-256.  Bit-identical, but measured no faster at Switch-128 C1 (FFN1 120 -> 124 us,
+        # FFN2 125 -> 123 us, profiles/r2_experiments.txt): the A padding is not what holds the
+        # weight stream below the TMA ceiling
+        swap = os.environ.get("HM_GEMM_SWAP", "") == "1" and not fused and cfg.activation == "relu"
+
         def gemm1():
+            if swap:
+                st["h"] = ops.grouped_gemm_swap(st["xs"], self.w_in, self.n_in, st["plan"].layout, self.epi_in,
+                                                stream=s)
+                return
             if fused:
                 st["h"] = ops.grouped_gemm(st["x"], self.w_in, self.n_in, st["plan"].layout, self.epi_in,
                                            a_gather=st["inv"], a_gather_div=k, out_rows=T * k, stream=s)
@@ -427,6 +438,16 @@ class HarMoEnyBlock:
         def gemm2():
             # FFN2 scatters its rows token-major (row_map = inverse permutation) so the
             # combine reads each token's k expert outputs as one contiguous block
+            if swap and (not fuse_comb or direct_comb):
+                if direct_comb:
+                    st["ys"] = None
+                    st["y"] = ops.grouped_gemm_swap(st["h"], self.w_out, cfg.d_model, st["plan"].layout,
+                                                    ops.HM_EPI_STORE, row_map=st["inv"], topk_w=st["w"],
+                                                    residual=st["x"] if cfg.residual else None, stream=s)
+                else:
+                    st["ys"] = ops.grouped_gemm_swap(st["h"], self.w_out, cfg.d_model, st["plan"].layout,
+                                                     ops.HM_EPI_STORE, row_map=st["inv"], stream=s)
+                return
             if fuse_comb:
                 st["ys"], st["y"] = ops.grouped_gemm_combine(
                     st["h"], self.w_out, cfg.d_model, st["plan"].layout, st["inv"], st["w"],

@@ -208,6 +208,14 @@ int hm_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_rows
                              slot_done, fetch);
 }
 
+int hm_grouped_gemm_swap(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                         const int32_t* segs, const int32_t* n_seg, int epilogue, void* out, const int32_t* row_map,
+                         const float* topk_w, const void* residual, void* y, void* stream) {
+  const CombineFuse cf{topk_w, residual, y, nullptr, 1};
+  return launch_grouped_gemm_swap(A, a_rows, W, w_rows, N, K, segs, n_seg, epilogue, out, row_map,
+                                  y != nullptr ? &cf : nullptr, as_stream(stream));
+}
+
 int hm_grouped_gemm_combine(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
                             const int32_t* segs, const int32_t* n_seg, const int32_t* mtile_prefix, void* Y,
                             const int32_t* row_map, const float* topk_w, int k, const void* residual, void* y,

@@ -1042,6 +1042,249 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
   if (a_arrive != nullptr) griddep_wait();
 }
 
+// ------------------------------------------------------------------------------------------
+// Swap-AB 2-CTA grouped GEMM for weight-streaming shapes (tens of rows per expert: Switch-128,
+// top-1).  The row-major kernel above puts the expert's token rows on the MMA's M (256 per pair,
+// 128 at best with half tiles), so a 32-row expert drags 96+ padding rows of A through L2->SM
+// per weight tile (355 of FFN1's 965 MB of L2->SM traffic at C1).  Here the MMA computes
+// D^T = W . X^T: M = 256 weight rows (128 per CTA, TMA boxes of the B map above), N = 64 token
+// rows (32 per CTA), so a 32-row expert pads to 64 token columns.  The epilogue transposes each
+// warp's 32 features x 32 tokens through shared memory and writes token-major rows (ReLU, plain
+// store, or the top-1 combine y[t] = (x[t] +) w[t] * Y with combine_dense_kernel's arithmetic).
+// No gather, half tiles, fetch pairs or remote outputs (the LOCAL Switch path needs none).
+// ------------------------------------------------------------------------------------------
+constexpr int kSwN = 64;                      // token rows per pair tile (MMA N)
+constexpr uint32_t kSwBBytes = (kSwN / 2) * kBK * 2;  // 4 KB: one CTA's 32 token rows per stage
+
+template <int kEpi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_swap_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+                             const int4* __restrict__ segs_g, const int* __restrict__ n_seg_ptr,
+                             __nv_bfloat16* __restrict__ out, int N, int K, int ldo, const int* __restrict__ row_map,
+                             const CombineFuse cf) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * 2 * k2Half);
+  uint64_t* empty = full + k2Stages;
+  uint64_t* tfull = empty + k2Stages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int4* s_segs = reinterpret_cast<int4*>(smem + k2Stages * 2 * k2Half + 256);
+  int* s_tp = reinterpret_cast<int*>(s_segs + kMaxSmemSegs);  // [n_seg + 1] tile prefix
+  uint8_t* s_stage = reinterpret_cast<uint8_t*>(s_tp + kMaxSmemSegs + 4);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+  const int n_seg = *n_seg_ptr;
+  if (n_seg > kMaxSmemSegs) __trap();  // the segment table is staged in shared memory
+  const int NB = N / kBN;
+  for (int i = threadIdx.x; i < n_seg; i += blockDim.x) s_segs[i] = segs_g[i];
+  __syncthreads();
+  if (warp == 0) {  // tile prefix: token tiles of kSwN rows x NB weight blocks per segment
+    int run = 0;
+    for (int base = 0; base < n_seg; base += 32) {
+      const int i = base + lane;
+      const int x = i < n_seg ? ((s_segs[i].y + kSwN - 1) / kSwN) * NB : 0;
+      int incl = x;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      if (i < n_seg) s_tp[i] = run + incl - x;
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_tp[n_seg] = run;
+  }
+  if (warp == 0 && lane == 0) {
+    for (int st = 0; st < k2Stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int st = 0; st < 2; ++st) {
+      mbar_init(&tfull[st], 1);
+      mbar_init(&tempty[st], 2 * kEpiWarps);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tmap_w);
+    tma_prefetch_desc(&tmap_x);
+  }
+  if (warp == 1) tmem_alloc_2cta<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = s_tp[n_seg];
+  const int KB = K / kBK;
+  // tile t -> (segment, token tile m, weight block nb); m-major inside a segment
+  auto seek = [&](int t, int4& sg, int& m, int& nb) {
+    int lo = 0, hi = n_seg - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_tp[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    sg = s_segs[lo];
+    const int loc = t - s_tp[lo];
+    m = loc / NB;
+    nb = loc - m * NB;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs): 128 weight rows + 32 token rows per stage =====
+      const uint64_t pol_x = l2_policy_evict_last();
+      const uint64_t pol_w_once = l2_policy_evict_first();
+      const uint64_t pol_w = l2_policy_evict_last();
+      const uint32_t full_leader = mapa_shared(full, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < total; t += npairs) {
+        int4 sg;
+        int m, nb;
+        seek(t, sg, m, nb);
+        const int wrow = sg.z * N + nb * kBN + (int)rank * (kBN / 2);
+        const int xrow = sg.x + m * kSwN + (int)rank * (kSwN / 2);
+        const uint64_t pw = sg.y <= kSwN ? pol_w_once : pol_w;  // one token tile: weights read once
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (k2Half + kSwBBytes));
+          uint8_t* sa = smem + stage * 2 * k2Half;
+          tma_load_2d_2cta(sa, &tmap_w, full_leader + stage * 8, kb * kBK, wrow, pw);
+          tma_load_2d_2cta(sa + k2Half, &tmap_x, full_leader + stage * 8, kb * kBK, xrow, pol_x);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ===== MMA issuer (leader CTA): M = 256 weight rows, N = 64 token rows =====
+      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, kSwN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = pair; t < total; t += npairs, ++i) {
+        const int acc = i & 1;
+        mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * 2 * k2Half);
+          const uint64_t a0 = make_sdesc_sw128(sa);
+          const uint64_t b0 = make_sdesc_sw128(sa + k2Half);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_bf16_2cta(d_tmem, a0 + (uint64_t)(k * 2), b0 + (uint64_t)(k * 2), idesc, (kb | k) != 0);
+          umma_commit_2cta_multicast(&empty[stage], 0x3);
+          if (++stage == k2Stages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2cta_multicast(&tfull[acc], 0x3);
+      }
+    }
+  } else {
+    // ===== epilogue: warp (q, half) drains features q*32.. of this CTA's 128, tokens half*32.. =====
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    const uint32_t stg = smem_u32(s_stage + ew * kStgBytes);  // [32 tokens][kStgPitch]: 32 features
+    const uint32_t tempty_leader = mapa_shared(tempty, 0);
+    const bool direct = kEpi == kEpiStore && cf.y != nullptr && cf.k == 1;
+    int i = 0;
+    for (int t = pair; t < total; t += npairs, ++i) {
+      int4 sg;
+      int m, nb;
+      seek(t, sg, m, nb);
+      const int tok0 = m * kSwN + half * (kSwN / 2);  // first token of this warp within the segment
+      // the 4 token rows this lane stores (it * 8 + lane / 4), their output rows loaded before the
+      // accumulator wait
+      int64_t orow[4];
+      float wv[4];
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int tl = it * 8 + (lane >> 2);
+        const bool ok = tok0 + tl < sg.y;
+        int64_t r = (int64_t)sg.x + tok0 + tl;
+        if (ok && row_map != nullptr) r = __ldg(row_map + r);
+        orow[it] = ok ? r : -1;
+        wv[it] = (direct && ok) ? __ldg(cf.w + r) : 0.0f;
+      }
+      const int acc = i & 1;
+      mbar_wait(&tfull[acc], (i >> 1) & 1);
+      tc_fence_after();
+      uint32_t a[32];
+      tmem_ld_32x32b_x32(tmem_base + acc * kBN + ((uint32_t)(q * 32) << 16) + half * (kSwN / 2), a);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+      // transpose: feature `lane`, token j -> stg[j][lane]
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float v = __uint_as_float(a[j]);
+        if constexpr (kEpi == kEpiRelu) v = fmaxf(v, 0.0f);
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        asm volatile("st.shared.b16 [%0], %1;" ::"r"(stg + j * kStgPitch + lane * 2),
+                     "h"(*reinterpret_cast<const unsigned short*>(&b))
+                     : "memory");
+      }
+      __syncwarp();
+      const int col = nb * kBN + (int)rank * (kBN / 2) + q * 32 + (lane & 3) * 8;
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        if (orow[it] < 0) continue;
+        const int tl = it * 8 + (lane >> 2);
+        const uint4 v = ld_shared_v4(stg + tl * kStgPitch + (lane & 3) * 16);
+        if (direct) {
+          float accv[8];
+          if (cf.residual != nullptr) {
+            const uint4 rv = ld_global_nc_v4(reinterpret_cast<const __nv_bfloat16*>(cf.residual) + orow[it] * ldo + col);
+            const uint32_t r4[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              accv[2 * h] = bf16lo(r4[h]);
+              accv[2 * h + 1] = bf16hi(r4[h]);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) accv[h] = 0.0f;
+          }
+          const uint32_t y4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            accv[2 * h] = __fadd_rn(accv[2 * h], __fmul_rn(wv[it], bf16lo(y4[h])));
+            accv[2 * h + 1] = __fadd_rn(accv[2 * h + 1], __fmul_rn(wv[it], bf16hi(y4[h])));
+          }
+          st_global_v4(reinterpret_cast<__nv_bfloat16*>(cf.y) + orow[it] * ldo + col, pack_bf16x2(accv[0], accv[1]),
+                       pack_bf16x2(accv[2], accv[3]), pack_bf16x2(accv[4], accv[5]), pack_bf16x2(accv[6], accv[7]));
+        } else {
+          st_global_v4(out + orow[it] * ldo + col, v.x, v.y, v.z, v.w);
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2cta<kTmemCols>(tmem_base);
+  }
+}
+
 static bool use_half_tiles() {
   static int v = -1;
   if (v < 0) {
@@ -1110,6 +1353,57 @@ static int resident_pairs_of() {
     cache[dev] = n;
   }
   return cache[dev];
+}
+
+int launch_grouped_gemm_swap(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                             const int32_t* segs, const int32_t* n_seg, int epilogue, void* out, const int32_t* row_map,
+                             const CombineFuse* combine, cudaStream_t stream) {
+  if (N % kBN != 0 || K % kBK != 0 || N <= 0 || K <= 0)
+    return set_error(HM_EINVAL, "grouped_gemm_swap: N %% 256 and K %% 64 must be 0");
+  if (w_rows % N != 0) return set_error(HM_EINVAL, "grouped_gemm_swap: weight rows must be a multiple of N");
+  if (epilogue != kEpiStore && epilogue != kEpiRelu)
+    return set_error(HM_EINVAL, "grouped_gemm_swap: STORE or RELU epilogue only");
+  CombineFuse cf = {};
+  if (combine != nullptr && combine->y != nullptr) {
+    cf = *combine;
+    if (epilogue != kEpiStore || cf.k != 1 || cf.w == nullptr || row_map == nullptr)
+      return set_error(HM_EINVAL, "grouped_gemm_swap: the fused combine is the top-1 one (STORE, k = 1, row map)");
+  } else if (out == nullptr) {
+    return set_error(HM_EINVAL, "grouped_gemm_swap: out is required");
+  }
+  if (a_rows <= 0) return HM_OK;
+  CUtensorMap tw, tx;
+  int rc = make_tmap_2d_bf16(&tw, W, (uint64_t)w_rows, (uint64_t)K, kBN / 2, kBK);
+  if (rc) return rc;
+  rc = make_tmap_2d_bf16(&tx, A, (uint64_t)a_rows, (uint64_t)K, kSwN / 2, kBK);
+  if (rc) return rc;
+  const int pairs = min(num_sms() / 2, gemm_resident_pairs(epilogue, false));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = kGemm2Smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int4* s4 = reinterpret_cast<const int4*>(segs);
+  auto* o = reinterpret_cast<__nv_bfloat16*>(out);
+  cudaError_t e;
+  if (epilogue == kEpiRelu) {
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<kEpiRelu>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGemm2Smem);
+    e = cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<kEpiRelu>, tw, tx, s4, n_seg, o, N, K, N, row_map, cf);
+  } else {
+    cudaFuncSetAttribute(grouped_gemm_swap_kernel<kEpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kGemm2Smem);
+    e = cudaLaunchKernelEx(&cfg, grouped_gemm_swap_kernel<kEpiStore>, tw, tx, s4, n_seg, o, N, K, N, row_map, cf);
+  }
+  if (e != cudaSuccess) return set_error(HM_ECUDA, "grouped_gemm_swap launch: %s", cudaGetErrorString(e));
+  return check_launch("grouped_gemm_swap");
 }
 
 int gemm_resident_pairs(int epilogue, bool gather) {

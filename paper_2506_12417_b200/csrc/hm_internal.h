@@ -40,6 +40,9 @@ int launch_grouped_gemm(const void* A, int64_t a_rows, const void* W, int64_t w_
                         const CombineFuse* combine = nullptr, const int32_t* a_arrive = nullptr, int pdl = 0);
 
 int gemm_resident_pairs(int epilogue, bool gather);
+int launch_grouped_gemm_swap(const void* A, int64_t a_rows, const void* W, int64_t w_rows, int N, int K,
+                             const int32_t* segs, const int32_t* n_seg, int epilogue, void* out, const int32_t* row_map,
+                             const CombineFuse* combine, cudaStream_t stream);
 
 int launch_router(const void* x, const void* wg, const float* bias, int n_ranks, int tokens_per_rank, int d, int E,
                   int k, int renormalize, int32_t* topk_idx, float* topk_w, int32_t* tile_hist, int32_t* lrank,

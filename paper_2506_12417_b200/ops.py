@@ -314,6 +314,28 @@ def grouped_gemm(A, W, N: int, layout_or_segs, epilogue: int, out=None, row_map=
     return out
 
 
+def grouped_gemm_swap(A, W, N: int, layout: "Layout", epilogue: int, out=None, row_map=None, topk_w=None,
+                      residual=None, y=None, stream=None):
+    """K5 with swap-AB tiles (weights on the MMA's M, 64 token rows on N) for weight-streaming
+    shapes.  With topk_w (top-1, STORE): returns y = (residual +) w * row at row_map (combine
+    fused, bit-identical); else returns out [rows, N]."""
+    segs, n_seg = (layout.segs, layout.n_seg) if isinstance(layout, Layout) else (layout[0], layout[1])
+    _require_cuda(A, W, row_map, topk_w, residual, y, out, segs, n_seg)
+    _require_dtype(torch.bfloat16, A, W, out, y, residual, what="grouped_gemm_swap operands")
+    rows, K = A.shape
+    if topk_w is not None:
+        _require_dtype(torch.float32, topk_w, what="combine weights")
+        if topk_w.dim() > 1 and topk_w.shape[-1] != 1:
+            raise ValueError("grouped_gemm_swap: the fused combine is the top-1 one")
+        if y is None:
+            y = torch.empty((topk_w.shape[0], N), dtype=torch.bfloat16, device=A.device)
+    elif out is None:
+        out = torch.empty((max(rows, 1), N), dtype=torch.bfloat16, device=A.device)
+    _lib.call("hm_grouped_gemm_swap", _ptr(A), rows, _ptr(W), W.shape[0], N, K, _ptr(segs), _ptr(n_seg),
+              int(epilogue), _ptr(out), _ptr(row_map), _ptr(topk_w), _ptr(residual), _ptr(y), _stream(stream))
+    return y if topk_w is not None else out
+
+
 def grouped_gemm_combine(H, W, N: int, layout: "Layout", row_map, topk_w, counters, Y=None, y=None, residual=None,
                          stream=None):
     """K5 (FFN2, STORE epilogue, token-major scatter through row_map) with K7 fused into the

@@ -264,6 +264,43 @@ def _segs_from_counts(counts, wslots, device):
             torch.tensor(mt, dtype=torch.int32, device=device)), starts
 
 
+@pytest.mark.parametrize("epi", ["store", "relu"])
+@pytest.mark.parametrize("N,K,counts", [
+    (256, 64, (1, 0, 300, 129, 64)),
+    (3072, 768, (32, 17, 0, 64, 65, 128, 5)),   # Switch FFN1 shape, ~32-row experts
+    (768, 3072, (40, 1, 95, 0, 33, 64, 200)),   # Switch FFN2 shape
+])
+def test_grouped_gemm_swap_matches_row_major(epi, N, K, counts):
+    """hm_grouped_gemm_swap (weights on the MMA's M, 64 token rows on N) gives the row-major
+    kernel's outputs (same fp32 accumulation over K), plain and scattered, and its top-1 combine
+    equals hm_combine after the row-major FFN2 bit for bit (with and without residual)."""
+    from paper_2506_12417_b200 import ops
+
+    dev = _cuda()
+    g = torch.Generator(device=dev).manual_seed(N * 7 + K)
+    E = len(counts)
+    wslots = list(reversed(range(E)))
+    lay, rows = _segs_from_counts(counts, wslots, dev)
+    A = torch.randn((rows, K), device=dev, generator=g).to(torch.bfloat16)
+    W = (torch.randn((E * N, K), device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    code = dict(store=ops.HM_EPI_STORE, relu=ops.HM_EPI_RELU)[epi]
+    ref = ops.grouped_gemm(A, W, N, lay, code)
+    out = ops.grouped_gemm_swap(A, W, N, lay, code)
+    perm = torch.randperm(rows, device=dev, generator=g).to(torch.int32)
+    out_s = ops.grouped_gemm_swap(A, W, N, lay, code, row_map=perm)
+    torch.cuda.synchronize()
+    assert torch.equal(out[:rows], ref[:rows])
+    assert torch.equal(out_s[perm.long()], ref[:rows])
+    if epi == "store":
+        w = torch.rand((rows, 1), device=dev, generator=g)
+        res = torch.randn((rows, N), device=dev, generator=g).to(torch.bfloat16)
+        for residual in (None, res):
+            y_ref = ops.combine(ops.grouped_gemm(A, W, N, lay, code, row_map=perm), None, w, residual=residual)
+            y = ops.grouped_gemm_swap(A, W, N, lay, code, row_map=perm, topk_w=w, residual=residual)
+            torch.cuda.synchronize()
+            assert torch.equal(y.view(torch.int16), y_ref.view(torch.int16))
+
+
 @pytest.mark.parametrize("epi", ["store", "relu", "swiglu"])
 @pytest.mark.parametrize("N,K,counts", [
     (256, 64, (1, 0, 300, 129, 64)),
