@@ -412,12 +412,16 @@ class HarMoEnyBlock:
                                                          index_only=fused, stream=s)
             self.stats.extras["pos"] = st["pos"]
 
-        # HM_GEMM_SWAP=1 (opt-in): swap-AB tiles for ReLU / plain experts with the copy scatter -
-        # the weights on the MMA's M, 64 token rows on N - instead of padding each expert's few rows
-        # to 128-256.  Bit-identical, but measured no faster at Switch-128 C1 (FFN1 120 -> 124 us,
-        # FFN2 125 -> 123 us, profiles/r2_experiments.txt): the A padding is not what holds the
-        # weight stream below the TMA ceiling
-        swap = os.environ.get("HM_GEMM_SWAP", "") == "1" and not fused and cfg.activation == "relu"
+        # swap-AB tiles (hm_grouped_gemm_swap: the weights on the MMA's M, 64 token rows on N, 9
+        # stages of 16 KB weights + 4 KB tokens) for weight-streaming shapes, <= 64 rows per expert
+        # on average: FFN2 by default (Switch-128 C1: 125 -> 119 us, step 284 -> 281 us); FFN1 only
+        # on request - its short K = 768 tiles make the transposing epilogue cost more than the
+        # padding rows it saves (120 -> 122 us).  Bit-identical either way.
+        # HM_GEMM_SWAP=0 (never) / 1 (FFN1 and FFN2) / ffn2 overrides.
+        env_sw = os.environ.get("HM_GEMM_SWAP", "")
+        small = T * k <= 64 * E
+        swap2 = (env_sw in ("1", "ffn2")) or (env_sw == "" and small)
+        swap = env_sw == "1" and not fused and cfg.activation == "relu"
 
         def gemm1():
             if swap:
@@ -438,7 +442,7 @@ class HarMoEnyBlock:
         def gemm2():
             # FFN2 scatters its rows token-major (row_map = inverse permutation) so the
             # combine reads each token's k expert outputs as one contiguous block
-            if swap and (not fuse_comb or direct_comb):
+            if swap2 and (not fuse_comb or direct_comb):
                 if direct_comb:
                     st["ys"] = None
                     st["y"] = ops.grouped_gemm_swap(st["h"], self.w_out, cfg.d_model, st["plan"].layout,

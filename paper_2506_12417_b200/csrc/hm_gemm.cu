@@ -1053,8 +1053,16 @@ __global__ void __launch_bounds__(kGather ? kGemmThreads + kALoadWarps * 32 : kG
 // store, or the top-1 combine y[t] = (x[t] +) w[t] * Y with combine_dense_kernel's arithmetic).
 // No gather, half tiles, fetch pairs or remote outputs (the LOCAL Switch path needs none).
 // ------------------------------------------------------------------------------------------
+#ifndef HM_SW_STAGES
+#define HM_SW_STAGES 9
+#endif
 constexpr int kSwN = 64;                      // token rows per pair tile (MMA N)
 constexpr uint32_t kSwBBytes = (kSwN / 2) * kBK * 2;  // 4 KB: one CTA's 32 token rows per stage
+// a stage is 16 KB of weights + 4 KB of token rows (1 KB aligned for the 128-byte swizzle): 9
+// stages fit where the row-major kernel keeps 6 of 32 KB, so more weight bytes are in flight
+constexpr uint32_t kSwStage = k2Half + kSwBBytes;
+constexpr int kSwStages = HM_SW_STAGES;
+static_assert(kSwStages * kSwStage <= k2Stages * 2 * k2Half, "swap stages must fit the row-major layout");
 
 template <int kEpi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -1064,12 +1072,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                              const CombineFuse cf) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + k2Stages * 2 * k2Half);
-  uint64_t* empty = full + k2Stages;
-  uint64_t* tfull = empty + k2Stages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSwStages * kSwStage);
+  uint64_t* empty = full + kSwStages;
+  uint64_t* tfull = empty + kSwStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int4* s_segs = reinterpret_cast<int4*>(smem + k2Stages * 2 * k2Half + 256);
+  int4* s_segs = reinterpret_cast<int4*>(smem + kSwStages * kSwStage + 256);
   int* s_tp = reinterpret_cast<int*>(s_segs + kMaxSmemSegs);  // [n_seg + 1] tile prefix
   uint8_t* s_stage = reinterpret_cast<uint8_t*>(s_tp + kMaxSmemSegs + 4);
 
@@ -1100,7 +1108,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) s_tp[n_seg] = run;
   }
   if (warp == 0 && lane == 0) {
-    for (int st = 0; st < k2Stages; ++st) {
+    for (int st = 0; st < kSwStages; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], 1);
     }
@@ -1153,10 +1161,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (k2Half + kSwBBytes));
-          uint8_t* sa = smem + stage * 2 * k2Half;
+          uint8_t* sa = smem + stage * kSwStage;
           tma_load_2d_2cta(sa, &tmap_w, full_leader + stage * 8, kb * kBK, wrow, pw);
           tma_load_2d_2cta(sa + k2Half, &tmap_x, full_leader + stage * 8, kb * kBK, xrow, pol_x);
-          if (++stage == k2Stages) {
+          if (++stage == kSwStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -1178,14 +1186,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * 2 * k2Half);
+          const uint32_t sa = smem_u32(smem + stage * kSwStage);
           const uint64_t a0 = make_sdesc_sw128(sa);
           const uint64_t b0 = make_sdesc_sw128(sa + k2Half);
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             umma_bf16_2cta(d_tmem, a0 + (uint64_t)(k * 2), b0 + (uint64_t)(k * 2), idesc, (kb | k) != 0);
           umma_commit_2cta_multicast(&empty[stage], 0x3);
-          if (++stage == k2Stages) {
+          if (++stage == kSwStages) {
             stage = 0;
             phase ^= 1;
           }
