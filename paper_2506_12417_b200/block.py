@@ -420,8 +420,9 @@ class HarMoEnyBlock:
         # HM_GEMM_SWAP=0 (never) / 1 (FFN1 and FFN2) / ffn2 overrides.
         env_sw = os.environ.get("HM_GEMM_SWAP", "")
         small = T * k <= 64 * E
-        swap2 = (env_sw in ("1", "ffn2")) or (env_sw == "" and small)
-        swap = env_sw == "1" and not fused and cfg.activation == "relu"
+        fits = G * E <= 512  # the swap kernel stages the segment table (<= G*E segments) in smem
+        swap2 = fits and ((env_sw in ("1", "ffn2")) or (env_sw == "" and small))
+        swap = fits and env_sw == "1" and not fused and cfg.activation == "relu"
 
         def gemm1():
             if swap:
