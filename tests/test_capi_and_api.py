@@ -213,3 +213,27 @@ def test_bounded_cache_needs_async_fetch():
         MoEConfig(expert_cache_size=2, async_fetch=False, **kw)
     with pytest.raises(ValueError, match="expert_cache_size"):
         MoEConfig(expert_cache_size=-1, **kw)
+
+
+def test_new_entry_points_validate_before_touching_the_device(lib):
+    """Round-2 entry points reject bad arguments with HM_EINVAL before any CUDA call (so this
+    runs without a GPU): the swap-AB GEMM's epilogues, the ordered push's power-of-two G, the
+    push work list's required outputs."""
+    import ctypes
+
+    from paper_2506_12417_b200 import _lib
+
+    L = _lib.load()
+    vp = ctypes.c_void_p
+    # SwiGLU is not a swap-AB epilogue
+    assert L.hm_grouped_gemm_swap(None, 0, None, 256, 256, 64, None, None, _lib.HM_EPI_SWIGLU, vp(16), None,
+                                  None, None, None, None) == _lib.HM_EINVAL
+    # N must be a multiple of 256
+    assert L.hm_grouped_gemm_swap(None, 0, None, 100, 100, 64, None, None, _lib.HM_EPI_STORE, vp(16), None,
+                                  None, None, None, None) == _lib.HM_EINVAL
+    # G = 3 is not a power of two
+    assert L.hm_dispatch_push_ordered(None, None, None, None, None, None, vp(16), vp(16), vp(16), 8, 0, 3, 16, 2, 256,
+                                      vp(16), vp(16), vp(16), vp(16), None, vp(16), None) == _lib.HM_EINVAL
+    # the push work list is required
+    assert L.hm_plan_dispatch(None, None, 4, 16, 4, 1, 0, *([None] * 9), 0, None, None, None, None) == _lib.HM_EINVAL
+    assert b"push_items" in L.hm_last_error()
