@@ -736,6 +736,39 @@ def run_ours(args, rank, world, local_rank):
         e_ms = float(t.item())
     e2e_value = T_total * e_steps / (e_ms / 1e3)
     nbytes = T_local * d * 2
+    # the e2e roofline of this box: the step's H2D and D2H bytes copied concurrently on their own
+    # (copy engines, pinned memory), no kernels
+    pcie = None
+    try:
+        xd2, yd2 = torch.empty_like(x), torch.empty_like(x)
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def _copies():
+            s_in.wait_stream(stream)
+            s_out.wait_stream(stream)
+            with torch.cuda.stream(s_in):
+                xd2.copy_(x_host, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                y_host.copy_(yd2, non_blocking=True)
+            stream.wait_stream(s_in)
+            stream.wait_stream(s_out)
+
+        for _ in range(2):
+            _copies()
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(10):
+            _copies()
+        p1.record(stream)
+        torch.cuda.synchronize()
+        p_ms = p0.elapsed_time(p1) / 10
+        pcie = {"copies_ms_per_step": p_ms, "bidirectional_gbs": 2 * nbytes / (p_ms * 1e6),
+                "bound_tokens_per_s": T_local / (p_ms / 1e3)}
+        pcie["e2e_frac_of_bound"] = (e2e_value / world) / pcie["bound_tokens_per_s"]
+        del xd2, yd2
+    except Exception as e:  # noqa: BLE001 - diagnostic only
+        pcie = {"error": str(e)[:120]}
 
     # ---- sustained: the same step back to back long enough for the 1 kW power cap to engage
     # (the default timed loop above is a short burst); reported beside the headline ----
@@ -832,7 +865,8 @@ def run_ours(args, rank, world, local_rank):
                 "path": (f"{type(blk).__name__}.host_pipeline({T_local}, {args.e2e_chunks}).run: pinned x -> HBM, "
                          f"block, HBM -> pinned y; copies overlapped with compute across token chunks and "
                          f"successive steps (ping-pong buffers)")
-                if graphed and args.e2e_chunks >= 1 else "forward_host (pinned H2D -> block -> D2H)"},
+                if graphed and args.e2e_chunks >= 1 else "forward_host (pinned H2D -> block -> D2H)",
+                "pcie_roofline": pcie},
         "gpu_launches": blk.KERNELS_PER_FORWARD * args.steps,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
