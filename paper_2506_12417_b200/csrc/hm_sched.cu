@@ -1231,17 +1231,17 @@ __global__ void __launch_bounds__(kPlanThreads)
   HM_PSTAMP(1);
   // fast path: every count < 2^21 (32-bit packed keys), harmony / static policy, LOCAL or
   // EP_EXPERT layout (HM_PLAN_FAST=0 forces the general path: A/B and tests)
-  __shared__ unsigned long long s_total;
-  if (threadIdx.x == 0) s_total = 0ull;
-  __syncthreads();
+  __shared__ unsigned long long s_wpart[32];  // per-warp partial sums of m_all (one barrier, no atomics)
   {
     unsigned long long part = 0ull;
     for (int i = threadIdx.x; i < GE; i += blockDim.x) part += (unsigned)s_m[i];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-    if ((threadIdx.x & 31) == 0 && part != 0ull) atomicAdd(&s_total, part);
+    if ((threadIdx.x & 31) == 0) s_wpart[threadIdx.x >> 5] = part;
   }
   __syncthreads();
+  unsigned long long s_total = 0ull;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s_total += s_wpart[w];
   if (fast && s_total < (1ull << 21) && rebalance != HM_POLICY_EVEN_SPLIT && mode != HM_LAYOUT_EP &&
       (G & (G - 1)) == 0) {
     const int Ep = E + 32 / G;
