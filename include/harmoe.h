@@ -76,7 +76,8 @@ extern "C" {
                               /* rank d's buffer; one GEMM segment per expert (all sources)       */
 
 /* diagnostics: %globaltimer stamps (ns) of the last hm_plan launch: start, after the histogram
- * reduce, after the schedule, after the layout (host buffer of 4 int64; synchronises the device) */
+ * reduce, after the schedule, after the layout (host buffer of 4 int64; synchronises the device).
+ * Recorded only by a library built with -DHM_PLAN_PHASES (zeros otherwise). */
 HM_API int hm_debug_plan_phases(long long* out4);
 
 HM_API int hm_version(void);

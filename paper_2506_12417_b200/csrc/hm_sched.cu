@@ -38,6 +38,16 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// %globaltimer phase stamps (hm_debug_plan_phases) only in a diagnostics build (-DHM_PLAN_PHASES,
+// tools/plan_phases*.py): the reads cost the production planner ~1.6 us per launch (Switch C1
+// router + planner + scatter stage 30.3 -> 28.7 us without them)
+#ifdef HM_PLAN_PHASES
+#define HM_PHASE(i) g_phase_ns[i] = globaltimer_ns()
+#else
+#define HM_PHASE(i) \
+  do {              \
+  } while (0)
+#endif
 
 int read_plan_phases(long long* out8) {
   unsigned long long h[8];
@@ -520,7 +530,7 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       *o.n_fetch = 0;
     }
     __syncthreads();
-    if (tid == 0) g_phase_ns[4] = globaltimer_ns();
+    if (tid == 0) HM_PHASE(4);
     HM_PSTAMP(5);
     for (int i = tid; i < E * G; i += nt) {
       const int e = i / G, d = i - (i / G) * G;
@@ -552,10 +562,10 @@ __device__ void dev_layout(const int* S, const int* home, int G, int E, int mode
       s_cnt[sidx] = (ne + 127) / 128;
     }
     __syncthreads();
-    if (tid == 0) g_phase_ns[5] = globaltimer_ns();
+    if (tid == 0) HM_PHASE(5);
     HM_PSTAMP(7);
     block_scan_to(s_cnt, s_nnz[G], o.mprefix, s_tmp);
-    if (tid == 0) g_phase_ns[6] = globaltimer_ns();
+    if (tid == 0) HM_PHASE(6);
     HM_PSTAMP(8);
     return;
   }
@@ -1160,9 +1170,9 @@ __global__ void __launch_bounds__(kPlanThreads)
   unsigned long long* s_key =       // [E] plan-order keys (8-byte aligned, shared address space kept)
       reinterpret_cast<unsigned long long*>(s_cnt + E + 1 + ((smem_u32(s_cnt + E + 1) & 4u) ? 1 : 0));
   const int tid = threadIdx.x;
-  if (tid == 0) g_phase_ns[0] = globaltimer_ns();
+  if (tid == 0) HM_PHASE(0);
   dev_hist_reduce(tile_hist, 1, tpr, E, s_m, m_out, tile_off, s_part);
-  if (tid == 0) g_phase_ns[1] = globaltimer_ns();
+  if (tid == 0) HM_PHASE(1);
   for (int e = tid; e < E; e += blockDim.x) {
     const int n = s_m[e];
     S_out[e] = n;  // S[0, e, 0]
@@ -1170,7 +1180,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   }
   block_scan_to(s_m, E, s_base, s_tmp);  // s_base[E] = total (ends with __syncthreads)
   if (tid == 0) {
-    g_phase_ns[2] = globaltimer_ns();
+    HM_PHASE(2);
     *iters_out = 0;
     if (loads_out != nullptr) loads_out[0] = s_base[E];
     *o.n_fetch = 0;
@@ -1191,7 +1201,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   }
   if (tid == 0) *o.n_seg = nseg;
   block_scan_to(s_cnt, nseg, o.mprefix, s_tmp);
-  if (tid == 0) g_phase_ns[3] = globaltimer_ns();
+  if (tid == 0) HM_PHASE(3);
 }
 
 // Whole planning stage in one launch.  kHist: m_all comes from the router's tile
@@ -1215,7 +1225,7 @@ __global__ void __launch_bounds__(kPlanThreads)
   for (int rep = 0; rep < 2; ++rep) {
   __syncthreads();
 #endif
-  if (threadIdx.x == 0) g_phase_ns[0] = globaltimer_ns();
+  if (threadIdx.x == 0) HM_PHASE(0);
   HM_PSTAMP(0);
 #ifdef HM_PLAN_CLOCK
   const long long c0 = clock64();
@@ -1227,7 +1237,7 @@ __global__ void __launch_bounds__(kPlanThreads)
     for (int i = threadIdx.x; i < GE; i += blockDim.x) s_m[i] = m_in[i];
   }
   __syncthreads();
-  if (threadIdx.x == 0) g_phase_ns[1] = globaltimer_ns();
+  if (threadIdx.x == 0) HM_PHASE(1);
   HM_PSTAMP(1);
   // fast path: every count < 2^21 (32-bit packed keys), harmony / static policy, LOCAL or
   // EP_EXPERT layout (HM_PLAN_FAST=0 forces the general path: A/B and tests)
@@ -1247,17 +1257,17 @@ __global__ void __launch_bounds__(kPlanThreads)
     const int Ep = E + 32 / G;
     dev_schedule_t(s_St, Ep, reinterpret_cast<int*>(F), s_m, s_home, G, E, q, rebalance, S_out, iters_out,
                    loads_out);
-    if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
+    if (threadIdx.x == 0) HM_PHASE(2);
     dev_layout_t(s_St, Ep, s_home, G, E, mode, me, o, s_scr);
   } else {
     // the push work list exists only on the fast path: flag it invalid (the push kernel traps)
     if (o.push_cprefix != nullptr && threadIdx.x == 0) o.push_cprefix[GE] = -1;
     dev_schedule(s_S, true, s_m, s_home, G, E, q, rebalance, iters_out, loads_out, F, s_St);
-    if (threadIdx.x == 0) g_phase_ns[2] = globaltimer_ns();
+    if (threadIdx.x == 0) HM_PHASE(2);
     for (int i = threadIdx.x; i < GE * G; i += blockDim.x) S_out[i] = s_S[i];
     dev_layout(s_S, s_home, G, E, mode, me, o, s_scr);
   }
-  if (threadIdx.x == 0) g_phase_ns[3] = globaltimer_ns();
+  if (threadIdx.x == 0) HM_PHASE(3);
 #ifdef HM_PLAN_CLOCK
   if (threadIdx.x == 0) g_phase_ns[7] = (unsigned long long)(clock64() - c0);
 #endif

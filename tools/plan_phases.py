@@ -1,3 +1,4 @@
+# needs a diagnostics build: bash tools/build_variant.sh phases -DHM_PLAN_PHASES; HM_LIB_PATH=paper_2506_12417_b200/libharmoe_phases.so
 """Diagnostics: phase timing inside the fused planner (hm_debug_plan_phases)."""
 
 import ctypes

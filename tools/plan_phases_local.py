@@ -1,3 +1,4 @@
+# needs a diagnostics build: bash tools/build_variant.sh phases -DHM_PLAN_PHASES; HM_LIB_PATH=paper_2506_12417_b200/libharmoe_phases.so
 import ctypes, sys, torch
 sys.path.insert(0, '.')
 from paper_2506_12417_b200 import _lib
