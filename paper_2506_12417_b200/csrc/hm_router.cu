@@ -127,11 +127,7 @@ __device__ __forceinline__ void top8_of_32_u32(uint32_t (&key)[32], uint32_t& ni
   merge8_u32(key, n0, key + 16, n2);
   ninth = n0;
 }
-// float -> order-preserving uint32 (-0 folded into +0, as the float compare treats them)
-__device__ __forceinline__ uint32_t ord_u32(float v) {
-  const uint32_t u = __float_as_uint(__fadd_rn(v, 0.0f));
-  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
+// order-preserving uint32 (of a float, -0 folded into +0 as the float compare treats them) -> float
 __device__ __forceinline__ float unord_u32(uint32_t u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
 }
