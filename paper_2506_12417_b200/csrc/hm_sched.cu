@@ -1163,7 +1163,6 @@ __global__ void __launch_bounds__(kPlanThreads)
                    int32_t* __restrict__ loads_out, LayoutOut o) {
   extern __shared__ int s_dyn[];
   __shared__ int s_part[8 * 128];
-  __shared__ int s_tmp[32];
   int* s_m = s_dyn;                 // [E]
   int* s_base = s_m + E;            // [E + 1] expert-major row starts
   int* s_cnt = s_base + E + 1;      // [E + 1] 128-row tiles per segment, plan order
@@ -1178,7 +1177,10 @@ __global__ void __launch_bounds__(kPlanThreads)
     S_out[e] = n;  // S[0, e, 0]
     s_key[e] = plan_key(true, n, e);
   }
-  block_scan_to(s_m, E, s_base, s_tmp);  // s_base[E] = total (ends with __syncthreads)
+  // s_base = exclusive scan of the counts (s_base[E] = total): one warp, then the block barrier
+  // that also publishes the keys
+  if ((tid >> 5) == 0) warp_scan_to(s_m, E, s_base, tid & 31);
+  __syncthreads();
   if (tid == 0) {
     HM_PHASE(2);
     *iters_out = 0;
@@ -1200,7 +1202,7 @@ __global__ void __launch_bounds__(kPlanThreads)
     nseg += __syncthreads_count(key != ~0ull);
   }
   if (tid == 0) *o.n_seg = nseg;
-  block_scan_to(s_cnt, nseg, o.mprefix, s_tmp);
+  if ((tid >> 5) == 0) warp_scan_to(s_cnt, nseg, o.mprefix, tid & 31);
   if (tid == 0) HM_PHASE(3);
 }
 
