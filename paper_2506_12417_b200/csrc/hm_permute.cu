@@ -156,14 +156,25 @@ __global__ void __launch_bounds__(kPermWarps * 32)
 // Dense combine: Y is token-major [T*k, d] (the FFN2 epilogue scattered its rows there),
 // so token t's k rows are one contiguous k*d*2-byte block.  One warp per token; for every
 // 16-byte column chunk the k row loads are issued back to back (KT unrolled).
+#ifndef HM_COMBINE_WARPS
+#define HM_COMBINE_WARPS kPermWarps
+#define HM_COMBINE_MINB 1
+#else
+#ifndef HM_COMBINE_MINB
+#define HM_COMBINE_MINB (44 / HM_COMBINE_WARPS)  // <= 46 registers: a warp fits on an SMSP beside 3 GEMM warps
+#endif
+#define HM_COMBINE_CORUN 1
+#endif
+constexpr int kCombWarps = HM_COMBINE_WARPS;
+
 template <int KT>
-__global__ void __launch_bounds__(kPermWarps * 32)
+__global__ void __launch_bounds__(kCombWarps * 32, HM_COMBINE_MINB)
     combine_dense_kernel(const uint4* __restrict__ Y, const float* __restrict__ w, int64_t T, int k, int n16,
                          const uint4* __restrict__ residual, uint4* __restrict__ y, int parts) {
   // warp (t, part): token t's 16-byte column chunks [part*32, ...) step 32*parts.  parts > 1 for
   // small batches, so enough warps are in flight to cover DRAM latency
   const int lane = threadIdx.x & 31;
-  const int64_t wg = (int64_t)blockIdx.x * kPermWarps + (threadIdx.x >> 5);
+  const int64_t wg = (int64_t)blockIdx.x * kCombWarps + (threadIdx.x >> 5);
   const int64_t t = wg / parts;
   const int part = (int)(wg - t * parts);
   if (t >= T) return;
@@ -254,14 +265,23 @@ int launch_combine(const void* Y, const int32_t* pos, const float* topk_w, int T
   // dense layout: split each token's columns over up to n16/32 warps until ~16K warps are in flight
   int parts = 1;
   while (parts * 2 <= (n16 + 31) / 32 && (int64_t)T * parts * 2 <= 16384) parts *= 2;
-  const unsigned grid_d = (unsigned)(((int64_t)T * parts + kPermWarps - 1) / kPermWarps);
+  const unsigned grid_d = (unsigned)(((int64_t)T * parts + kCombWarps - 1) / kCombWarps);
   auto* Ys = reinterpret_cast<const uint4*>(Y);
   auto* o = reinterpret_cast<uint4*>(y);
   auto* res = reinterpret_cast<const uint4*>(residual);
   if (pos == nullptr) {
     if (k > 16) return set_error(HM_EINVAL, "combine: dense layout needs k <= 16");
-#define HM_DENSE(KT) \
-  combine_dense_kernel<KT><<<grid_d, kPermWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, res, o, parts)
+#ifdef HM_COMBINE_CORUN
+#define HM_DENSE_ATTR(KT) \
+  cudaFuncSetAttribute(combine_dense_kernel<KT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#else
+#define HM_DENSE_ATTR(KT)
+#endif
+#define HM_DENSE(KT)                                                                                  \
+  do {                                                                                                \
+    HM_DENSE_ATTR(KT)                                                                                 \
+    combine_dense_kernel<KT><<<grid_d, kCombWarps * 32, 0, stream>>>(Ys, topk_w, T, k, n16, res, o, parts); \
+  } while (0)
     if (k == 1) HM_DENSE(1);
     else if (k == 2) HM_DENSE(2);
     else if (k == 4) HM_DENSE(4);
